@@ -181,7 +181,7 @@ typedef enum lk_stage {
     LK_STAGE_COUNT = 22
 } lk_stage;
 
-typedef struct lk_edge {   /* lanekit::EdgePixel (preprocess.hpp:94-97) */
+typedef struct lk_edge {   /* lanekit::EdgePixel (preprocess.hpp:92-95) */
     int32_t u, v;
     double gx, gy, theta;
 } lk_edge;
@@ -190,7 +190,7 @@ typedef struct lk_vote {   /* lanekit::SparseVpxMap::Vote (vanish.hpp:35-38) */
     int32_t u_e, v_e, col;
 } lk_vote;
 
-typedef struct lk_lane {   /* lanekit::Lane (lanes.hpp:138-142) minus the polyline */
+typedef struct lk_lane {   /* lanekit::Lane (lanes.hpp:131-135) minus the polyline */
     int32_t bottom_col;
     int32_t n_points;      /* non-NaN rows of the track = polyline length */
     double energy;
@@ -244,6 +244,14 @@ lk_status lk_stage_times(lk_ctx* ctx, float ms[13]);
 
 /* Number of kernel launches one lk_run_batch / lk_enqueue issues. */
 int lk_launches_per_batch(lk_ctx* ctx);
+
+/* Page-locked host buffers for host-fed (end-to-end) runs. */
+lk_status lk_host_alloc(void** ptr, size_t bytes);
+lk_status lk_host_free(void* ptr);
+
+/* sizeof of lk_config, lk_frame_report, lk_scene_params, lk_edge, lk_vote,
+ * lk_lane (in that order) — lets bindings verify their struct layouts. */
+void lk_abi_sizes(size_t out[6]);
 
 /* ---- synthetic input generator: restates lanekit::gen_scene (synth.hpp:103-200)
  * and extends it with obstacles and a pitch change (stress config). Output is

@@ -1,0 +1,637 @@
+// lk_api.cu — host side of the C-ABI (include/lanekit_b200.h): context,
+// device buffers, host-built exact tables, CUDA-graph replay, hooks.
+//
+// Host code here is compiled with -ffp-contract=off so the tables it builds
+// with glibc's exp (the same libm the reference links) are bit-identical to
+// what the reference computes inline (preprocess.hpp:47-50).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/lanekit_b200.h"
+#include "lk_kernels.h"
+
+using lkg::Dev;
+using lkg::FrameAux;
+using lkg::LaunchPlan;
+
+namespace {
+
+thread_local std::string g_err;
+
+lk_status fail(lk_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define CU(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(LK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+const char* kStageNames[12] = {
+    "block statistics", "left disparity",      "right disparity",
+    "consistency check", "v-disparity accumulation", "road path extraction",
+    "road profile fit",  "road mask",           "bilateral smoothing",
+    "edge detection",    "vanishing point estimation", "lane detection",
+};  // pipeline.hpp:101-116
+
+// config.hpp:124-152 (same checks, same messages)
+const char* config_problem(const lk_config& c) {
+    if (c.rho < 1) return "rho must be >= 1";
+    if (c.tau < 0) return "tau must be >= 0";
+    if (c.d_max < 1) return "d_max must be >= 1";
+    if (c.tr_lrc < 0) return "tr_lrc must be >= 0";
+    if (!(c.sigma_floor > 0)) return "sigma_floor must be > 0";
+    if (c.lambda_y < 0) return "lambda_y must be >= 0";
+    if (!(c.tr_y > 0)) return "tr_y must be > 0";
+    if (!(c.eps_y > 0 && c.eps_y <= 1)) return "eps_y must be in (0, 1]";
+    if (c.varpi < 0) return "varpi must be >= 0";
+    if (!(c.sigma_s > 0)) return "sigma_s must be > 0";
+    if (!(c.sigma_r > 0)) return "sigma_r must be > 0";
+    if (c.bf_window < 1 || c.bf_window % 2 == 0) return "bf_window must be odd and >= 1";
+    if (c.sobel_threshold < 0) return "sobel_threshold must be >= 0";
+    if (c.chi < 0) return "chi must be >= 0";
+    if (!(c.rho_vote > 0)) return "rho_vote must be > 0";
+    if (c.lambda_x < 0) return "lambda_x must be >= 0";
+    if (!(c.tr_x > 0)) return "tr_x must be > 0";
+    if (!(c.eps_x > 0 && c.eps_x <= 1)) return "eps_x must be in (0, 1]";
+    if (!(c.sigma_g > 0)) return "sigma_g must be > 0";
+    if (c.nu < 0) return "nu must be >= 0";
+    if (c.varsigma < 0) return "varsigma must be >= 0";
+    if (c.lambda_g < 0) return "lambda_g must be >= 0";
+    if (c.xi < 0) return "xi must be >= 0";
+    if (!std::isnan(c.tr_lpv) && !(c.tr_lpv < 0)) return "tr_lpv must be negative (or auto)";
+    if (c.min_lane_sep < 0) return "min_lane_sep must be >= 0";
+    if (c.threads < 1) return "threads must be >= 1";
+    return nullptr;
+}
+
+constexpr int kMaxIter = 200;  // pipeline.hpp:198, 244
+
+}  // namespace
+
+struct lk_ctx {
+    int device = 0;
+    uint32_t flags = 0;
+    int max_batch = 0;
+    lk_config cfg{};
+    Dev d{};
+    LaunchPlan lp{};
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[13] = {};
+    bool timed = false;
+    std::vector<void*> allocs;
+    std::map<int, cudaGraphExec_t> graphs;
+    uint8_t* in_grey = nullptr;
+    uint8_t* in_disp = nullptr;
+    int last_n = 0;
+
+    template <typename T>
+    lk_status alloc(T** p, size_t count) {
+        void* q = nullptr;
+        const size_t bytes = count * sizeof(T);
+        if (bytes) {
+            cudaError_t e = cudaMalloc(&q, bytes);
+            if (e != cudaSuccess)
+                return fail(LK_ERR_CUDA, "cudaMalloc(" + std::to_string(bytes) +
+                                             " B): " + cudaGetErrorString(e));
+            allocs.push_back(q);
+        }
+        *p = static_cast<T*>(q);
+        return LK_OK;
+    }
+};
+
+extern "C" {
+
+int lk_abi_version(void) { return LK_ABI_VERSION; }
+
+const char* lk_last_error(void) { return g_err.c_str(); }
+
+const char* lk_stage_name(int stage) {
+    return (stage >= 1 && stage <= 12) ? kStageNames[stage - 1] : "";
+}
+
+void lk_config_default(lk_config* c) {  // config.hpp:16-46
+    std::memset(c, 0, sizeof *c);
+    c->rho = 3;
+    c->tau = 1;
+    c->d_max = 64;
+    c->tr_lrc = 3;
+    c->sigma_floor = 1e-4;
+    c->lambda_y = 30.0;
+    c->tr_y = 4.0;
+    c->eps_y = 0.99;
+    c->varpi = 3.0;
+    c->sigma_s = 300.0;
+    c->sigma_r = 0.3;
+    c->bf_window = 11;
+    c->sobel_threshold = 100.0;
+    c->chi = 25;
+    c->rho_vote = 1.0;
+    c->lambda_x = 10.0;
+    c->tr_x = 16.0;
+    c->eps_x = 0.99;
+    c->sigma_g = 3.5;
+    c->nu = 1;
+    c->varsigma = 3;
+    c->lambda_g = 1.0;
+    c->xi = 0.5;
+    c->tr_lpv = std::numeric_limits<double>::quiet_NaN();
+    c->min_lane_sep = 20;
+    c->rng_seed = 1;
+    c->paper_sign = 0;
+    c->threads = 1;
+}
+
+lk_status lk_validate_config(const lk_config* c) {
+    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null config");
+    if (const char* m = config_problem(*c)) return fail(LK_ERR_CONFIG, std::string("config: ") + m);
+    return LK_OK;
+}
+
+lk_status lk_frame_message(const lk_frame_report* rep, char* buf, size_t len) {
+    if (!rep || !buf || !len) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    static const char* texts[] = {
+        "",
+        "empty input image",
+        "v-disparity histogram is empty; no road surface evidence",
+        "ransac: fewer points than the sample size",
+        "ransac: no sample produced a fit",
+        "road profile: singular V_py derivative at row ",
+        "sobel: image smaller than the kernel",
+        "vanishing-point accumulator is empty; no lane edge evidence",
+        "m1: image smaller than the kernel",
+        "stereo pair dimensions differ",
+    };
+    if (rep->status == 0) {
+        buf[0] = 0;
+        return LK_OK;
+    }
+    const int st = (int)rep->failed_stage, m = (int)rep->msg;
+    std::string text = (m >= 0 && m <= 9) ? texts[m] : "unknown failure";
+    if (m == LK_MSG_SINGULAR_VPY) text += std::to_string(rep->err_row);
+    std::snprintf(buf, len, "stage %d (%s): %s", st, lk_stage_name(st), text.c_str());
+    return LK_OK;
+}
+
+lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, int height,
+                    int max_batch, uint32_t flags) {
+    if (!out || !cfg) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (lk_status s = lk_validate_config(cfg)) return s;
+    if (width <= 0 || height <= 0)
+        return fail(LK_ERR_INVALID_ARGUMENT, "stage 1 (block statistics): empty input image");
+    if (width > 65535 || height > 32767)
+        return fail(LK_ERR_INVALID_ARGUMENT, "frame dimensions exceed 65535 x 32767");
+    if (max_batch < 1) return fail(LK_ERR_INVALID_ARGUMENT, "max_batch must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(LK_ERR_NO_DEVICE, "no CUDA device visible");
+    if (device < 0 || device >= ndev) return fail(LK_ERR_NO_DEVICE, "device index out of range");
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return fail(LK_ERR_NO_DEVICE, std::string("lanekit_b200 needs sm_100 (Blackwell); got ") +
+                                          prop.name);
+    CU(cudaSetDevice(device));
+
+    auto* c = new lk_ctx();
+    c->device = device;
+    c->flags = flags;
+    c->max_batch = max_batch;
+    c->cfg = *cfg;
+    Dev& d = c->d;
+    const int W = width, H = height, B = max_batch;
+    d.W = W;
+    d.H = H;
+    d.d_max = cfg->d_max;
+    d.D1 = cfg->d_max + 1;
+    d.px = (size_t)W * H;
+    d.ext_lo = -(int)std::llround(cfg->xi * W);          // vanish.hpp:24-26
+    d.ext_cols = (int)std::llround((2 * cfg->xi + 1) * W);  // vanish.hpp:28-30
+    d.rho = (cfg->bf_window - 1) / 2;                     // pipeline.hpp:220
+    d.win = 2 * d.rho + 1;
+    d.words_per_row = (W + 31) / 32;
+    d.hooks = (flags & LK_FLAG_HOOKS) ? 1 : 0;
+    d.lambda_y = cfg->lambda_y;
+    d.tr_y = cfg->tr_y;
+    d.eps_y = cfg->eps_y;
+    d.varpi = cfg->varpi;
+    d.rho_vote = cfg->rho_vote;
+    d.lambda_x = cfg->lambda_x;
+    d.tr_x = cfg->tr_x;
+    d.eps_x = cfg->eps_x;
+    d.sigma_g = cfg->sigma_g;
+    d.lambda_g = cfg->lambda_g;
+    d.tr_lpv = cfg->tr_lpv;
+    d.chi = cfg->chi;
+    d.nu = cfg->nu;
+    d.varsigma = cfg->varsigma;
+    d.min_lane_sep = cfg->min_lane_sep;
+    d.paper_sign = cfg->paper_sign ? 1 : 0;
+    d.max_iter = kMaxIter;
+    if (d.ext_cols < 1) {
+        delete c;
+        return fail(LK_ERR_CONFIG, "extended column axis is empty");
+    }
+    const int C = d.ext_cols, D1 = d.D1;
+
+    // ---- exact host tables (glibc exp, as the reference evaluates them)
+    const int win = d.win, rho = d.rho;
+    std::vector<double> ws((size_t)win * win), wr(256 * 256), val(256);
+    const double inv_s2 = 1.0 / (cfg->sigma_s * cfg->sigma_s);  // preprocess.hpp:36-37
+    const double inv_r2 = 1.0 / (cfg->sigma_r * cfg->sigma_r);
+    for (int dj = -rho; dj <= rho; ++dj)
+        for (int di = -rho; di <= rho; ++di) {
+            const double ds = static_cast<double>(di) * di + static_cast<double>(dj) * dj;
+            ws[(size_t)(dj + rho) * win + (di + rho)] = std::exp(-ds * inv_s2);
+        }
+    for (int k = 0; k < 256; ++k) val[k] = k / 255.0;  // image_io.hpp:147
+    for (int kc = 0; kc < 256; ++kc)
+        for (int kv = 0; kv < 256; ++kv) {
+            const double dr = val[kv] - val[kc];
+            wr[kc * 256 + kv] = std::exp(-dr * dr * inv_r2);
+        }
+    // smallest s with !(sqrt(s) < t): the edge test of preprocess.hpp:109
+    // made sqrt-free and exact (sqrt is correctly rounded and monotone)
+    {
+        const double t = cfg->sobel_threshold / 255.0;
+        auto pass = [&](double s) { return !(std::sqrt(s) < t); };
+        uint64_t lo = 0, hi = 0x7ff0000000000000ULL;  // +0 .. +inf
+        if (pass(0.0)) {
+            d.sobel_s_star = 0.0;
+        } else {
+            while (hi - lo > 1) {
+                const uint64_t mid = lo + (hi - lo) / 2;
+                double m;
+                std::memcpy(&m, &mid, 8);
+                if (pass(m))
+                    hi = mid;
+                else
+                    lo = mid;
+            }
+            std::memcpy(&d.sobel_s_star, &hi, 8);
+        }
+    }
+    std::vector<uint64_t> rng((size_t)kMaxIter * 5);
+    {
+        std::mt19937_64 eng(cfg->rng_seed);  // ransac.hpp:44
+        for (auto& x : rng) x = eng();
+    }
+
+    lk_status s = LK_OK;
+    auto A = [&](auto** p, size_t n) {
+        if (s == LK_OK) s = c->alloc(p, n);
+    };
+    double *d_ws, *d_wr, *d_val;
+    uint64_t* d_rng;
+    A(&d_ws, ws.size());
+    A(&d_wr, wr.size());
+    A(&d_val, val.size());
+    A(&d_rng, rng.size());
+    A(&c->in_grey, (size_t)B * d.px);
+    A(&c->in_disp, (size_t)B * d.px);
+    A(&d.rep, (size_t)B);
+    A(&d.aux, (size_t)B);
+    A(&d.vhist, (size_t)B * H * D1);
+    A(&c->lp.vhistT, (size_t)B * H * D1);
+    A(&d.vpath, (size_t)B * D1 * 2);
+    A(&d.beta_inl, (size_t)B * D1 * 2);
+    A(&d.vpy, (size_t)B * H);
+    A(&d.vsing, (size_t)B * H);
+    A(&d.fv, (size_t)B * H);
+    A(&d.vpx, (size_t)B * H);
+    A(&d.smoothed, (size_t)B * d.px);
+    A(&d.ebits, (size_t)B * H * d.words_per_row);
+    A(&d.row_cnt, (size_t)B * H);
+    A(&d.row_off, (size_t)B * (H + 1));
+    A(&d.e_uv, (size_t)B * d.px);
+    A(&d.e_gx, (size_t)B * d.px);
+    A(&d.e_gy, (size_t)B * d.px);
+    A(&d.e_th, (size_t)B * d.px);
+    A(&d.e_wg, (size_t)B * d.px);
+    A(&d.e_col, (size_t)B * d.px);
+    A(&d.uchoice, (size_t)B * H * C);
+    A(&d.upath, (size_t)B * H * 2);
+    A(&d.gamma_inl, (size_t)B * H * 2);
+    A(&d.m1, (size_t)B * d.px);
+    A(&d.p99hist, (size_t)B * 2048);
+    A(&d.p99cand, (size_t)B * d.px);
+    A(&d.energy, (size_t)B * C);
+    int sort_cap = 1;
+    while (sort_cap < C / 2 + 2) sort_cap <<= 1;
+    d.lane_cap = sort_cap;
+    A(&d.lanes, (size_t)B * d.lane_cap);
+    if (d.hooks) {
+        A(&d.mask, (size_t)B * d.px);
+        A(&d.gx, (size_t)B * d.px);
+        A(&d.gy, (size_t)B * d.px);
+        A(&d.mag, (size_t)B * d.px);
+        A(&d.theta, (size_t)B * d.px);
+        A(&d.acc, (size_t)B * H * C);
+        A(&d.m0, (size_t)B * d.px);
+        A(&d.polylines, (size_t)B * d.lane_cap * H);
+    }
+    if (s != LK_OK) {
+        lk_destroy(c);
+        return s;
+    }
+    d.ws = d_ws;
+    d.wr = d_wr;
+    d.val = d_val;
+    d.rng = d_rng;
+    d.grey = c->in_grey;
+    d.disp = c->in_disp;
+    if (!d.hooks) d.vchoice = nullptr;
+
+    // ---- shared-memory plan
+    LaunchPlan& lp = c->lp;
+    const size_t vp_base = (size_t)2 * H * 8;
+    lp.vpath_choice_smem = vp_base + (size_t)D1 * H <= 160 * 1024;
+    lp.vpath_smem = vp_base + (lp.vpath_choice_smem ? (size_t)D1 * H : 0);
+    if (!lp.vpath_choice_smem) A(&d.vchoice, (size_t)B * D1 * H);
+    lp.road_smem = (size_t)(5 * D1 + 2) * 4 + (size_t)D1 * 8 + 16;
+    lp.bf_smem = (size_t)(256 + win * win) * 8 +
+                 (size_t)(lkg::BF_TH + 2 * rho) * (lkg::BF_TW + 2 * rho) + 16;
+    lp.vanish_smem = (size_t)2 * C * 8 + (size_t)C * 4 + (size_t)2 * H * 4 +
+                     (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 16;
+    lp.gamma_smem = (size_t)5 * H * 4 + 8 + (size_t)H * 8 + 16;
+    lp.m_tile_h = 16;
+    auto m_bytes = [&](int th) {
+        const size_t GH = th + 2 + 2 * cfg->varsigma, GW = lkg::M_TW + 2 + 2 * cfg->nu;
+        const size_t MH = th + 2, MW = lkg::M_TW + 2;
+        return (GH * GW + MH * MW) * 8 + 2048 * 4;
+    };
+    while (lp.m_tile_h > 1 && m_bytes(lp.m_tile_h) > 96 * 1024) lp.m_tile_h /= 2;
+    lp.m_smem = m_bytes(lp.m_tile_h);
+    lp.collect_blocks = 32;
+    lp.sort_cap = sort_cap;
+    lp.select_smem = (size_t)sort_cap * 12;
+    const size_t smem_cap = prop.sharedMemPerBlockOptin;
+    if (lp.vpath_smem > smem_cap || lp.road_smem > smem_cap || lp.bf_smem > smem_cap ||
+        lp.vanish_smem > smem_cap || lp.gamma_smem > smem_cap || lp.m_smem > smem_cap || lp.select_smem > smem_cap) {
+        lk_destroy(c);
+        return fail(LK_ERR_CONFIG, "frame geometry / window sizes exceed shared memory");
+    }
+    if (s != LK_OK) {
+        lk_destroy(c);
+        return s;
+    }
+    cudaError_t e = lkg::configure_kernels(lp);
+    if (e == cudaSuccess) e = cudaMemcpy(d_ws, ws.data(), ws.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_wr, wr.data(), wr.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_val, val.data(), val.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_rng, rng.data(), rng.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 13 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    if (e != cudaSuccess) {
+        lk_destroy(c);
+        return fail(LK_ERR_CUDA, std::string("context setup: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return LK_OK;
+}
+
+lk_status lk_destroy(lk_ctx* c) {
+    if (!c) return LK_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (cudaEvent_t e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (void* p : c->allocs) cudaFree(p);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return LK_OK;
+}
+
+void* lk_stream(lk_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int lk_launches_per_batch(lk_ctx* c) { return c ? lkg::launches_per_batch(c->d) : 0; }
+
+lk_status lk_device_inputs(lk_ctx* c, uint8_t** grey, uint8_t** disparity) {
+    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
+    if (grey) *grey = c->in_grey;
+    if (disparity) *disparity = c->in_disp;
+    return LK_OK;
+}
+
+static lk_status enqueue_direct(lk_ctx* c, int n, bool timed) {
+    const Dev& d = c->d;
+    CU(cudaMemsetAsync(d.rep, 0, (size_t)n * sizeof(lk_frame_report), c->stream));
+    CU(cudaMemsetAsync(d.aux, 0, (size_t)n * sizeof(FrameAux), c->stream));
+    if (std::isnan(d.tr_lpv))
+        CU(cudaMemsetAsync(d.p99hist, 0, (size_t)n * 2048 * sizeof(unsigned), c->stream));
+    CU(lkg::launch_pipeline(d, c->lp, n, c->stream, timed ? c->ev : nullptr));
+    return LK_OK;
+}
+
+lk_status lk_enqueue(lk_ctx* c, int n) {
+    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
+    if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
+    CU(cudaSetDevice(c->device));
+    c->last_n = n;
+    if (c->flags & LK_FLAG_NO_GRAPH) {
+        c->timed = true;
+        return enqueue_direct(c, n, true);
+    }
+    c->timed = false;
+    auto it = c->graphs.find(n);
+    if (it == c->graphs.end()) {
+        cudaGraph_t g;
+        CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        lk_status s = enqueue_direct(c, n, false);
+        cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        if (s != LK_OK) return s;
+        if (e != cudaSuccess) return fail(LK_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        cudaGraphExec_t ex;
+        e = cudaGraphInstantiate(&ex, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(LK_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        it = c->graphs.emplace(n, ex).first;
+    }
+    CU(cudaGraphLaunch(it->second, c->stream));
+    return LK_OK;
+}
+
+lk_status lk_synchronize(lk_ctx* c) {
+    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
+    CU(cudaStreamSynchronize(c->stream));
+    return LK_OK;
+}
+
+lk_status lk_fetch_reports(lk_ctx* c, lk_frame_report* reports, int n) {
+    if (!c || !reports) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
+    CU(cudaMemcpyAsync(reports, c->d.rep, (size_t)n * sizeof(lk_frame_report),
+                       cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    bool any = false;
+    for (int i = 0; i < n; ++i) {
+        reports[i].rng_seed = c->cfg.rng_seed;
+        any |= reports[i].status != 0;
+    }
+    return any ? LK_ERR_FRAME : LK_OK;
+}
+
+lk_status lk_run_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* disparity, int n,
+                       lk_mem where, lk_frame_report* reports) {
+    if (!c || !grey || !disparity) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
+    CU(cudaSetDevice(c->device));
+    const size_t bytes = (size_t)n * c->d.px;
+    const cudaMemcpyKind k = where == LK_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (grey != c->in_grey) CU(cudaMemcpyAsync(c->in_grey, grey, bytes, k, c->stream));
+    if (disparity != c->in_disp) CU(cudaMemcpyAsync(c->in_disp, disparity, bytes, k, c->stream));
+    if (lk_status s = lk_enqueue(c, n)) return s;
+    if (reports) return lk_fetch_reports(c, reports, n);
+    CU(cudaStreamSynchronize(c->stream));
+    return LK_OK;
+}
+
+lk_status lk_stage_times(lk_ctx* c, float ms[13]) {
+    if (!c || !ms) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    for (int i = 0; i < 13; ++i) ms[i] = 0.f;
+    if (!c->timed) return fail(LK_ERR_UNAVAILABLE, "stage times need LK_FLAG_NO_GRAPH");
+    CU(cudaStreamSynchronize(c->stream));
+    int prev = 0;
+    for (int st : {5, 6, 7, 8, 9, 10, 11, 12}) {
+        CU(cudaEventElapsedTime(&ms[st], c->ev[prev], c->ev[st]));
+        prev = st;
+    }
+    CU(cudaEventElapsedTime(&ms[0], c->ev[0], c->ev[12]));
+    return LK_OK;
+}
+
+lk_status lk_get_stage(lk_ctx* c, int frame, int stage, void* dst, size_t capacity,
+                       size_t* needed) {
+    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
+    if (frame < 0 || frame >= c->last_n) return fail(LK_ERR_INVALID_ARGUMENT, "frame out of range");
+    if (stage < 0 || stage >= LK_STAGE_COUNT) return fail(LK_ERR_INVALID_ARGUMENT, "unknown stage");
+    CU(cudaSetDevice(c->device));
+    CU(cudaStreamSynchronize(c->stream));
+    const Dev& d = c->d;
+    lk_frame_report rep;
+    CU(cudaMemcpy(&rep, d.rep + frame, sizeof rep, cudaMemcpyDeviceToHost));
+    static const int produced_by[LK_STAGE_COUNT] = {5, 6, 7, 7, 7, 8, 9, 10, 10, 10, 10,
+                                                    10, 11, 11, 11, 11, 11, 12, 12, 12, 12, 12};
+    if (rep.status != 0 && rep.failed_stage <= produced_by[stage])
+        return fail(LK_ERR_UNAVAILABLE, "stage not reached: the frame failed earlier");
+    const bool hook_only = stage == LK_STAGE_MASK || stage == LK_STAGE_GX || stage == LK_STAGE_GY ||
+                           stage == LK_STAGE_MAG || stage == LK_STAGE_THETA ||
+                           stage == LK_STAGE_VPX_ACC || stage == LK_STAGE_M0 ||
+                           stage == LK_STAGE_POLYLINES;
+    if (hook_only && !d.hooks) return fail(LK_ERR_UNAVAILABLE, "hook needs LK_FLAG_HOOKS");
+    const size_t px = d.px, H = d.H, C = d.ext_cols, D1 = d.D1;
+    const size_t rows = (size_t)(d.H - rep.horizon);
+    const size_t f = (size_t)frame;
+    const int n_edges = (int)rep.edge_pixels;
+    std::vector<char> buf;
+    auto grab = [&](const void* src, size_t bytes) -> lk_status {
+        buf.resize(bytes);
+        if (bytes) CU(cudaMemcpy(buf.data(), src, bytes, cudaMemcpyDeviceToHost));
+        return LK_OK;
+    };
+    lk_status s = LK_OK;
+    switch (stage) {
+        case LK_STAGE_VDISPARITY: s = grab(d.vhist + f * H * D1, H * D1 * 4); break;
+        case LK_STAGE_VPATH: s = grab(d.vpath + f * D1 * 2, D1 * 8); break;
+        case LK_STAGE_BETA_INLIERS:
+            s = grab(d.beta_inl + f * D1 * 2, (size_t)rep.beta_inlier_count * 8);
+            break;
+        case LK_STAGE_VPY: s = grab(d.vpy + f * H, H * 8); break;
+        case LK_STAGE_VPY_SINGULAR: s = grab(d.vsing + f * H, H); break;
+        case LK_STAGE_MASK: s = grab(d.mask + f * px, px); break;
+        case LK_STAGE_SMOOTHED: s = grab(d.smoothed + f * px, px * 8); break;
+        case LK_STAGE_GX: s = grab(d.gx + f * px, px * 8); break;
+        case LK_STAGE_GY: s = grab(d.gy + f * px, px * 8); break;
+        case LK_STAGE_MAG: s = grab(d.mag + f * px, px * 8); break;
+        case LK_STAGE_THETA: s = grab(d.theta + f * px, px * 8); break;
+        case LK_STAGE_EDGES:
+        case LK_STAGE_VOTES: {
+            std::vector<int32_t> uv(n_edges), col(n_edges);
+            std::vector<double> gx(n_edges), gy(n_edges), th(n_edges);
+            if (n_edges) {
+                CU(cudaMemcpy(uv.data(), d.e_uv + f * px, n_edges * 4, cudaMemcpyDeviceToHost));
+                CU(cudaMemcpy(col.data(), d.e_col + f * px, n_edges * 4, cudaMemcpyDeviceToHost));
+                CU(cudaMemcpy(gx.data(), d.e_gx + f * px, n_edges * 8, cudaMemcpyDeviceToHost));
+                CU(cudaMemcpy(gy.data(), d.e_gy + f * px, n_edges * 8, cudaMemcpyDeviceToHost));
+                CU(cudaMemcpy(th.data(), d.e_th + f * px, n_edges * 8, cudaMemcpyDeviceToHost));
+            }
+            if (stage == LK_STAGE_EDGES) {
+                std::vector<lk_edge> e(n_edges);
+                for (int i = 0; i < n_edges; ++i)
+                    e[i] = {uv[i] & 0xffff, uv[i] >> 16, gx[i], gy[i], th[i]};
+                buf.assign((char*)e.data(), (char*)e.data() + e.size() * sizeof(lk_edge));
+            } else {
+                std::vector<lk_vote> v;
+                for (int i = 0; i < n_edges; ++i)
+                    if (col[i] != lkg::kSkipCol) v.push_back({uv[i] & 0xffff, uv[i] >> 16, col[i]});
+                buf.assign((char*)v.data(), (char*)v.data() + v.size() * sizeof(lk_vote));
+            }
+            break;
+        }
+        case LK_STAGE_VPX_ACC: s = grab(d.acc + f * H * C, rows * C * 8); break;
+        case LK_STAGE_UPATH: s = grab(d.upath + f * H * 2, rows * 8); break;
+        case LK_STAGE_GAMMA_INLIERS:
+            s = grab(d.gamma_inl + f * H * 2, (size_t)rep.gamma_inlier_count * 8);
+            break;
+        case LK_STAGE_VPX: s = grab(d.vpx + f * H, H * 8); break;
+        case LK_STAGE_M0: s = grab(d.m0 + f * px, px * 8); break;
+        case LK_STAGE_M1: s = grab(d.m1 + f * px, px * 8); break;
+        case LK_STAGE_ENERGY: s = grab(d.energy + f * C, C * 8); break;
+        case LK_STAGE_LANES:
+            s = grab(d.lanes + f * d.lane_cap, (size_t)rep.lane_count * sizeof(lk_lane));
+            break;
+        case LK_STAGE_POLYLINES: {
+            const size_t nl = (size_t)rep.lane_count;
+            buf.resize(nl * rows * 8);
+            for (size_t k = 0; k < nl; ++k)
+                CU(cudaMemcpy(buf.data() + k * rows * 8, d.polylines + (f * d.lane_cap + k) * H,
+                              rows * 8, cudaMemcpyDeviceToHost));
+            break;
+        }
+    }
+    if (s != LK_OK) return s;
+    if (needed) *needed = buf.size();
+    if (dst) {
+        if (capacity < buf.size()) return fail(LK_ERR_INVALID_ARGUMENT, "destination too small");
+        if (!buf.empty()) std::memcpy(dst, buf.data(), buf.size());
+    }
+    return LK_OK;
+}
+
+// Pinned host memory for end-to-end (host-fed) runs.
+lk_status lk_host_alloc(void** p, size_t bytes) {
+    if (!p) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    CU(cudaMallocHost(p, bytes));
+    return LK_OK;
+}
+
+lk_status lk_host_free(void* p) {
+    CU(cudaFreeHost(p));
+    return LK_OK;
+}
+
+// Layout check for bindings: sizes of the ABI structs.
+void lk_abi_sizes(size_t* out) {
+    out[0] = sizeof(lk_config);
+    out[1] = sizeof(lk_frame_report);
+    out[2] = sizeof(lk_scene_params);
+    out[3] = sizeof(lk_edge);
+    out[4] = sizeof(lk_vote);
+    out[5] = sizeof(lk_lane);
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+// lk_device.cuh — device-side layout and exact-arithmetic helpers shared by
+// the stage kernels. Every translation unit is compiled with --fmad=false so
+// each double + and * rounds exactly like the reference's SSE2 build
+// (no -march, no FMA contraction: reference proj/CMakeLists.txt:8-10).
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/lanekit_b200.h"
+
+namespace lkg {
+
+constexpr double kPi = 3.14159265358979323846;  // common.hpp:11
+constexpr int kSkipCol = INT32_MIN;              // edge without a vote (vanish.hpp:59-62)
+
+// Per-frame scratch scalars that are not part of the public report.
+struct FrameAux {
+    unsigned long long hist_total;  // pixels counted by the v-disparity (evidence)
+    unsigned long long mask_px;
+    unsigned long long edge_px;
+    unsigned long long votes;
+    unsigned long long skipped;
+    unsigned int p99_cands;         // candidates in the p99 exponent bucket
+    unsigned int p99_bucket;
+    unsigned long long p99_rank;    // rank of the percentile inside the bucket
+    double tr;                      // tr_lpv used
+    int lanes;                      // kept lanes
+    int pad;
+};
+
+// Everything a kernel needs, passed by value. Pointers index frame-major
+// buffers sized for the context's max_batch.
+struct Dev {
+    // geometry
+    int W, H, D1, d_max, ext_lo, ext_cols, rho, win, words_per_row;
+    int lane_cap;
+    int hooks;
+    size_t px;  // W*H
+    // config (config.hpp:16-46)
+    double lambda_y, tr_y, eps_y, varpi, rho_vote, lambda_x, tr_x, eps_x, sigma_g, lambda_g,
+        tr_lpv;
+    int chi, nu, varsigma, min_lane_sep, paper_sign, max_iter;
+    double sobel_s_star;  // smallest s with !(sqrt(s) < threshold): exact sqrt-free test
+    // inputs
+    const uint8_t* grey;
+    const uint8_t* disp;
+    // tables built on the host with the reference's libm
+    const double* ws;       // [win*win] exp(-ds*inv_s2)
+    const double* wr;       // [256][256] exp(-dr*dr*inv_r2)
+    const double* val;      // [256] k/255.0
+    const uint64_t* rng;    // mt19937_64(seed) outputs 0..max_iter*5-1
+    // outputs / intermediates
+    lk_frame_report* rep;
+    FrameAux* aux;
+    int32_t* vhist;         // [B][H][D1]
+    int8_t* vchoice;        // [B][D1][H]
+    int32_t* vpath;         // [B][D1][2]
+    int32_t* beta_inl;      // [B][D1][2]
+    double* vpy;            // [B][H]
+    uint8_t* vsing;         // [B][H]
+    double* fv;             // [B][H]
+    double* vpx;            // [B][H]
+    double* smoothed;       // [B][H][W]
+    uint32_t* ebits;        // [B][H][words_per_row]
+    int32_t* row_cnt;       // [B][H]
+    int32_t* row_off;       // [B][H+1]
+    int32_t* e_uv;          // [B][px]  u | v << 16
+    double* e_gx;           // [B][px]
+    double* e_gy;
+    double* e_th;
+    double* e_wg;
+    int32_t* e_col;         // [B][px]  vote column or kSkipCol
+    int8_t* uchoice;        // [B][H][ext_cols]
+    int32_t* upath;         // [B][H][2]
+    int32_t* gamma_inl;     // [B][H][2]
+    double* m1;             // [B][H][W]
+    unsigned int* p99hist;  // [B][2048]
+    unsigned long long* p99cand;  // [B][px]
+    double* energy;         // [B][ext_cols]
+    lk_lane* lanes;         // [B][lane_cap]
+    double* polylines;      // [B][lane_cap][H] (hooks)
+    // hooks (LK_FLAG_HOOKS)
+    uint8_t* mask;
+    double* gx;
+    double* gy;
+    double* mag;
+    double* theta;
+    double* acc;            // [B][H][ext_cols] rows from horizon
+    double* m0;
+};
+
+// std::llround as glibc/x86-64 behaves: round half away from zero; NaN and
+// |x| >= 2^63 give LLONG_MIN (cvttsd2si "integer indefinite").
+__device__ __forceinline__ long long llround_ref(double x) {
+    if (!(fabs(x) < 9223372036854775808.0)) return (long long)0x8000000000000000ULL;
+    return llround(x);
+}
+
+// common.hpp:28-35
+__device__ __forceinline__ int mirror(int i, int n) {
+    if (n <= 1) return 0;
+    while (i < 0 || i >= n) {
+        if (i < 0) i = -i - 1;
+        if (i >= n) i = 2 * n - 1 - i;
+    }
+    return i;
+}
+
+__device__ __forceinline__ bool frame_failed(const Dev& d, int f) {
+    return d.rep[f].status != 0;
+}
+
+__device__ __forceinline__ void fail_frame(const Dev& d, int f, int stage, int msg, int row = 0) {
+    lk_frame_report& r = d.rep[f];
+    r.status = LK_ERR_FRAME;
+    r.failed_stage = stage;
+    r.msg = msg;
+    r.err_row = row;
+}
+
+__device__ __forceinline__ double* align8(void* p) {
+    return (double*)(((uintptr_t)p + 7) & ~(uintptr_t)7);
+}
+
+// Ordered double -> u64 key (total order equal to '<' for non-NaN values).
+__device__ __forceinline__ unsigned long long order_key(double x) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+}  // namespace lkg

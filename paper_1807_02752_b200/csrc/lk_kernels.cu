@@ -1,0 +1,1184 @@
+// lk_kernels.cu — sm_100a kernels for lanekit stages 5-12.
+//
+// Built with --fmad=false: every double + - * / rounds exactly as the
+// reference's SSE2 build does, so FP-derived integer decisions (mask, edges,
+// votes, DP paths, RANSAC sets, lane columns) are reproduced bit for bit.
+// Transcendentals: the bilateral's exp factors come from host-built glibc
+// tables (exact); atan2 (Sobel theta, w_g ray) and exp (w_g) use CUDA's
+// libdevice (<= 2 ulp from glibc, covered by the parity tolerance).
+#include <cuda_runtime.h>
+
+#include "lk_fit.cuh"
+#include "lk_kernels.h"
+
+namespace lkg {
+
+// =====================================================================
+// K1  build_vdisparity (road_profile.hpp:32-45) + valid-disparity count.
+// grid (ceil(H/K1_ROWS), n), 256 threads. Warp-aggregated shared atomics:
+// lanes holding the same (row, d) key add once via __match_any_sync.
+// Also writes the transposed histogram [D1][H] the v-path DP reads.
+// =====================================================================
+
+__global__ void __launch_bounds__(256) k_vdisparity(Dev d, int32_t* vhistT) {
+    extern __shared__ int32_t sh_hist[];  // [K1_ROWS][D1]
+    const int f = blockIdx.y;
+    const int v0 = blockIdx.x * K1_ROWS;
+    const int rows = min(K1_ROWS, d.H - v0);
+    const int D1 = d.D1;
+    for (int i = threadIdx.x; i < K1_ROWS * D1; i += blockDim.x) sh_hist[i] = 0;
+    __syncthreads();
+    const uint8_t* disp = d.disp + (size_t)f * d.px + (size_t)v0 * d.W;
+    const int npx = rows * d.W;
+    unsigned long long valid = 0, counted = 0;
+    for (int base = 0; base < npx; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        int key = -1;
+        if (i < npx) {
+            const int dv = disp[i];
+            valid += dv != 0;
+            if (dv >= 1 && dv <= d.d_max) key = (i / d.W) * D1 + dv;
+        }
+        const unsigned active = __ballot_sync(0xffffffffu, key >= 0);
+        if (key >= 0) {
+            const unsigned grp = __match_any_sync(active, key);
+            if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&sh_hist[key], __popc(grp));
+            counted += 1;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        valid += __shfl_xor_sync(0xffffffffu, valid, o);
+        counted += __shfl_xor_sync(0xffffffffu, counted, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (valid) atomicAdd((unsigned long long*)&d.rep[f].valid_disparities, valid);
+        if (counted) atomicAdd(&d.aux[f].hist_total, counted);
+    }
+    __syncthreads();
+    int32_t* out = d.vhist + ((size_t)f * d.H + v0) * D1;
+    int32_t* outT = vhistT + (size_t)f * D1 * d.H;
+    for (int i = threadIdx.x; i < rows * D1; i += blockDim.x) {
+        out[i] = sh_hist[i];
+        const int r = i / D1, c = i - r * D1;
+        outT[(size_t)c * d.H + v0 + r] = sh_hist[i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        lk_frame_report& rep = d.rep[f];
+        rep.width = d.W;
+        rep.height = d.H;
+    }
+}
+
+// Block-wide (value, index) argmin, first index among equal minima (the
+// terminal scan of dp.hpp:60-62). Returns the index to every thread.
+__device__ int block_argmin(double val, int idx, double* sv, int* si) {
+    for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, val, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ov < val || (ov == val && oi < idx)) {
+            val = ov;
+            idx = oi;
+        }
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        sv[w] = val;
+        si[w] = idx;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        val = threadIdx.x < nw ? sv[threadIdx.x] : __longlong_as_double(0x7ff0000000000000LL);
+        idx = threadIdx.x < nw ? si[threadIdx.x] : 0x7fffffff;
+        for (int o = 16; o; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, val, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+            if (ov < val || (ov == val && oi < idx)) {
+                val = ov;
+                idx = oi;
+            }
+        }
+        if (threadIdx.x == 0) si[0] = idx;
+    }
+    __syncthreads();
+    const int r = si[0];
+    __syncthreads();
+    return r;
+}
+
+// =====================================================================
+// K2a  dp_extract_vpath (road_profile.hpp:54-78) on dp_min_path (dp.hpp:29-73).
+// One CTA per frame; states = rows in parallel, stages = disparities in
+// sequence. Offsets {0..6} are scanned in list order with strict '<', energy
+// order (prev + pen) + data. Choices live in shared memory when they fit.
+// =====================================================================
+__global__ void __launch_bounds__(512) k_vpath(Dev d, const int32_t* vhistT, int choice_in_smem) {
+    extern __shared__ double sh[];
+    const int f = blockIdx.x;
+    if (frame_failed(d, f)) return;
+    const int H = d.H, D1 = d.D1;
+    double* prev = sh;
+    double* cur = sh + H;
+    __shared__ double sv[32];
+    __shared__ int si[32];
+    int8_t* choice = choice_in_smem ? (int8_t*)(sh + 2 * H) : d.vchoice + (size_t)f * D1 * H;
+    const int32_t* hT = vhistT + (size_t)f * D1 * H;
+    double pen[7];
+    for (int o = 0; o < 7; ++o) pen[o] = d.paper_sign ? -d.lambda_y * o : d.lambda_y * o;
+    // stage 0 <-> d = d_max
+    for (int s = threadIdx.x; s < H; s += blockDim.x)
+        prev[s] = -(double)hT[(size_t)d.d_max * H + s];
+    __syncthreads();
+    for (int st = 1; st < D1; ++st) {
+        const int32_t* col = hT + (size_t)(d.d_max - st) * H;
+        for (int s = threadIdx.x; s < H; s += blockDim.x) {
+            double best = __longlong_as_double(0x7ff0000000000000LL);
+            int bo = 0;
+#pragma unroll
+            for (int o = 0; o < 7; ++o) {
+                const int ps = s + o;
+                if (ps >= H) continue;
+                const double e = prev[ps] + pen[o];
+                if (e < best) {
+                    best = e;
+                    bo = o;
+                }
+            }
+            cur[s] = best + -(double)col[s];
+            choice[(size_t)st * H + s] = (int8_t)bo;
+        }
+        __syncthreads();
+        double* t = prev;
+        prev = cur;
+        cur = t;
+    }
+    double mv = __longlong_as_double(0x7ff0000000000000LL);
+    int mi = 0x7fffffff;
+    for (int s = threadIdx.x; s < H; s += blockDim.x)
+        if (prev[s] < mv) {
+            mv = prev[s];
+            mi = s;
+        }
+    const int term = block_argmin(mv, mi, sv, si);
+    if (threadIdx.x == 0) {
+        int32_t* pts = d.vpath + (size_t)f * D1 * 2;
+        int p = term;
+        pts[(D1 - 1) * 2] = d.d_max - (D1 - 1);
+        pts[(D1 - 1) * 2 + 1] = p;
+        for (int st = D1 - 1; st > 0; --st) {
+            p += choice[(size_t)st * H + p];
+            pts[(st - 1) * 2] = d.d_max - (st - 1);
+            pts[(st - 1) * 2 + 1] = p;
+        }
+        lk_frame_report& rep = d.rep[f];
+        rep.vpath_energy = prev[term];
+        const bool ev = d.aux[f].hist_total > 0;
+        rep.vpath_has_evidence = ev;
+        if (!ev) fail_frame(d, f, 6, LK_MSG_NO_ROAD_EVIDENCE);  // pipeline.hpp:189-190
+    }
+}
+
+// =====================================================================
+// K2b  ransac_beta (road_profile.hpp:121-137) + make_road_profile
+// (road_profile.hpp:145-227): horizon, V_py, singular rows, f(v) per row.
+// One CTA (128 threads) per frame; warp 0 runs the RANSAC.
+// =====================================================================
+__global__ void __launch_bounds__(128) k_road_fit(Dev d) {
+    extern __shared__ int sh_i[];
+    const int f = blockIdx.x;
+    if (frame_failed(d, f)) return;
+    const int n = d.D1, H = d.H;
+    int* px = sh_i;
+    int* pv = px + n;
+    int* bA = pv + n;
+    int* bB = bA + n;
+    int* bC = bB + n;
+    double* tbuf = align8(bC + n);
+    __shared__ RansacState st;
+    __shared__ int s_bad_row;
+    const int32_t* pts = d.vpath + (size_t)f * n * 2;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        px[i] = pts[2 * i];
+        pv[i] = pts[2 * i + 1];
+    }
+    if (threadIdx.x == 0) s_bad_row = 0x7fffffff;
+    __syncthreads();
+    if (threadIdx.x < 32)
+        warp_ransac<3>(px, pv, n, d.tr_y, d.eps_y, d.max_iter, d.rng, bA, bB, bC, tbuf, st);
+    __syncthreads();
+    lk_frame_report& rep = d.rep[f];
+    if (st.msg) {
+        if (threadIdx.x == 0) {
+            rep.beta_iterations = st.iterations;
+            fail_frame(d, f, 7, st.msg);
+        }
+        return;
+    }
+    const double b0 = st.model[0], b1 = st.model[1], b2 = st.model[2];
+    // horizon_row (road_profile.hpp:161-176)
+    int horizon = 0;
+    bool in_range = true;
+    {
+        double root = 0;
+        bool ok = true;
+        if (b2 == 0) {
+            if (b1 <= 0)
+                ok = false;
+            else
+                root = -b0 / b1;
+        } else {
+            const double disc = b1 * b1 - 4 * b2 * b0;
+            if (disc <= 0)
+                ok = false;
+            else
+                root = (-b1 + sqrt(disc)) / (2 * b2);
+        }
+        if (ok) {
+            const long long r = llround_ref(root);
+            if (r < 0 || r >= H)
+                ok = false;
+            else
+                horizon = (int)r;
+        }
+        if (!ok) {
+            horizon = 0;
+            in_range = false;
+        }
+    }
+    // vpy_profile (road_profile.hpp:184-199) and road_f per row
+    int bad = 0x7fffffff;
+    for (int v = threadIdx.x; v < H; v += blockDim.x) {
+        const double vv = (double)v;
+        const double fp = b1 + 2 * b2 * vv;
+        const double fvv = b0 + b1 * vv + b2 * vv * vv;
+        uint8_t sing = 0;
+        double vpy;
+        if (fabs(fp) < 1e-12) {
+            sing = 1;
+            vpy = vv;
+            if (v >= horizon) bad = min(bad, v);
+        } else {
+            vpy = vv - fvv / fp;
+        }
+        d.vpy[(size_t)f * H + v] = vpy;
+        d.vsing[(size_t)f * H + v] = sing;
+        d.fv[(size_t)f * H + v] = fvv;
+    }
+    if (bad != 0x7fffffff) atomicMin(&s_bad_row, bad);
+    for (int i = threadIdx.x; i < st.n_inl; i += blockDim.x) {
+        const int id = st.inl[i];
+        d.beta_inl[((size_t)f * n + i) * 2] = px[id];
+        d.beta_inl[((size_t)f * n + i) * 2 + 1] = pv[id];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        rep.beta[0] = b0;
+        rep.beta[1] = b1;
+        rep.beta[2] = b2;
+        rep.beta_iterations = st.iterations;
+        rep.beta_inlier_fraction = st.fraction;
+        rep.beta_degraded = st.degraded;
+        rep.beta_inlier_count = st.n_inl;
+        rep.horizon = horizon;
+        rep.horizon_in_range = in_range;
+        if (s_bad_row != 0x7fffffff)  // road_profile.hpp:223-225
+            fail_frame(d, f, 7, LK_MSG_SINGULAR_VPY, s_bad_row);
+    }
+}
+
+// =====================================================================
+// K3a  bilateral_filter (preprocess.hpp:30-59), 8-bit input.
+// w = exp(-ds*inv_s2) * exp(-dr*dr*inv_r2): the first factor depends only on
+// the tap (ws table), the second only on the (centre, neighbour) byte pair
+// (wr table), both tabulated on the host with the reference's libm, so the
+// product and the j-major / i-minor sums are bit-identical. Tile 32x8 with a
+// mirrored halo staged in shared memory.
+// =====================================================================
+
+template <int RHO>
+__global__ void __launch_bounds__(256) k_bilateral(Dev d) {
+    extern __shared__ double sh_bf[];
+    const int rho = RHO >= 0 ? RHO : d.rho;
+    const int win = 2 * rho + 1;
+    const int f = blockIdx.z;
+    if (frame_failed(d, f)) return;
+    const int TWh = BF_TW + 2 * rho, THh = BF_TH + 2 * rho;
+    double* s_val = sh_bf;               // [256]
+    double* s_ws = s_val + 256;          // [win*win]
+    uint8_t* s_px = (uint8_t*)(s_ws + win * win);  // [THh][TWh]
+    const int u0 = blockIdx.x * BF_TW, v0 = blockIdx.y * BF_TH;
+    const uint8_t* g = d.grey + (size_t)f * d.px;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_val[i] = d.val[i];
+    for (int i = threadIdx.x; i < win * win; i += blockDim.x) s_ws[i] = d.ws[i];
+    for (int i = threadIdx.x; i < TWh * THh; i += blockDim.x) {
+        const int ty = i / TWh, tx = i - ty * TWh;
+        const int gu = mirror(u0 + tx - rho, d.W), gv = mirror(v0 + ty - rho, d.H);
+        s_px[i] = g[(size_t)gv * d.W + gu];
+    }
+    __syncthreads();
+    const int tx = threadIdx.x % BF_TW, ty = threadIdx.x / BF_TW;
+    const int u = u0 + tx, v = v0 + ty;
+    if (u >= d.W || v >= d.H) return;
+    const int kc = s_px[(ty + rho) * TWh + tx + rho];
+    const double* __restrict__ wrow = d.wr + kc * 256;
+    double num = 0.0, den = 0.0;
+    if (RHO >= 0) {
+#pragma unroll
+        for (int j = 0; j < 2 * RHO + 1; ++j) {
+            const uint8_t* prow = s_px + (ty + j) * TWh + tx;
+#pragma unroll
+            for (int i = 0; i < 2 * RHO + 1; ++i) {
+                const int kv = prow[i];
+                const double w = s_ws[j * (2 * RHO + 1) + i] * __ldg(wrow + kv);
+                num += w * s_val[kv];
+                den += w;
+            }
+        }
+    } else {
+        for (int j = 0; j < win; ++j) {
+            const uint8_t* prow = s_px + (ty + j) * TWh + tx;
+            for (int i = 0; i < win; ++i) {
+                const int kv = prow[i];
+                const double w = s_ws[j * win + i] * __ldg(wrow + kv);
+                num += w * s_val[kv];
+                den += w;
+            }
+        }
+    }
+    d.smoothed[(size_t)f * d.px + (size_t)v * d.W + u] = num / den;
+}
+
+// Sobel taps on the smoothed image with mirrored borders (preprocess.hpp:71-81).
+__device__ __forceinline__ void sobel_at(const double* img, int W, int H, int u, int v,
+                                         double& gx, double& gy) {
+    const int um = mirror(u - 1, W), up = mirror(u + 1, W), uc = mirror(u, W);
+    const double* rm = img + (size_t)mirror(v - 1, H) * W;
+    const double* rc = img + (size_t)mirror(v, H) * W;
+    const double* rp = img + (size_t)mirror(v + 1, H) * W;
+    gx = (rm[up] - rm[um]) + 2 * (rc[up] - rc[um]) + (rp[up] - rp[um]);
+    gy = (rp[um] - rm[um]) + 2 * (rp[uc] - rm[uc]) + (rp[up] - rm[up]);
+}
+
+// =====================================================================
+// K3b  road_mask (preprocess.hpp:14-26) + sobel_gradients (:67-90) +
+// edge_map test (:103-113). One CTA per (row, frame). The magnitude test
+// !(sqrt(s) < t) is evaluated exactly as s >= s* (s* from the host).
+// Writes an edge bitmap, the row's edge count and mask / edge totals.
+// =====================================================================
+__global__ void __launch_bounds__(256) k_sobel_edges(Dev d) {
+    const int v = blockIdx.x, f = blockIdx.y;
+    if (frame_failed(d, f)) return;
+    if (d.W < 3 || d.H < 3) {  // preprocess.hpp:68-69
+        if (v == 0 && threadIdx.x == 0) fail_frame(d, f, 10, LK_MSG_SOBEL_TOO_SMALL);
+        return;
+    }
+    const int W = d.W;
+    const double* img = d.smoothed + (size_t)f * d.px;
+    const uint8_t* disp = d.disp + (size_t)f * d.px + (size_t)v * W;
+    const int horizon = (int)d.rep[f].horizon;
+    const double fvv = d.fv[(size_t)f * d.H + v];
+    __shared__ int s_cnt[2];
+    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    int n_edge = 0, n_mask = 0;
+    const int lane = threadIdx.x & 31;
+    for (int base = 0; base < W; base += blockDim.x) {
+        const int u = base + threadIdx.x;
+        bool edge = false;
+        if (u < W) {
+            double gx, gy;
+            sobel_at(img, W, d.H, u, v, gx, gy);
+            const double s = gx * gx + gy * gy;
+            const int dv = disp[u];
+            const bool m = v >= horizon && dv != 0 && fabs((double)dv - fvv) <= d.varpi;
+            n_mask += m;
+            edge = m && s >= d.sobel_s_star;
+            n_edge += edge;
+            if (d.hooks) {
+                const size_t i = (size_t)f * d.px + (size_t)v * W + u;
+                d.mask[i] = m;
+                d.gx[i] = gx;
+                d.gy[i] = gy;
+                d.mag[i] = sqrt(s);
+                double th = atan2(gy, gx);
+                if (th <= -kPi) th = kPi;
+                d.theta[i] = th;
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, edge);
+        const int word = (base >> 5) + (threadIdx.x >> 5);
+        if (lane == 0 && word < d.words_per_row)
+            d.ebits[((size_t)f * d.H + v) * d.words_per_row + word] = bal;
+    }
+    for (int o = 16; o; o >>= 1) {
+        n_edge += __shfl_xor_sync(0xffffffffu, n_edge, o);
+        n_mask += __shfl_xor_sync(0xffffffffu, n_mask, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&s_cnt[0], n_edge);
+        atomicAdd(&s_cnt[1], n_mask);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        d.row_cnt[(size_t)f * d.H + v] = s_cnt[0];
+        if (s_cnt[0]) atomicAdd(&d.aux[f].edge_px, (unsigned long long)s_cnt[0]);
+        if (s_cnt[1]) atomicAdd(&d.aux[f].mask_px, (unsigned long long)s_cnt[1]);
+    }
+}
+
+// =====================================================================
+// K3c  edge list in row-major order (edge_map, preprocess.hpp:103-113) +
+// sparse_vpx votes (vanish.hpp:49-70). One CTA per (row, frame): the row's
+// offset is the sum of the earlier rows' counts; edges are emitted in u
+// order by a block-wide ballot scan.
+// =====================================================================
+__global__ void __launch_bounds__(256) k_edge_emit(Dev d) {
+    const int v = blockIdx.x, f = blockIdx.y;
+    if (frame_failed(d, f)) return;
+    const int W = d.W, H = d.H;
+    const int32_t* rc = d.row_cnt + (size_t)f * H;
+    __shared__ int s_warp[8];
+    __shared__ int s_red[2];
+    int part = 0;
+    for (int r = threadIdx.x; r < v; r += blockDim.x) part += rc[r];
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x < 2) s_red[threadIdx.x] = 0;
+    __syncthreads();
+    if (lane == 0) atomicAdd(&s_red[0], part);
+    __syncthreads();
+    const int off = s_red[0];
+    const int cnt = rc[v];
+    if (threadIdx.x == 0) {
+        d.row_off[(size_t)f * (H + 1) + v] = off;
+        if (v == H - 1) d.row_off[(size_t)f * (H + 1) + H] = off + cnt;
+    }
+    if (cnt == 0) return;
+    const double* img = d.smoothed + (size_t)f * d.px;
+    const uint32_t* bits = d.ebits + ((size_t)f * H + v) * d.words_per_row;
+    const double vpy = d.vpy[(size_t)f * H + v];
+    const bool sing = d.vsing[(size_t)f * H + v] != 0;
+    const int ext_hi = d.ext_lo + d.ext_cols - 1;
+    int run = 0, n_vote = 0, n_skip = 0;
+    for (int base = 0; base < W; base += blockDim.x) {
+        const int u = base + threadIdx.x;
+        bool edge = false;
+        if (u < W) edge = (bits[u >> 5] >> (u & 31)) & 1u;
+        const unsigned bal = __ballot_sync(0xffffffffu, edge);
+        if (lane == 0) s_warp[wid] = __popc(bal);
+        __syncthreads();
+        int before = run;
+        for (int w = 0; w < wid; ++w) before += s_warp[w];
+        int total = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += s_warp[w];
+        if (edge) {
+            const size_t e = (size_t)f * d.px + off + before + __popc(bal & ((1u << lane) - 1u));
+            double gx, gy;
+            sobel_at(img, W, H, u, v, gx, gy);
+            double th = atan2(gy, gx);
+            if (th <= -kPi) th = kPi;
+            d.e_uv[e] = u | (v << 16);
+            d.e_gx[e] = gx;
+            d.e_gy[e] = gy;
+            d.e_th[e] = th;
+            int col = kSkipCol;
+            if (!(sing || fabs(gx) < 1e-3)) {  // kGradientFloor, vanish.hpp:20, 59
+                const double c = (double)u + ((double)v - vpy) * (gy / gx);
+                long long cc = llround_ref(c);
+                cc = cc < d.ext_lo ? d.ext_lo : (cc > ext_hi ? ext_hi : cc);
+                col = (int)cc;
+                ++n_vote;
+            } else {
+                ++n_skip;
+            }
+            d.e_col[e] = col;
+        }
+        run += total;
+        __syncthreads();
+    }
+    for (int o = 16; o; o >>= 1) {
+        n_vote += __shfl_xor_sync(0xffffffffu, n_vote, o);
+        n_skip += __shfl_xor_sync(0xffffffffu, n_skip, o);
+    }
+    if (lane == 0) {
+        if (n_vote) atomicAdd(&d.aux[f].votes, (unsigned long long)n_vote);
+        if (n_skip) atomicAdd(&d.aux[f].skipped, (unsigned long long)n_skip);
+    }
+}
+
+// lanes.hpp:20-25
+__device__ __forceinline__ double piecewise_weight(double te, double tv, double sg) {
+    double dd = fmod(fabs(te - tv), kPi);
+    if (dd > kPi / 2) dd = kPi - dd;
+    if (dd > kPi / 6) return 0.0;
+    return exp(-(dd / (sg * sg)) * (36 / kPi));
+}
+
+// =====================================================================
+// K4a accumulate_dense_vpx (vanish.hpp:113-148) + dp_extract_upath
+// (:156-182). One CTA per frame.
+// The banded accumulator is never materialised: per-column band counts slide
+// with the DP stage (exact integer +-1 updates from the per-row vote lists),
+// and each DP stage reads -rho_vote * count directly.
+// =====================================================================
+
+__global__ void __launch_bounds__(K4_THREADS) k_vanish(Dev d) {
+    extern __shared__ double sh4[];
+    const int f = blockIdx.x;
+    if (frame_failed(d, f)) return;
+    const int H = d.H, C = d.ext_cols;
+    lk_frame_report& rep = d.rep[f];
+    const int v_top = (int)rep.horizon, v_max = H - 1;
+    const int nrows = v_max - v_top + 1;
+    double* prev = sh4;
+    double* cur = prev + C;
+    int* cnt = (int*)(cur + C);
+    int* px = cnt + C;
+    int* pv = px + H;
+    int8_t* win = (int8_t*)(pv + H);  // [BT_CHUNK][2*BT_SPAN+1]
+    __shared__ double sv[32];
+    __shared__ int si[32];
+    __shared__ int s_votes;
+    const int32_t* roff = d.row_off + (size_t)f * (H + 1);
+    const int32_t* ecol = d.e_col + (size_t)f * d.px;
+    int8_t* choice = d.uchoice + (size_t)f * H * C;
+    double pen[11];
+    const int offs[11] = {0, -1, 1, -2, 2, -3, 3, -4, 4, -5, 5};
+#pragma unroll
+    for (int o = 0; o < 11; ++o)
+        pen[o] = d.paper_sign ? d.lambda_x * offs[o] : d.lambda_x * abs(offs[o]);
+    for (int c = threadIdx.x; c < C; c += blockDim.x) cnt[c] = 0;
+    if (threadIdx.x == 0) s_votes = 0;
+    __syncthreads();
+    const double nrv = -d.rho_vote;
+    int top_cur = v_max + 1, bot_cur = v_max;
+    int my_votes = 0;
+    for (int stg = 0; stg < nrows; ++stg) {
+        const int v = v_max - stg;
+        int bt, bb;  // vote_band (vanish.hpp:101-105)
+        if (v > v_max - d.chi - 1) {
+            bt = v;
+            bb = v_max;
+        } else if (v >= v_top + d.chi) {
+            bt = v - d.chi;
+            bb = v + d.chi;
+        } else {
+            bt = v_top;
+            bb = v + d.chi;
+        }
+        if (bt < top_cur) {  // rows entering at the top: [bt, top_cur)
+            for (int e = roff[bt] + threadIdx.x; e < roff[top_cur]; e += blockDim.x) {
+                const int c = ecol[e];
+                if (c != kSkipCol) {
+                    atomicAdd(&cnt[c - d.ext_lo], 1);
+                    ++my_votes;
+                }
+            }
+        }
+        top_cur = bt;
+        if (bb < bot_cur) {  // rows leaving at the bottom: (bb, bot_cur]
+            for (int e = roff[bb + 1] + threadIdx.x; e < roff[bot_cur + 1]; e += blockDim.x) {
+                const int c = ecol[e];
+                if (c != kSkipCol) atomicSub(&cnt[c - d.ext_lo], 1);
+            }
+        }
+        bot_cur = bb;
+        __syncthreads();
+        if (d.hooks) {
+            double* arow = d.acc + ((size_t)f * H + (v - v_top)) * C;
+            for (int c = threadIdx.x; c < C; c += blockDim.x) arow[c] = nrv * cnt[c];
+        }
+        if (stg == 0) {
+            for (int c = threadIdx.x; c < C; c += blockDim.x) prev[c] = nrv * cnt[c];
+        } else {
+            int8_t* ch = choice + (size_t)stg * C;
+            for (int s = threadIdx.x; s < C; s += blockDim.x) {
+                double best = __longlong_as_double(0x7ff0000000000000LL);
+                int bo = 0;
+#pragma unroll
+                for (int o = 0; o < 11; ++o) {
+                    const int ps = s + offs[o];
+                    if (ps < 0 || ps >= C) continue;
+                    const double e = prev[ps] + pen[o];
+                    if (e < best) {
+                        best = e;
+                        bo = offs[o];
+                    }
+                }
+                cur[s] = best + nrv * cnt[s];
+                ch[s] = (int8_t)bo;
+            }
+        }
+        __syncthreads();
+        if (stg > 0) {
+            double* t = prev;
+            prev = cur;
+            cur = t;
+        }
+    }
+    for (int o = 16; o; o >>= 1) my_votes += __shfl_xor_sync(0xffffffffu, my_votes, o);
+    if ((threadIdx.x & 31) == 0 && my_votes) atomicAdd(&s_votes, my_votes);
+    double mv = __longlong_as_double(0x7ff0000000000000LL);
+    int mi = 0x7fffffff;
+    for (int s = threadIdx.x; s < C; s += blockDim.x)
+        if (prev[s] < mv) {
+            mv = prev[s];
+            mi = s;
+        }
+    const int term = block_argmin(mv, mi, sv, si);
+    const double energy = prev[term];
+    // backtrack (dp.hpp:67-71) in windows of BT_CHUNK stages staged in smem
+    int p = term;
+    if (threadIdx.x == 0) {
+        px[nrows - 1] = d.ext_lo + p;
+        pv[nrows - 1] = v_max - (nrows - 1);
+    }
+    const int span = 2 * BT_SPAN + 1;
+    for (int hi = nrows - 1; hi > 0; hi -= BT_CHUNK) {
+        const int lo = max(1, hi - BT_CHUNK + 1);  // stages lo..hi are read
+        const int c0 = p - BT_SPAN;
+        __syncthreads();
+        for (int i = threadIdx.x; i < (hi - lo + 1) * span; i += blockDim.x) {
+            const int r = i / span, c = c0 + (i - r * span);
+            win[i] = (c >= 0 && c < C) ? choice[(size_t)(lo + r) * C + c] : 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int stg = hi; stg >= lo; --stg) {
+                p += win[(stg - lo) * span + (p - c0)];
+                px[stg - 1] = d.ext_lo + p;
+                pv[stg - 1] = v_max - (stg - 1);
+            }
+            si[0] = p;
+        }
+        __syncthreads();
+        p = si[0];
+    }
+    __syncthreads();
+    int32_t* up = d.upath + (size_t)f * H * 2;
+    for (int i = threadIdx.x; i < nrows; i += blockDim.x) {
+        up[2 * i] = px[i];
+        up[2 * i + 1] = pv[i];
+    }
+    if (threadIdx.x == 0) {
+        rep.upath_energy = energy;
+        rep.upath_has_evidence = s_votes > 0;
+        if (s_votes == 0) fail_frame(d, f, 11, LK_MSG_NO_EDGE_EVIDENCE);  // pipeline.hpp:238-239
+    }
+}
+
+
+// =====================================================================
+// K4b  ransac_gamma (vanish.hpp:253-270) on the u-path points, vpx_profile
+// (:276-281), then the w_g edge weights of build_m0 (lanes.hpp:35-44).
+// One CTA per frame; warp 0 runs the RANSAC.
+// =====================================================================
+__global__ void __launch_bounds__(256) k_gamma_fit(Dev d) {
+    extern __shared__ int sh_g[];
+    const int f = blockIdx.x;
+    if (frame_failed(d, f)) return;
+    const int H = d.H;
+    lk_frame_report& rep = d.rep[f];
+    const int v_top = (int)rep.horizon, v_max = H - 1;
+    const int nrows = v_max - v_top + 1;
+    int* px = sh_g;
+    int* pv = px + H;
+    int* bA = pv + H;
+    int* bB = bA + H;
+    int* bC = bB + H;
+    double* tbuf = align8(bC + H);
+    __shared__ RansacState st;
+    const int32_t* up = d.upath + (size_t)f * H * 2;
+    for (int i = threadIdx.x; i < nrows; i += blockDim.x) {
+        px[i] = up[2 * i];
+        pv[i] = up[2 * i + 1];
+    }
+    __syncthreads();
+    if (threadIdx.x < 32)
+        warp_ransac<5>(px, pv, nrows, d.tr_x, d.eps_x, d.max_iter, d.rng, bA, bB, bC, tbuf, st);
+    __syncthreads();
+    if (st.msg) {
+        if (threadIdx.x == 0) {
+            rep.gamma_iterations = st.iterations;
+            fail_frame(d, f, 11, st.msg);
+        }
+        return;
+    }
+    const double g0 = st.model[0], g1 = st.model[1], g2 = st.model[2], g3 = st.model[3],
+                 g4 = st.model[4];
+    double* vpx = d.vpx + (size_t)f * H;
+    for (int v = threadIdx.x; v < H; v += blockDim.x) {
+        const double vv = (double)v;
+        vpx[v] = g0 + vv * (g1 + vv * (g2 + vv * (g3 + vv * g4)));
+    }
+    for (int i = threadIdx.x; i < st.n_inl; i += blockDim.x) {
+        const int id = st.inl[i];
+        d.gamma_inl[((size_t)f * H + i) * 2] = px[id];
+        d.gamma_inl[((size_t)f * H + i) * 2 + 1] = pv[id];
+    }
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 5; ++k) rep.gamma[k] = st.model[k];
+        rep.gamma_kappa = 1.0;
+        rep.gamma_v_normalizer = st.s;
+        rep.gamma_iterations = st.iterations;
+        rep.gamma_inlier_fraction = st.fraction;
+        rep.gamma_degraded = st.degraded;
+        rep.gamma_inlier_count = st.n_inl;
+    }
+    __syncthreads();
+    // w_g per edge (lanes.hpp:35-44)
+    const double* vpy = d.vpy + (size_t)f * H;
+    const int n_edges = d.row_off[(size_t)f * (H + 1) + H];
+    const size_t eb = (size_t)f * d.px;
+    for (int e = threadIdx.x; e < n_edges; e += blockDim.x) {
+        const int uv = d.e_uv[eb + e];
+        const int u = uv & 0xffff, v = uv >> 16;
+        double wg = 0.0;
+        if (v >= v_top && v <= v_max) {
+            const double dx = vpx[v] - (double)u;
+            const double dy = vpy[v] - (double)v;
+            if (!(fabs(dx) < 1e-12 && fabs(dy) < 1e-12)) {
+                const double theta_ray = atan2(dy, dx);
+                const double theta_tangent = d.e_th[eb + e] + kPi / 2;
+                wg = d.e_gx[eb + e] * piecewise_weight(theta_tangent, theta_ray, d.sigma_g);
+            }
+        }
+        d.e_wg[eb + e] = wg;
+    }
+}
+
+// =====================================================================
+// K5a  build_m0 (lanes.hpp:46-60) + build_m1 (:67-76) + the exponent
+// histogram of |m1| over the road rows for the auto threshold (:182-193).
+// Tile M_TW x M_TH; w_g scattered from the row-ordered edge list into a
+// zeroed shared tile; the box sum keeps the y-major / x-minor order (adding
+// the zeros the reference adds is exact, so the order is all that matters).
+// =====================================================================
+
+__global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist) {
+    extern __shared__ double sh5[];
+    const int f = blockIdx.z;
+    if (frame_failed(d, f)) return;
+    if (d.W < 3 || d.H < 3) {  // lanes.hpp:68 (stage 10 already rejects this)
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+            fail_frame(d, f, 12, LK_MSG_M1_TOO_SMALL);
+        return;
+    }
+    const int W = d.W, H = d.H, nu = d.nu, vs = d.varsigma;
+    const int u0 = blockIdx.x * M_TW, v0 = blockIdx.y * tile_h;
+    const int v_top = (int)d.rep[f].horizon, v_max = H - 1;
+    // wg region rows [v0-1-vs, v0+tile_h+vs], cols [u0-1-nu, u0+M_TW+nu]
+    const int gr0 = v0 - 1 - vs, gc0 = u0 - 1 - nu;
+    const int GH = tile_h + 2 + 2 * vs, GW = M_TW + 2 + 2 * nu;
+    // m0 region rows [v0-1, v0+tile_h], cols [u0-1, u0+M_TW]
+    const int MH = tile_h + 2, MW = M_TW + 2;
+    double* gw = sh5;
+    double* m0 = gw + GH * GW;
+    unsigned int* hist = (unsigned int*)(m0 + MH * MW);
+    for (int i = threadIdx.x; i < GH * GW; i += blockDim.x) gw[i] = 0.0;
+    if (want_hist)
+        for (int i = threadIdx.x; i < 2048; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const int32_t* roff = d.row_off + (size_t)f * (H + 1);
+    const size_t eb = (size_t)f * d.px;
+    const int r_lo = max(max(gr0, 0), v_top), r_hi = min(gr0 + GH - 1, v_max);
+    if (r_lo <= r_hi) {
+        for (int e = roff[r_lo] + threadIdx.x; e < roff[r_hi + 1]; e += blockDim.x) {
+            const int uv = d.e_uv[eb + e];
+            const int u = uv & 0xffff, v = uv >> 16;
+            if (u >= gc0 && u < gc0 + GW) gw[(v - gr0) * GW + (u - gc0)] = d.e_wg[eb + e];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < MH * MW; i += blockDim.x) {
+        const int r = i / MW, c = i - r * MW;
+        const int v = v0 - 1 + r, u = u0 - 1 + c;
+        double s = 0.0;
+        if (v >= 0 && v < H && u >= 0 && u < W) {
+            for (int y = -vs; y <= vs; ++y) {
+                const int vv = v + y;
+                if (vv < 0 || vv >= H) continue;
+                const double* grow = gw + (vv - gr0) * GW;
+                for (int x = -nu; x <= nu; ++x) {
+                    const int uu = u + x;
+                    if (uu < 0 || uu >= W) continue;
+                    s += grow[uu - gc0];
+                }
+            }
+        }
+        m0[i] = s;
+    }
+    __syncthreads();
+    const int t_lo = max(0, v_top), t_hi = min(H - 1, v_max);
+    for (int i = threadIdx.x; i < tile_h * M_TW; i += blockDim.x) {
+        const int r = i / M_TW, c = i - r * M_TW;
+        const int v = v0 + r, u = u0 + c;
+        if (v >= H || u >= W) continue;
+        double m1 = 0.0;
+        if (v >= 1 && v < H - 1 && u >= 1 && u < W - 1) {
+            const double* a = m0 + r * MW + c;            // row v-1, col u-1
+            const double* b = a + MW;                      // row v
+            const double* cc = b + MW;                     // row v+1
+            m1 = (a[2] - a[0]) + 2 * (b[2] - b[0]) + (cc[2] - cc[0]);
+        }
+        const size_t gi = (size_t)f * d.px + (size_t)v * W + u;
+        d.m1[gi] = m1;
+        if (d.hooks) d.m0[gi] = m0[(r + 1) * MW + c + 1];
+        if (want_hist && v >= t_lo && v <= t_hi)
+            atomicAdd(&hist[(unsigned long long)__double_as_longlong(fabs(m1)) >> 52], 1u);
+    }
+    if (want_hist) {
+        __syncthreads();
+        unsigned int* gh = d.p99hist + (size_t)f * 2048;
+        for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+            if (hist[i]) atomicAdd(&gh[i], hist[i]);
+    }
+}
+
+// =====================================================================
+// auto_lane_threshold (lanes.hpp:182-193): the k-th smallest |m1|,
+// k = floor(0.99*(n-1)), selected EXACTLY on the IEEE bit patterns
+// (non-negative doubles order like their bits): exponent histogram (K5a),
+// bucket pick, candidate gather, then MSB radix select inside the bucket.
+// =====================================================================
+__global__ void __launch_bounds__(256) k_p99_bucket(Dev d) {
+    const int f = blockIdx.x;
+    if (frame_failed(d, f)) return;
+    __shared__ unsigned long long s_part[256];
+    const unsigned int* h = d.p99hist + (size_t)f * 2048;
+    const int v_top = (int)d.rep[f].horizon, v_max = d.H - 1;
+    const int t_lo = max(0, v_top), t_hi = min(d.H - 1, v_max);
+    const unsigned long long n = (unsigned long long)(t_hi - t_lo + 1) * d.W;
+    const unsigned long long k = (unsigned long long)floor(0.99 * (double)(n - 1));
+    // each thread owns 8 consecutive bins
+    unsigned long long mine = 0;
+    for (int b = 0; b < 8; ++b) mine += h[threadIdx.x * 8 + b];
+    s_part[threadIdx.x] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        int t = 0;
+        for (; t < 256; ++t) {
+            if (run + s_part[t] > k) break;
+            run += s_part[t];
+        }
+        int b = t * 8;
+        for (;; ++b) {
+            if (run + h[b] > k) break;
+            run += h[b];
+        }
+        d.aux[f].p99_bucket = b;
+        d.aux[f].p99_rank = k - run;
+        d.aux[f].p99_cands = 0;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_p99_collect(Dev d) {
+    const int f = blockIdx.y;
+    if (frame_failed(d, f)) return;
+    const int v_top = (int)d.rep[f].horizon, v_max = d.H - 1;
+    const int t_lo = max(0, v_top), t_hi = min(d.H - 1, v_max);
+    const size_t n = (size_t)(t_hi - t_lo + 1) * d.W;
+    const unsigned bucket = d.aux[f].p99_bucket;
+    const double* m1 = d.m1 + (size_t)f * d.px + (size_t)t_lo * d.W;
+    unsigned long long* out = d.p99cand + (size_t)f * d.px;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(m1[i]));
+        const bool hit = (b >> 52) == bucket;
+        const unsigned bal = __ballot_sync(__activemask(), hit);
+        if (!bal) continue;
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(bal) - 1;
+        unsigned base = 0;
+        if (lane == leader) base = atomicAdd(&d.aux[f].p99_cands, (unsigned)__popc(bal));
+        base = __shfl_sync(__activemask(), base, leader);
+        if (hit) out[base + __popc(bal & ((1u << lane) - 1u))] = b;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_p99_select(Dev d) {
+    const int f = blockIdx.x;
+    if (frame_failed(d, f)) return;
+    __shared__ unsigned int hist[256];
+    __shared__ unsigned long long s_prefix, s_rank;
+    const unsigned ncand = d.aux[f].p99_cands;
+    const unsigned long long* c = d.p99cand + (size_t)f * d.px;
+    unsigned long long prefix = (unsigned long long)d.aux[f].p99_bucket << 52;
+    unsigned long long mask = 0xFFF0000000000000ULL;
+    unsigned long long rank = d.aux[f].p99_rank;
+    const int shifts[7] = {44, 36, 28, 20, 12, 4, 0};
+    const int widths[7] = {8, 8, 8, 8, 8, 8, 4};
+    for (int pass = 0; pass < 7; ++pass) {
+        const int sh = shifts[pass];
+        const unsigned dm = (1u << widths[pass]) - 1u;
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < ncand; i += blockDim.x) {
+            const unsigned long long x = c[i];
+            if ((x & mask) == prefix) atomicAdd(&hist[(x >> sh) & dm], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long run = 0;
+            unsigned dg = 0;
+            for (; dg <= dm; ++dg) {
+                if (run + hist[dg] > rank) break;
+                run += hist[dg];
+            }
+            s_prefix = prefix | ((unsigned long long)dg << sh);
+            s_rank = rank - run;
+        }
+        __syncthreads();
+        prefix = s_prefix;
+        rank = s_rank;
+        mask |= (unsigned long long)dm << sh;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double p99 = __longlong_as_double((long long)prefix);
+        const int v_top = (int)d.rep[f].horizon, v_max = d.H - 1;
+        const double tr = -0.15 * (double)(v_max - v_top + 1) * p99;
+        d.aux[f].tr = tr;
+        d.rep[f].tr_lpv_used = tr;
+    }
+}
+
+// =====================================================================
+// K5c  aggregate_energy (lanes.hpp:106-129) with lane_track (:83-96) fused:
+// one thread per extended bottom column, the track recursion and the decayed
+// m1 sum run together from the bottom row upward.
+// =====================================================================
+__global__ void __launch_bounds__(128) k_energy(Dev d) {
+    const int f = blockIdx.y;
+    if (frame_failed(d, f)) return;
+    const int ci = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ci >= d.ext_cols) return;
+    const int W = d.W, H = d.H;
+    const int v_top = (int)d.rep[f].horizon, v_max = H - 1;
+    const double* vpx = d.vpx + (size_t)f * H;
+    const double* vpy = d.vpy + (size_t)f * H;
+    const double* m1 = d.m1 + (size_t)f * d.px;
+    const double lg = d.lambda_g;
+    double u = (double)(d.ext_lo + ci);
+    bool alive = true;
+    double e = 0.0;
+    for (int v = v_max; v >= v_top; --v) {
+        if (v < v_max && alive) {
+            const double py = vpy[v + 1];
+            const double denom = (double)(v + 1) - py;
+            if (fabs(denom) < 0.5) {
+                alive = false;
+            } else {
+                u = (vpx[v + 1] + v * u - py * u) / denom;
+            }
+        }
+        double contrib = 0.0;
+        if (alive && !isnan(u)) {
+            const long long r = llround_ref(u);
+            if (r >= 0 && r < W && v >= 0 && v < H) contrib = m1[(size_t)v * W + (int)r];
+        }
+        e = contrib + lg * e;
+    }
+    d.energy[(size_t)f * d.ext_cols + ci] = e;
+}
+
+// =====================================================================
+// K5d  select_lanes (lanes.hpp:144-178): strict interior minima under the
+// threshold, sorted by (energy, column) with a shared-memory bitonic sort,
+// greedy min_sep suppression, then each kept lane's track length.
+// =====================================================================
+__global__ void __launch_bounds__(256) k_select(Dev d, int sort_cap) {
+    extern __shared__ unsigned long long sh_keys[];  // [sort_cap] keys, [sort_cap] cols
+    const int f = blockIdx.x;
+    if (frame_failed(d, f)) return;
+    int* cols = (int*)(sh_keys + sort_cap);
+    __shared__ int s_n, s_kept;
+    const int n = d.ext_cols;
+    const double* h = d.energy + (size_t)f * n;
+    const double tr = isnan(d.tr_lpv) ? d.aux[f].tr : d.tr_lpv;
+    if (threadIdx.x == 0) {
+        s_n = 0;
+        if (!isnan(d.tr_lpv)) d.rep[f].tr_lpv_used = tr;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (i >= 1 && i + 1 < n && h[i] < h[i - 1] && h[i] < h[i + 1] && h[i] < tr) {
+            const int slot = atomicAdd(&s_n, 1);
+            if (slot < sort_cap) {
+                sh_keys[slot] = order_key(h[i]);
+                cols[slot] = i;
+            }
+        }
+    }
+    __syncthreads();
+    const int m = min(s_n, sort_cap);
+    int p2 = 1;
+    while (p2 < m) p2 <<= 1;
+    for (int i = m + threadIdx.x; i < p2; i += blockDim.x) {
+        sh_keys[i] = ~0ULL;
+        cols[i] = 0x7fffffff;
+    }
+    __syncthreads();
+    for (int k = 2; k <= p2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    const bool gt = sh_keys[i] > sh_keys[l] ||
+                                    (sh_keys[i] == sh_keys[l] && cols[i] > cols[l]);
+                    if (gt == up) {
+                        const unsigned long long tk = sh_keys[i];
+                        sh_keys[i] = sh_keys[l];
+                        sh_keys[l] = tk;
+                        const int tc = cols[i];
+                        cols[i] = cols[l];
+                        cols[l] = tc;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    lk_lane* lanes = d.lanes + (size_t)f * d.lane_cap;
+    if (threadIdx.x == 0) {
+        int kept = 0;
+        for (int q = 0; q < m; ++q) {
+            const int i = cols[q];
+            bool close = false;
+            for (int k = 0; k < kept; ++k)
+                if (abs(i - (lanes[k].bottom_col - d.ext_lo)) < d.min_lane_sep) {
+                    close = true;
+                    break;
+                }
+            if (close) continue;
+            if (kept < d.lane_cap) {
+                lanes[kept].bottom_col = d.ext_lo + i;
+                lanes[kept].energy = h[i];
+                lanes[kept].n_points = 0;
+            }
+            ++kept;
+        }
+        s_kept = kept;
+        lk_frame_report& rep = d.rep[f];
+        rep.lane_count = kept;
+        for (int k = 0; k < kept && k < LK_MAX_INLINE_LANES; ++k) {
+            rep.lane_bottom_col[k] = lanes[k].bottom_col;
+            rep.lane_energy[k] = lanes[k].energy;
+        }
+    }
+    __syncthreads();
+    // polylines: lane_track per kept lane (lanes.hpp:161-166)
+    const int H = d.H, v_top = (int)d.rep[f].horizon, v_max = H - 1, rows = v_max - v_top + 1;
+    const double* vpx = d.vpx + (size_t)f * H;
+    const double* vpy = d.vpy + (size_t)f * H;
+    for (int k = threadIdx.x; k < min(s_kept, d.lane_cap); k += blockDim.x) {
+        double u = (double)lanes[k].bottom_col;
+        double* poly = d.hooks ? d.polylines + ((size_t)f * d.lane_cap + k) * H : nullptr;
+        int np = 1;
+        if (poly) poly[rows - 1] = u;
+        int v = v_max - 1;
+        for (; v >= v_top; --v) {
+            const double py = vpy[v + 1];
+            const double denom = (double)(v + 1) - py;
+            if (fabs(denom) < 0.5) break;
+            u = (vpx[v + 1] + v * u - py * u) / denom;
+            np += !isnan(u);
+            if (poly) poly[v - v_top] = u;
+        }
+        if (poly)
+            for (; v >= v_top; --v) poly[v - v_top] = __longlong_as_double(0x7ff8000000000000LL);
+        lanes[k].n_points = np;
+    }
+}
+
+// Copies the aux counters into the public report at the end of the batch.
+__global__ void k_finish(Dev d, int n) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= n) return;
+    lk_frame_report& r = d.rep[f];
+    const FrameAux& a = d.aux[f];
+    r.road_mask_pixels = (int64_t)a.mask_px;
+    r.edge_pixels = (int64_t)a.edge_px;
+    r.vpx_votes = (int64_t)a.votes;
+    r.vpx_skipped = (int64_t)a.skipped;
+}
+
+}  // namespace lkg
+
+// ------------------------------------------------------------------ launchers
+namespace lkg {
+
+cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s,
+                            cudaEvent_t* stage_ev) {
+    auto mark = [&](int stage) {
+        if (stage_ev) cudaEventRecord(stage_ev[stage], s);
+    };
+    mark(0);
+    k_vdisparity<<<dim3((d.H + K1_ROWS - 1) / K1_ROWS, n), 256, K1_ROWS * d.D1 * 4, s>>>(
+        d, lp.vhistT);
+    mark(5);
+    k_vpath<<<n, 512, lp.vpath_smem, s>>>(d, lp.vhistT, lp.vpath_choice_smem);
+    mark(6);
+    k_road_fit<<<n, 128, lp.road_smem, s>>>(d);
+    mark(7);
+    mark(8);  // road mask is fused into the Sobel pass (stage 10)
+    const dim3 bg((d.W + BF_TW - 1) / BF_TW, (d.H + BF_TH - 1) / BF_TH, n);
+    if (d.rho == 5)
+        k_bilateral<5><<<bg, 256, lp.bf_smem, s>>>(d);
+    else
+        k_bilateral<-1><<<bg, 256, lp.bf_smem, s>>>(d);
+    mark(9);
+    k_sobel_edges<<<dim3(d.H, n), 256, 0, s>>>(d);
+    k_edge_emit<<<dim3(d.H, n), 256, 0, s>>>(d);
+    mark(10);
+    k_vanish<<<n, K4_THREADS, lp.vanish_smem, s>>>(d);
+    k_gamma_fit<<<n, 256, lp.gamma_smem, s>>>(d);
+    mark(11);
+    const bool auto_tr = isnan(d.tr_lpv);
+    k_m0_m1<<<dim3((d.W + M_TW - 1) / M_TW, (d.H + lp.m_tile_h - 1) / lp.m_tile_h, n), 256,
+              lp.m_smem, s>>>(d, lp.m_tile_h, auto_tr ? 1 : 0);
+    if (auto_tr) {
+        k_p99_bucket<<<n, 256, 0, s>>>(d);
+        k_p99_collect<<<dim3(lp.collect_blocks, n), 256, 0, s>>>(d);
+        k_p99_select<<<n, 256, 0, s>>>(d);
+    }
+    k_energy<<<dim3((d.ext_cols + 127) / 128, n), 128, 0, s>>>(d);
+    k_select<<<n, 256, lp.select_smem, s>>>(d, lp.sort_cap);
+    k_finish<<<(n + 127) / 128, 128, 0, s>>>(d, n);
+    mark(12);
+    return cudaGetLastError();
+}
+
+int launches_per_batch(const Dev& d) { return isnan(d.tr_lpv) ? 15 : 12; }
+
+cudaError_t configure_kernels(const LaunchPlan& lp) {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_vpath, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lp.vpath_smem)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_road_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lp.road_smem)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_bilateral<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lp.bf_smem)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_bilateral<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lp.bf_smem)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_vanish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lp.vanish_smem)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_gamma_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lp.gamma_smem)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_m0_m1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lp.m_smem)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lp.select_smem)))
+        return e;
+    return cudaSuccess;
+}
+
+}  // namespace lkg

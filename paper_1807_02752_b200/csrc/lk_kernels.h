@@ -1,0 +1,39 @@
+// lk_kernels.h — host-visible launch plan for the stage kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "lk_device.cuh"
+
+namespace lkg {
+
+constexpr int K1_ROWS = 8;              // rows per v-disparity CTA
+constexpr int BF_TW = 32, BF_TH = 8;    // bilateral tile
+constexpr int K4_THREADS = 1024;        // V_px CTA
+constexpr int BT_CHUNK = 32;            // u-path backtrack: stages per window
+constexpr int BT_SPAN = 5 * BT_CHUNK;   // max drift inside a window (|offset| <= 5)
+constexpr int M_TW = 128;               // m0/m1 tile width
+
+struct LaunchPlan {
+    int32_t* vhistT;          // [B][D1][H] transposed v-disparity for the v-path DP
+    size_t vpath_smem;
+    int vpath_choice_smem;    // choices of the v-path DP kept in shared memory
+    size_t road_smem;
+    size_t bf_smem;
+    size_t vanish_smem;
+    size_t gamma_smem;
+    size_t m_smem;
+    int m_tile_h;
+    int collect_blocks;
+    size_t select_smem;
+    int sort_cap;
+};
+
+// Enqueues stages 5-12 for n frames on stream s. stage_ev (13 events, may
+// be null) are recorded at the stage boundaries: [0] start, [k] end of stage k.
+cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s,
+                            cudaEvent_t* stage_ev);
+cudaError_t configure_kernels(const LaunchPlan& lp);
+int launches_per_batch(const Dev& d);
+
+}  // namespace lkg

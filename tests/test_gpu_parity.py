@@ -1,0 +1,135 @@
+"""GPU path vs the CPU oracle, hook by hook, through the C-ABI.
+
+Integer outputs bit-exact, FP outputs within 1e-5 relative (tests/parity.py).
+Covers the probe scene (config 1), config-2 batch members, the obstacle /
+pitch-change stress scenes (config 3), the acceptance family at 320x240,
+and failure paths (StageError numbers and messages)."""
+import numpy as np
+import pytest
+
+from paper_1807_02752_b200 import abi, lanekit, scenes
+from parity import compare_frame, compare_reports
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_and_compare(oracle, params, cfg, hooks=True):
+    grey, disp = lanekit.synth_batch(params, threads=8)
+    n, H, W = grey.shape
+    with lanekit.GpuPipeline(W, H, cfg, max_batch=n, hooks=hooks) as pipe:
+        reps = pipe.run(grey, disp)
+        problems = []
+        for i in range(n):
+            o = oracle.run(grey[i], disp[i], cfg)
+            p = compare_reports(reps[i], o.report)
+            p += compare_frame(lambda name: pipe.stage(i, name), o, hooks=hooks)
+            problems += [f"frame {i}: {x}" for x in p]
+        return reps, problems
+
+
+def test_probe_scene_all_hooks(oracle):
+    reps, problems = _run_and_compare(oracle, [scenes.probe_scene()], abi.default_config())
+    assert not problems, "\n".join(problems)
+    assert reps[0].status == 0
+    assert sorted(reps[0].as_dict()["lane_bottom_col"]) == [370, 767]
+
+
+def test_config2_members(oracle):
+    params = [scenes.batch_scene(i) for i in range(6)]
+    reps, problems = _run_and_compare(oracle, params, abi.default_config())
+    assert not problems, "\n".join(problems)
+
+
+def test_stress_obstacles_pitch(oracle):
+    params = [scenes.stress_scene(i) for i in range(4)]
+    reps, problems = _run_and_compare(oracle, params, abi.default_config())
+    assert not problems, "\n".join(problems)
+
+
+def test_acceptance_family(oracle):
+    params = [scenes.acceptance_scene(i) for i in range(20)]
+    reps, problems = _run_and_compare(oracle, params, scenes.acceptance_config())
+    assert not problems, "\n".join(problems)
+
+
+def test_no_hooks_mode_matches(oracle):
+    params = [scenes.batch_scene(i) for i in range(3)]
+    reps, problems = _run_and_compare(oracle, params, abi.default_config(), hooks=False)
+    assert not problems, "\n".join(problems)
+
+
+def test_paper_sign_and_manual_threshold(oracle):
+    params = [scenes.batch_scene(i) for i in range(2)]
+    cfg = abi.default_config(paper_sign=True, tr_lpv=-400.0, lambda_g=0.98, nu=2, chi=10)
+    reps, problems = _run_and_compare(oracle, params, cfg)
+    assert not problems, "\n".join(problems)
+
+
+def test_stage6_no_road_evidence(oracle):
+    """Identical views -> empty disparity -> StageError 6 (test_pipeline.cpp:119-127)."""
+    grey, disp = lanekit.synth_batch([scenes.acceptance_scene(0)])
+    disp[:] = 0
+    with pytest.raises(lanekit.StageError) as ei:
+        lanekit.run_pipeline_from_disparity(grey[0], disp[0], scenes.acceptance_config())
+    assert ei.value.stage == 6
+    assert ei.value.stage_name == "road path extraction"
+    assert str(ei.value) == ("stage 6 (road path extraction): v-disparity histogram is empty; "
+                             "no road surface evidence")
+    o = oracle.run(grey[0], disp[0], scenes.acceptance_config())
+    assert o.report.failed_stage == 6
+
+
+def test_failed_frame_does_not_abort_batch(oracle):
+    params = [scenes.acceptance_scene(i) for i in range(3)]
+    grey, disp = lanekit.synth_batch(params)
+    disp[1] = 0
+    cfg = scenes.acceptance_config()
+    with lanekit.GpuPipeline(320, 240, cfg, max_batch=3, hooks=True) as pipe:
+        reps = pipe.run(grey, disp)
+        assert reps[1].status == abi.LK_ERR_FRAME and reps[1].failed_stage == 6
+        for i in (0, 2):
+            o = oracle.run(grey[i], disp[i], cfg)
+            assert not compare_reports(reps[i], o.report)
+            assert not compare_frame(lambda n: pipe.stage(i, n), o)
+
+
+def test_stage11_no_edge_evidence(oracle):
+    """A flat frame has no edges: StageError 11 (pipeline.hpp:238-239)."""
+    grey, disp = lanekit.synth_batch([scenes.acceptance_scene(0)])
+    grey[:] = 128
+    cfg = scenes.acceptance_config()
+    with lanekit.GpuPipeline(320, 240, cfg, max_batch=1) as pipe:
+        rep = pipe.run(grey, disp)[0]
+    o = oracle.run(grey[0], disp[0], cfg)
+    assert o.report.failed_stage == 11
+    assert not compare_reports(rep, o.report)
+    assert abi.frame_message(rep).startswith("stage 11 (vanishing point estimation): ")
+
+
+def test_determinism_and_batch_invariance(oracle):
+    """Criterion 12 analogue: reruns and different batch compositions are bit-identical."""
+    params = [scenes.batch_scene(i) for i in range(4)]
+    grey, disp = lanekit.synth_batch(params)
+    cfg = abi.default_config()
+    with lanekit.GpuPipeline(1242, 375, cfg, max_batch=4) as pipe:
+        a = [r.as_dict() for r in pipe.run(grey, disp)]
+        ea = [pipe.stage(i, "ENERGY").copy() for i in range(4)]
+        b = [r.as_dict() for r in pipe.run(grey, disp)]
+        c = [r.as_dict() for r in pipe.run(grey[2:3], disp[2:3])]
+        ec = pipe.stage(0, "ENERGY")
+    assert a == b
+    assert a[2] == c[0]
+    assert np.array_equal(ea[2], ec)
+
+
+def test_direct_launch_matches_graph(oracle):
+    params = [scenes.batch_scene(i) for i in range(2)]
+    grey, disp = lanekit.synth_batch(params)
+    cfg = abi.default_config()
+    with lanekit.GpuPipeline(1242, 375, cfg, max_batch=2, graph=False) as p1:
+        a = [r.as_dict() for r in p1.run(grey, disp)]
+        t = p1.stage_times()
+    with lanekit.GpuPipeline(1242, 375, cfg, max_batch=2) as p2:
+        b = [r.as_dict() for r in p2.run(grey, disp)]
+    assert a == b
+    assert t[0] > 0 and t[9] > 0
