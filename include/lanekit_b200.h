@@ -238,9 +238,13 @@ lk_status lk_get_stage(lk_ctx* ctx, int frame, int stage, void* dst, size_t capa
                        size_t* needed);
 
 /* Device milliseconds of the last batch per pipeline stage 5..12 (ms[5..12]),
- * measured with CUDA events around each stage's kernels when
- * LK_FLAG_NO_GRAPH is set; ms[0] is the whole batch. */
+ * from CUDA events recorded on the context stream around each stage's kernels
+ * (event-record nodes inside the CUDA graph); ms[0] is the whole batch.
+ * Stage 8 (road mask) is fused into stage 10's Sobel pass and reads ~0. */
 lk_status lk_stage_times(lk_ctx* ctx, float ms[13]);
+
+/* Measured FP64 add+mul issue rate of this device (ops/s), for rooflines. */
+lk_status lk_measure_fp64(int device, double* ops_per_s);
 
 /* Number of kernel launches one lk_run_batch / lk_enqueue issues. */
 int lk_launches_per_batch(lk_ctx* ctx);

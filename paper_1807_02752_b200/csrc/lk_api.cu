@@ -361,12 +361,19 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     lp.vpath_choice_smem = vp_base + (size_t)D1 * H <= 160 * 1024;
     lp.vpath_smem = vp_base + (lp.vpath_choice_smem ? (size_t)D1 * H : 0);
     if (!lp.vpath_choice_smem) A(&d.vchoice, (size_t)B * D1 * H);
-    lp.road_smem = (size_t)(5 * D1 + 2) * 4 + (size_t)D1 * 8 + 16;
+    lp.road_smem = (size_t)(8 * D1 + 2) * 4 + (size_t)D1 * 8 + 16;
     lp.bf_smem = (size_t)(256 + win * win) * 8 +
                  (size_t)(lkg::BF_TH + 2 * rho) * (lkg::BF_TW + 2 * rho) + 16;
+    {
+        const size_t twh = lkg::BT_W + 10, thh = lkg::BT_H + 10, npx = twh * thh;
+        const size_t tri = (size_t)lkg::BT_TRI_N * (lkg::BT_TRI_N + 1) / 2;
+        lp.bt_smem = tri * 8 + npx * 8 + npx * 4 + 2 * 256 * 4 + npx + 256 + 16;
+        if (win == 11)
+            for (int i = 0; i < 121; ++i) lp.ws.w[i] = ws[i];
+    }
     lp.vanish_smem = (size_t)2 * C * 8 + (size_t)C * 4 + (size_t)2 * H * 4 +
                      (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 16;
-    lp.gamma_smem = (size_t)5 * H * 4 + 8 + (size_t)H * 8 + 16;
+    lp.gamma_smem = (size_t)12 * H * 4 + 8 + (size_t)H * 8 + 16;
     lp.m_tile_h = 16;
     auto m_bytes = [&](int th) {
         const size_t GH = th + 2 + 2 * cfg->varsigma, GW = lkg::M_TW + 2 + 2 * cfg->nu;
@@ -379,7 +386,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     lp.sort_cap = sort_cap;
     lp.select_smem = (size_t)sort_cap * 12;
     const size_t smem_cap = prop.sharedMemPerBlockOptin;
-    if (lp.vpath_smem > smem_cap || lp.road_smem > smem_cap || lp.bf_smem > smem_cap ||
+    if (lp.vpath_smem > smem_cap || lp.road_smem > smem_cap || lp.bf_smem > smem_cap || lp.bt_smem > smem_cap ||
         lp.vanish_smem > smem_cap || lp.gamma_smem > smem_cap || lp.m_smem > smem_cap || lp.select_smem > smem_cap) {
         lk_destroy(c);
         return fail(LK_ERR_CONFIG, "frame geometry / window sizes exceed shared memory");
@@ -446,12 +453,12 @@ lk_status lk_enqueue(lk_ctx* c, int n) {
         c->timed = true;
         return enqueue_direct(c, n, true);
     }
-    c->timed = false;
+    c->timed = true;
     auto it = c->graphs.find(n);
     if (it == c->graphs.end()) {
         cudaGraph_t g;
         CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        lk_status s = enqueue_direct(c, n, false);
+        lk_status s = enqueue_direct(c, n, true);
         cudaError_t e = cudaStreamEndCapture(c->stream, &g);
         if (s != LK_OK) return s;
         if (e != cudaSuccess) return fail(LK_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
@@ -503,7 +510,7 @@ lk_status lk_run_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* disparity,
 lk_status lk_stage_times(lk_ctx* c, float ms[13]) {
     if (!c || !ms) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
     for (int i = 0; i < 13; ++i) ms[i] = 0.f;
-    if (!c->timed) return fail(LK_ERR_UNAVAILABLE, "stage times need LK_FLAG_NO_GRAPH");
+    if (!c->timed) return fail(LK_ERR_UNAVAILABLE, "no batch has run yet");
     CU(cudaStreamSynchronize(c->stream));
     int prev = 0;
     for (int st : {5, 6, 7, 8, 9, 10, 11, 12}) {
@@ -635,3 +642,16 @@ void lk_abi_sizes(size_t* out) {
 }
 
 }  // extern "C"
+
+namespace lkg {
+cudaError_t fp64_probe(int sms, double* ops_per_s);
+}
+
+extern "C" lk_status lk_measure_fp64(int device, double* ops_per_s) {
+    if (!ops_per_s) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    CU(lkg::fp64_probe(prop.multiProcessorCount, ops_per_s));
+    return LK_OK;
+}

@@ -188,12 +188,12 @@ __global__ void __launch_bounds__(128) k_road_fit(Dev d) {
     const int f = blockIdx.x;
     if (frame_failed(d, f)) return;
     const int n = d.D1, H = d.H;
+    constexpr int NW = 4;  // 128 threads
     int* px = sh_i;
     int* pv = px + n;
-    int* bA = pv + n;
-    int* bB = bA + n;
-    int* bC = bB + n;
-    double* tbuf = align8(bC + n);
+    int* bufs[NW + 2];
+    for (int b = 0; b < NW + 2; ++b) bufs[b] = pv + n + b * n;
+    double* tbuf = align8(pv + n + (NW + 2) * n);
     __shared__ RansacState st;
     __shared__ int s_bad_row;
     const int32_t* pts = d.vpath + (size_t)f * n * 2;
@@ -203,9 +203,7 @@ __global__ void __launch_bounds__(128) k_road_fit(Dev d) {
     }
     if (threadIdx.x == 0) s_bad_row = 0x7fffffff;
     __syncthreads();
-    if (threadIdx.x < 32)
-        warp_ransac<3>(px, pv, n, d.tr_y, d.eps_y, d.max_iter, d.rng, bA, bB, bC, tbuf, st);
-    __syncthreads();
+    block_ransac<3, NW>(px, pv, n, d.tr_y, d.eps_y, d.max_iter, d.rng, bufs, tbuf, st);
     lk_frame_report& rep = d.rep[f];
     if (st.msg) {
         if (threadIdx.x == 0) {
@@ -346,6 +344,152 @@ __global__ void __launch_bounds__(256) k_bilateral(Dev d) {
         }
     }
     d.smoothed[(size_t)f * d.px + (size_t)v * d.W + u] = num / den;
+}
+
+// ---------------------------------------------------------------------
+// K3a' tiled bilateral for the default 11x11 window (RHO = 5).
+// The exact wr LUT is 512 KB. A tile of BT_W x BT_H outputs (plus its 5-px
+// mirrored halo) only touches the values V present in that region, and
+// wr[a][b] == wr[b][a] exactly (a-b == -(b-a) in IEEE arithmetic), so the CTA
+// compacts V (typically 40-130 values) and stages the exact symmetric
+// sub-table, |V|(|V|+1)/2 doubles, in shared memory: every tap's weight is one
+// LDS.64 instead of an L1/L2 gather (tiles with |V| > BT_TRI_N fall back to
+// __ldg on the full table). The 121 spatial factors ws are a by-value kernel
+// parameter, so they reach the DMULs as constant-bank operands. Each thread
+// produces BT_R vertically adjacent outputs: a window row is loaded once
+// (conflict-free, consecutive lanes) and folded into every output whose
+// window contains it, still in the reference's j-major / i-minor order.
+// ---------------------------------------------------------------------
+template <int RHO, bool SMEM_TABLE>
+__device__ __forceinline__ void bilateral_rows(const Dev& d, const WsParam& ws,
+                                               const double* s_sub, const int* s_map,
+                                               const double* s_v, const uint32_t* s_kt,
+                                               const uint8_t* s_g, int f, int u0, int v0) {
+    constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO;
+    const int tx = threadIdx.x % BT_W, ty = threadIdx.x / BT_W;
+    const int r0 = ty * BT_R;
+    int ca[BT_R], ta[BT_R];
+    const double* grow[BT_R];
+#pragma unroll
+    for (int r = 0; r < BT_R; ++r) {
+        const int kc = s_g[(r0 + r + RHO) * TWh + tx + RHO];
+        ca[r] = SMEM_TABLE ? s_map[kc] : kc;
+        ta[r] = (ca[r] * (ca[r] + 1)) >> 1;
+        grow[r] = d.wr + kc * 256;
+    }
+    double num[BT_R], den[BT_R];
+#pragma unroll
+    for (int r = 0; r < BT_R; ++r) num[r] = den[r] = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < BT_R + 2 * RHO; ++jj) {
+        const int prow = (r0 + jj) * TWh + tx;
+        uint32_t kt[WIN];
+        double vv[WIN];
+#pragma unroll
+        for (int i = 0; i < WIN; ++i) {
+            kt[i] = s_kt[prow + i];
+            vv[i] = s_v[prow + i];
+        }
+#pragma unroll
+        for (int r = 0; r < BT_R; ++r) {
+            const int dj = jj - r;
+            if (dj < 0 || dj >= WIN) continue;
+#pragma unroll
+            for (int i = 0; i < WIN; ++i) {
+                const int b = (int)(kt[i] & 0xffu);
+                double wrv;
+                if (SMEM_TABLE) {
+                    const int tb = (int)(kt[i] >> 8);
+                    wrv = s_sub[b <= ca[r] ? ta[r] + b : tb + ca[r]];
+                } else {
+                    wrv = __ldg(grow[r] + b);
+                }
+                const double w = ws.w[dj * WIN + i] * wrv;
+                num[r] += w * vv[i];
+                den[r] += w;
+            }
+        }
+    }
+    const int u = u0 + tx;
+#pragma unroll
+    for (int r = 0; r < BT_R; ++r) {
+        const int v = v0 + r0 + r;
+        if (u < d.W && v < d.H) d.smoothed[(size_t)f * d.px + (size_t)v * d.W + u] = num[r] / den[r];
+    }
+}
+
+template <int RHO>
+__global__ void __launch_bounds__(256, 2) k_bilateral_tile(Dev d, WsParam ws) {
+    constexpr int TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
+    constexpr int NPX = TWh * THh;
+    constexpr int TRI = BT_TRI_N * (BT_TRI_N + 1) / 2;
+    extern __shared__ double sm_bt[];
+    double* s_sub = sm_bt;                       // [TRI] symmetric exact sub-table
+    double* s_v = s_sub + TRI;                   // [NPX] neighbour values k/255.0
+    uint32_t* s_kt = (uint32_t*)(s_v + NPX);     // [NPX] local index | tri(index) << 8
+    int* s_map = (int*)(s_kt + NPX);             // [256] value -> local index
+    int* s_inv = s_map + 256;                    // [256] local index -> value
+    uint8_t* s_g = (uint8_t*)(s_inv + 256);      // [NPX] raw 8-bit grey
+    uint8_t* s_fv = s_g + NPX;                   // [256] value present
+    __shared__ int s_warp[8];
+    __shared__ int s_n;
+    const int f = blockIdx.z;
+    if (frame_failed(d, f)) return;
+    const int u0 = blockIdx.x * BT_W, v0 = blockIdx.y * BT_H;
+    const uint8_t* g = d.grey + (size_t)f * d.px;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_fv[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < NPX; i += blockDim.x) {
+        const int ty = i / TWh, tx = i - ty * TWh;
+        const int gu = mirror(u0 + tx - RHO, d.W), gv = mirror(v0 + ty - RHO, d.H);
+        const int k = g[(size_t)gv * d.W + gu];
+        s_g[i] = (uint8_t)k;
+        s_v[i] = d.val[k];
+        s_fv[k] = 1;  // benign race: every writer stores 1
+    }
+    __syncthreads();
+    {  // exclusive scan of the presence vector -> value <-> local index
+        const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+        const int fv = s_fv[t];
+        int iv = fv;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int b = __shfl_up_sync(0xffffffffu, iv, o);
+            if (lane >= o) iv += b;
+        }
+        if (lane == 31) s_warp[w] = iv;
+        __syncthreads();
+        int ov = 0;
+        for (int k = 0; k < w; ++k) ov += s_warp[k];
+        iv += ov - fv;
+        s_map[t] = iv;
+        if (fv) s_inv[iv] = t;
+        if (t == 255) s_n = iv + fv;
+    }
+    __syncthreads();
+    const int nv = s_n;
+    const bool smem_table = nv <= BT_TRI_N;
+    if (smem_table) {
+        const int ntri = nv * (nv + 1) / 2;
+        for (int e = threadIdx.x; e < ntri; e += blockDim.x) {
+            // e = b(b+1)/2 + a, a <= b
+            int b = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+            while (b * (b + 1) / 2 > e) --b;
+            while ((b + 1) * (b + 2) / 2 <= e) ++b;
+            const int a = e - b * (b + 1) / 2;
+            s_sub[e] = __ldg(d.wr + s_inv[a] * 256 + s_inv[b]);
+        }
+        for (int i = threadIdx.x; i < NPX; i += blockDim.x) {
+            const uint32_t b = (uint32_t)s_map[s_g[i]];
+            s_kt[i] = b | (((b * (b + 1)) >> 1) << 8);
+        }
+    } else {
+        for (int i = threadIdx.x; i < NPX; i += blockDim.x) s_kt[i] = s_g[i];
+    }
+    __syncthreads();
+    if (smem_table)
+        bilateral_rows<RHO, true>(d, ws, s_sub, s_map, s_v, s_kt, s_g, f, u0, v0);
+    else
+        bilateral_rows<RHO, false>(d, ws, s_sub, s_map, s_v, s_kt, s_g, f, u0, v0);
 }
 
 // Sobel taps on the smoothed image with mirrored borders (preprocess.hpp:71-81).
@@ -681,12 +825,12 @@ __global__ void __launch_bounds__(256) k_gamma_fit(Dev d) {
     lk_frame_report& rep = d.rep[f];
     const int v_top = (int)rep.horizon, v_max = H - 1;
     const int nrows = v_max - v_top + 1;
+    constexpr int NW = 8;  // 256 threads
     int* px = sh_g;
     int* pv = px + H;
-    int* bA = pv + H;
-    int* bB = bA + H;
-    int* bC = bB + H;
-    double* tbuf = align8(bC + H);
+    int* bufs[NW + 2];
+    for (int b = 0; b < NW + 2; ++b) bufs[b] = pv + H + b * H;
+    double* tbuf = align8(pv + H + (NW + 2) * H);
     __shared__ RansacState st;
     const int32_t* up = d.upath + (size_t)f * H * 2;
     for (int i = threadIdx.x; i < nrows; i += blockDim.x) {
@@ -694,9 +838,7 @@ __global__ void __launch_bounds__(256) k_gamma_fit(Dev d) {
         pv[i] = up[2 * i + 1];
     }
     __syncthreads();
-    if (threadIdx.x < 32)
-        warp_ransac<5>(px, pv, nrows, d.tr_x, d.eps_x, d.max_iter, d.rng, bA, bB, bC, tbuf, st);
-    __syncthreads();
+    block_ransac<5, NW>(px, pv, nrows, d.tr_x, d.eps_x, d.max_iter, d.rng, bufs, tbuf, st);
     if (st.msg) {
         if (threadIdx.x == 0) {
             rep.gamma_iterations = st.iterations;
@@ -1111,8 +1253,14 @@ namespace lkg {
 
 cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s,
                             cudaEvent_t* stage_ev) {
-    auto mark = [&](int stage) {
-        if (stage_ev) cudaEventRecord(stage_ev[stage], s);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    auto mark = [&](int stage) {  // event-record nodes when captured into the graph
+        if (!stage_ev) return;
+        if (cap == cudaStreamCaptureStatusActive)
+            cudaEventRecordWithFlags(stage_ev[stage], s, cudaEventRecordExternal);
+        else
+            cudaEventRecord(stage_ev[stage], s);
     };
     mark(0);
     k_vdisparity<<<dim3((d.H + K1_ROWS - 1) / K1_ROWS, n), 256, K1_ROWS * d.D1 * 4, s>>>(
@@ -1125,7 +1273,8 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     mark(8);  // road mask is fused into the Sobel pass (stage 10)
     const dim3 bg((d.W + BF_TW - 1) / BF_TW, (d.H + BF_TH - 1) / BF_TH, n);
     if (d.rho == 5)
-        k_bilateral<5><<<bg, 256, lp.bf_smem, s>>>(d);
+        k_bilateral_tile<5><<<dim3((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n), 256,
+                               lp.bt_smem, s>>>(d, lp.ws);
     else
         k_bilateral<-1><<<bg, 256, lp.bf_smem, s>>>(d);
     mark(9);
@@ -1160,8 +1309,8 @@ cudaError_t configure_kernels(const LaunchPlan& lp) {
     if ((e = cudaFuncSetAttribute(k_road_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lp.road_smem)))
         return e;
-    if ((e = cudaFuncSetAttribute(k_bilateral<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  lp.bf_smem)))
+    if ((e = cudaFuncSetAttribute(k_bilateral_tile<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lp.bt_smem)))
         return e;
     if ((e = cudaFuncSetAttribute(k_bilateral<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lp.bf_smem)))
@@ -1181,4 +1330,45 @@ cudaError_t configure_kernels(const LaunchPlan& lp) {
     return cudaSuccess;
 }
 
+}  // namespace lkg
+
+// ------------------------------------------------------------------ FP64 probe
+// Throughput of dependent-free DADD/DMUL streams (8 chains per thread) for the
+// FP64 roofline denominator; ops counted as individual adds and multiplies.
+namespace lkg {
+__global__ void __launch_bounds__(256) k_fp64_probe(double* sink, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = x[k] * a + b;  // 1 DMUL + 1 DADD (no contraction)
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 12345.678) sink[0] = s;
+}
+
+cudaError_t fp64_probe(int sms, double* ops_per_s) {
+    double* sink;
+    cudaError_t e = cudaMalloc(&sink, 8);
+    if (e) return e;
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    const int blocks = sms * 8, iters = 4096;
+    k_fp64_probe<<<blocks, 256>>>(sink, 64, 0.999999, 1e-7);  // warm-up
+    cudaEventRecord(t0);
+    k_fp64_probe<<<blocks, 256>>>(sink, iters, 0.999999, 1e-7);
+    cudaEventRecord(t1);
+    e = cudaEventSynchronize(t1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    *ops_per_s = (double)blocks * 256 * iters * 8 * 2 / (ms * 1e-3);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    cudaFree(sink);
+    return e ? e : cudaGetLastError();
+}
 }  // namespace lkg

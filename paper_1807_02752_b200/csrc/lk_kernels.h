@@ -8,18 +8,27 @@
 namespace lkg {
 
 constexpr int K1_ROWS = 8;              // rows per v-disparity CTA
-constexpr int BF_TW = 32, BF_TH = 8;    // bilateral tile
+constexpr int BF_TW = 32, BF_TH = 8;    // bilateral tile (generic window)
+constexpr int BT_W = 64, BT_H = 16, BT_R = 4;  // bilateral tile (11x11), outputs per thread
+constexpr int BT_TRI_N = 128;           // max distinct values per tile for the smem sub-table
 constexpr int K4_THREADS = 1024;        // V_px CTA
 constexpr int BT_CHUNK = 32;            // u-path backtrack: stages per window
 constexpr int BT_SPAN = 5 * BT_CHUNK;   // max drift inside a window (|offset| <= 5)
 constexpr int M_TW = 128;               // m0/m1 tile width
 
+// 11x11 spatial weights exp(-ds*inv_s2), passed by value (constant bank)
+struct WsParam {
+    double w[121];
+};
+
 struct LaunchPlan {
+    WsParam ws;
     int32_t* vhistT;          // [B][D1][H] transposed v-disparity for the v-path DP
     size_t vpath_smem;
     int vpath_choice_smem;    // choices of the v-path DP kept in shared memory
     size_t road_smem;
     size_t bf_smem;
+    size_t bt_smem;
     size_t vanish_smem;
     size_t gamma_smem;
     size_t m_smem;

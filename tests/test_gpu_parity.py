@@ -40,6 +40,27 @@ def test_config2_members(oracle):
     assert not problems, "\n".join(problems)
 
 
+def test_ransac_heavy_frames(oracle):
+    """Config-2 members whose RANSAC-gamma runs 83-181 iterations (speculative
+    multi-warp commit must reproduce the serial trimming exactly)."""
+    params = [scenes.batch_scene(i) for i in (92, 199, 68, 159, 25, 206)]
+    reps, problems = _run_and_compare(oracle, params, abi.default_config())
+    assert not problems, "\n".join(problems)
+    assert max(r.gamma_iterations for r in reps) == 181
+
+
+def test_batch_reports_64(oracle):
+    """64-frame batch without hooks: every report field vs the oracle."""
+    params = [scenes.batch_scene(i) for i in range(64)]
+    grey, disp = lanekit.synth_batch(params, threads=8)
+    cfg = abi.default_config()
+    with lanekit.GpuPipeline(1242, 375, cfg, max_batch=64) as pipe:
+        reps = pipe.run(grey, disp)
+        orc = oracle.run_batch(grey, disp, cfg, threads=8)
+        problems = [f"frame {i}: {x}" for i in range(64) for x in compare_reports(reps[i], orc[i])]
+    assert not problems, "\n".join(problems)
+
+
 def test_stress_obstacles_pitch(oracle):
     params = [scenes.stress_scene(i) for i in range(4)]
     reps, problems = _run_and_compare(oracle, params, abi.default_config())
