@@ -314,7 +314,9 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     A(&d.vpx, (size_t)B * H);
     A(&d.smoothed, (size_t)B * d.px);
     A(&d.ebits, (size_t)B * H * d.words_per_row);
-    A(&d.row_cnt, (size_t)B * H);
+    d.n_seg = (W + lkg::SB_TW - 1) / lkg::SB_TW;
+    A(&d.seg_cnt, (size_t)B * H * d.n_seg);
+    A(&d.seg_off, (size_t)B * H * d.n_seg);
     A(&d.row_off, (size_t)B * (H + 1));
     A(&d.e_uv, (size_t)B * d.px);
     A(&d.e_gx, (size_t)B * d.px);
@@ -373,6 +375,9 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     }
     lp.vanish_smem = (size_t)2 * C * 8 + (size_t)C * 4 + (size_t)2 * H * 4 +
                      (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 16;
+    lp.upath_sp = (C + lkg::K4_THREADS - 1) / lkg::K4_THREADS;
+    if (lp.upath_sp == 7) lp.upath_sp = 8;
+    if (lp.upath_sp > 8) lp.upath_sp = 0;
     lp.gamma_smem = (size_t)12 * H * 4 + 8 + (size_t)H * 8 + 16;
     lp.m_tile_h = 16;
     auto m_bytes = [&](int th) {

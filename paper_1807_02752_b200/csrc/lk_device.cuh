@@ -62,7 +62,9 @@ struct Dev {
     double* vpx;            // [B][H]
     double* smoothed;       // [B][H][W]
     uint32_t* ebits;        // [B][H][words_per_row]
-    int32_t* row_cnt;       // [B][H]
+    int n_seg;              // edge-list segments per row (ceil(W / SB_TW))
+    int32_t* seg_cnt;       // [B][H][n_seg]
+    int32_t* seg_off;       // [B][H][n_seg]
     int32_t* row_off;       // [B][H+1]
     int32_t* e_uv;          // [B][px]  u | v << 16
     double* e_gx;           // [B][px]

@@ -505,118 +505,160 @@ __device__ __forceinline__ void sobel_at(const double* img, int W, int H, int u,
 
 // =====================================================================
 // K3b  road_mask (preprocess.hpp:14-26) + sobel_gradients (:67-90) +
-// edge_map test (:103-113). One CTA per (row, frame). The magnitude test
-// !(sqrt(s) < t) is evaluated exactly as s >= s* (s* from the host).
-// Writes an edge bitmap, the row's edge count and mask / edge totals.
+// edge_map test (:103-113). Tile SB_TW x SB_TH with the mirrored 1-px halo
+// of the smoothed image staged in shared memory. The magnitude test
+// !(sqrt(s) < t) is evaluated exactly as s >= s* (s* from the host). Writes
+// the edge bitmap and, per (row, SB_TW-column segment), the edge count.
 // =====================================================================
 __global__ void __launch_bounds__(256) k_sobel_edges(Dev d) {
-    const int v = blockIdx.x, f = blockIdx.y;
+    constexpr int SW = SB_TW + 2;
+    __shared__ double s_img[(SB_TH + 2) * SW];
+    __shared__ int s_seg[SB_TH];
+    __shared__ int s_tot[2];
+    const int f = blockIdx.z;
     if (frame_failed(d, f)) return;
     if (d.W < 3 || d.H < 3) {  // preprocess.hpp:68-69
-        if (v == 0 && threadIdx.x == 0) fail_frame(d, f, 10, LK_MSG_SOBEL_TOO_SMALL);
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+            fail_frame(d, f, 10, LK_MSG_SOBEL_TOO_SMALL);
         return;
     }
-    const int W = d.W;
+    const int W = d.W, H = d.H;
+    const int u0 = blockIdx.x * SB_TW, v0 = blockIdx.y * SB_TH;
     const double* img = d.smoothed + (size_t)f * d.px;
-    const uint8_t* disp = d.disp + (size_t)f * d.px + (size_t)v * W;
-    const int horizon = (int)d.rep[f].horizon;
-    const double fvv = d.fv[(size_t)f * d.H + v];
-    __shared__ int s_cnt[2];
-    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    for (int i = threadIdx.x; i < (SB_TH + 2) * SW; i += blockDim.x) {
+        const int r = i / SW, c = i - r * SW;
+        s_img[i] = img[(size_t)mirror(v0 - 1 + r, H) * W + mirror(u0 - 1 + c, W)];
+    }
+    if (threadIdx.x < SB_TH) s_seg[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_tot[threadIdx.x] = 0;
     __syncthreads();
-    int n_edge = 0, n_mask = 0;
+    const int horizon = (int)d.rep[f].horizon;
     const int lane = threadIdx.x & 31;
-    for (int base = 0; base < W; base += blockDim.x) {
-        const int u = base + threadIdx.x;
+    int n_edge = 0, n_mask = 0;
+#pragma unroll
+    for (int k = 0; k < SB_TW * SB_TH / 256; ++k) {
+        const int i = threadIdx.x + k * 256;
+        const int r = i / SB_TW, c = i % SB_TW;
+        const int v = v0 + r, u = u0 + c;
         bool edge = false;
-        if (u < W) {
-            double gx, gy;
-            sobel_at(img, W, d.H, u, v, gx, gy);
+        if (v < H && u < W) {
+            const double* a = s_img + r * SW + c;  // row v-1, col u-1
+            const double* b = a + SW;               // row v
+            const double* cc = b + SW;              // row v+1
+            const double gx = (a[2] - a[0]) + 2 * (b[2] - b[0]) + (cc[2] - cc[0]);
+            const double gy = (cc[0] - a[0]) + 2 * (cc[1] - a[1]) + (cc[2] - a[2]);
             const double s = gx * gx + gy * gy;
-            const int dv = disp[u];
-            const bool m = v >= horizon && dv != 0 && fabs((double)dv - fvv) <= d.varpi;
+            const int dv = d.disp[(size_t)f * d.px + (size_t)v * W + u];
+            const bool m = v >= horizon && dv != 0 &&
+                           fabs((double)dv - d.fv[(size_t)f * H + v]) <= d.varpi;
             n_mask += m;
             edge = m && s >= d.sobel_s_star;
             n_edge += edge;
             if (d.hooks) {
-                const size_t i = (size_t)f * d.px + (size_t)v * W + u;
-                d.mask[i] = m;
-                d.gx[i] = gx;
-                d.gy[i] = gy;
-                d.mag[i] = sqrt(s);
+                const size_t gi = (size_t)f * d.px + (size_t)v * W + u;
+                d.mask[gi] = m;
+                d.gx[gi] = gx;
+                d.gy[gi] = gy;
+                d.mag[gi] = sqrt(s);
                 double th = atan2(gy, gx);
                 if (th <= -kPi) th = kPi;
-                d.theta[i] = th;
+                d.theta[gi] = th;
             }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, edge);
-        const int word = (base >> 5) + (threadIdx.x >> 5);
-        if (lane == 0 && word < d.words_per_row)
-            d.ebits[((size_t)f * d.H + v) * d.words_per_row + word] = bal;
+        if (lane == 0 && v < H) {
+            const int word = (u0 + c) >> 5;
+            if (word < d.words_per_row) d.ebits[((size_t)f * H + v) * d.words_per_row + word] = bal;
+            if (bal) atomicAdd(&s_seg[r], __popc(bal));
+        }
     }
     for (int o = 16; o; o >>= 1) {
         n_edge += __shfl_xor_sync(0xffffffffu, n_edge, o);
         n_mask += __shfl_xor_sync(0xffffffffu, n_mask, o);
     }
     if (lane == 0) {
-        atomicAdd(&s_cnt[0], n_edge);
-        atomicAdd(&s_cnt[1], n_mask);
+        if (n_edge) atomicAdd(&s_tot[0], n_edge);
+        if (n_mask) atomicAdd(&s_tot[1], n_mask);
     }
     __syncthreads();
+    if (threadIdx.x < SB_TH && v0 + threadIdx.x < H)
+        d.seg_cnt[((size_t)f * H + v0 + threadIdx.x) * d.n_seg + blockIdx.x] = s_seg[threadIdx.x];
     if (threadIdx.x == 0) {
-        d.row_cnt[(size_t)f * d.H + v] = s_cnt[0];
-        if (s_cnt[0]) atomicAdd(&d.aux[f].edge_px, (unsigned long long)s_cnt[0]);
-        if (s_cnt[1]) atomicAdd(&d.aux[f].mask_px, (unsigned long long)s_cnt[1]);
+        if (s_tot[0]) atomicAdd(&d.aux[f].edge_px, (unsigned long long)s_tot[0]);
+        if (s_tot[1]) atomicAdd(&d.aux[f].mask_px, (unsigned long long)s_tot[1]);
     }
+}
+
+// Exclusive scan of the per-segment edge counts in row-major order: every
+// (row, segment) gets the index of its first edge in the frame's edge list;
+// row_off[v] is the first edge of row v (row_off[H] = edge count).
+__global__ void __launch_bounds__(1024) k_edge_scan(Dev d) {
+    const int f = blockIdx.x;
+    if (frame_failed(d, f)) return;
+    __shared__ int s_w[32];
+    const int total = d.H * d.n_seg;
+    const int per = (total + blockDim.x - 1) / blockDim.x;
+    const int start = threadIdx.x * per;
+    const int32_t* cnt = d.seg_cnt + (size_t)f * total;
+    int32_t* off = d.seg_off + (size_t)f * total;
+    int sum = 0;
+    for (int i = start; i < min(start + per, total); ++i) sum += cnt[i];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int inc = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        int x = s_w[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
+        }
+        s_w[lane] = x;
+    }
+    __syncthreads();
+    int run = inc - sum + (w > 0 ? s_w[w - 1] : 0);
+    for (int i = start; i < min(start + per, total); ++i) {
+        off[i] = run;
+        run += cnt[i];
+    }
+    __syncthreads();
+    int32_t* roff = d.row_off + (size_t)f * (d.H + 1);
+    for (int v = threadIdx.x; v < d.H; v += blockDim.x) roff[v] = off[(size_t)v * d.n_seg];
+    if (threadIdx.x == blockDim.x - 1) roff[d.H] = run;
 }
 
 // =====================================================================
 // K3c  edge list in row-major order (edge_map, preprocess.hpp:103-113) +
-// sparse_vpx votes (vanish.hpp:49-70). One CTA per (row, frame): the row's
-// offset is the sum of the earlier rows' counts; edges are emitted in u
-// order by a block-wide ballot scan.
+// sparse_vpx votes (vanish.hpp:49-70). One warp per (row, segment): the
+// segment's bitmap words are walked in u order and each edge is written at
+// its scanned position, so the list order equals the reference's.
 // =====================================================================
 __global__ void __launch_bounds__(256) k_edge_emit(Dev d) {
-    const int v = blockIdx.x, f = blockIdx.y;
+    const int f = blockIdx.y;
     if (frame_failed(d, f)) return;
+    const int lane = threadIdx.x & 31;
+    const int seg = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int W = d.W, H = d.H;
-    const int32_t* rc = d.row_cnt + (size_t)f * H;
-    __shared__ int s_warp[8];
-    __shared__ int s_red[2];
-    int part = 0;
-    for (int r = threadIdx.x; r < v; r += blockDim.x) part += rc[r];
-    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (threadIdx.x < 2) s_red[threadIdx.x] = 0;
-    __syncthreads();
-    if (lane == 0) atomicAdd(&s_red[0], part);
-    __syncthreads();
-    const int off = s_red[0];
-    const int cnt = rc[v];
-    if (threadIdx.x == 0) {
-        d.row_off[(size_t)f * (H + 1) + v] = off;
-        if (v == H - 1) d.row_off[(size_t)f * (H + 1) + H] = off + cnt;
-    }
-    if (cnt == 0) return;
+    if (seg >= H * d.n_seg) return;
+    const int v = seg / d.n_seg, sx = seg - v * d.n_seg;
+    const int base = d.seg_off[(size_t)f * H * d.n_seg + seg];
     const double* img = d.smoothed + (size_t)f * d.px;
     const uint32_t* bits = d.ebits + ((size_t)f * H + v) * d.words_per_row;
     const double vpy = d.vpy[(size_t)f * H + v];
     const bool sing = d.vsing[(size_t)f * H + v] != 0;
     const int ext_hi = d.ext_lo + d.ext_cols - 1;
     int run = 0, n_vote = 0, n_skip = 0;
-    for (int base = 0; base < W; base += blockDim.x) {
-        const int u = base + threadIdx.x;
-        bool edge = false;
-        if (u < W) edge = (bits[u >> 5] >> (u & 31)) & 1u;
-        const unsigned bal = __ballot_sync(0xffffffffu, edge);
-        if (lane == 0) s_warp[wid] = __popc(bal);
-        __syncthreads();
-        int before = run;
-        for (int w = 0; w < wid; ++w) before += s_warp[w];
-        int total = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += s_warp[w];
-        if (edge) {
-            const size_t e = (size_t)f * d.px + off + before + __popc(bal & ((1u << lane) - 1u));
+    for (int w = 0; w < SB_TW / 32; ++w) {
+        const int word = sx * (SB_TW / 32) + w;
+        if (word >= d.words_per_row) break;
+        const uint32_t b = bits[word];
+        if ((b >> lane) & 1u) {
+            const int u = word * 32 + lane;
+            const size_t e = (size_t)f * d.px + base + run + __popc(b & ((1u << lane) - 1u));
             double gx, gy;
             sobel_at(img, W, H, u, v, gx, gy);
             double th = atan2(gy, gx);
@@ -637,8 +679,7 @@ __global__ void __launch_bounds__(256) k_edge_emit(Dev d) {
             }
             d.e_col[e] = col;
         }
-        run += total;
-        __syncthreads();
+        run += __popc(b);
     }
     for (int o = 16; o; o >>= 1) {
         n_vote += __shfl_xor_sync(0xffffffffu, n_vote, o);
@@ -666,6 +707,71 @@ __device__ __forceinline__ double piecewise_weight(double te, double tv, double 
 // and each DP stage reads -rho_vote * count directly.
 // =====================================================================
 
+// One DP stage over the thread's SP consecutive states, operands from a
+// register window prev[s0-5 .. s0+SP+4]. INT: exact packed keys
+// (energy << 4 | offset index), whose minimum is the smallest energy and,
+// among ties, the earliest offset in list order — the strict-'<' scan of
+// dp.hpp:43-51. Otherwise doubles with the reference's scan verbatim.
+template <int SP, bool INT>
+__device__ __forceinline__ void upath_stage(const void* prevv, void* curv, const int* cnt,
+                                            int8_t* ch, int C, const double* pen,
+                                            const int* pen_i, double nrv, int nrv_i) {
+    const int s0 = threadIdx.x * SP;
+    if (s0 >= C) return;
+    if (INT) {
+        const int* prev = (const int*)prevv;
+        int* cur = (int*)curv;
+        int wv[SP + 10];
+#pragma unroll
+        for (int k = 0; k < SP + 10; ++k) {
+            const int idx = s0 - 5 + k;
+            wv[k] = (idx >= 0 && idx < C) ? prev[idx] : (1 << 26);
+        }
+#pragma unroll
+        for (int j = 0; j < SP; ++j) {
+            const int s = s0 + j;
+            if (s >= C) break;
+            int best = 0x7fffffff;
+#pragma unroll
+            for (int oi = 0; oi < 11; ++oi) {
+                const int off = (oi & 1) ? -((oi + 1) >> 1) : (oi >> 1);
+                best = min(best, (wv[j + 5 + off] + pen_i[oi]) * 16 + oi);
+            }
+            cur[s] = (best >> 4) + nrv_i * cnt[s];
+            const int oi = best & 15;
+            ch[s] = (int8_t)((oi & 1) ? -((oi + 1) >> 1) : (oi >> 1));
+        }
+    } else {
+        const double* prev = (const double*)prevv;
+        double* cur = (double*)curv;
+        double wv[SP + 10];
+#pragma unroll
+        for (int k = 0; k < SP + 10; ++k) {
+            const int idx = s0 - 5 + k;
+            wv[k] = (idx >= 0 && idx < C) ? prev[idx] : __longlong_as_double(0x7ff0000000000000LL);
+        }
+#pragma unroll
+        for (int j = 0; j < SP; ++j) {
+            const int s = s0 + j;
+            if (s >= C) break;
+            double best = __longlong_as_double(0x7ff0000000000000LL);
+            int bo = 0;
+#pragma unroll
+            for (int oi = 0; oi < 11; ++oi) {
+                const int off = (oi & 1) ? -((oi + 1) >> 1) : (oi >> 1);
+                const double e = wv[j + 5 + off] + pen[oi];
+                if (e < best) {
+                    best = e;
+                    bo = off;
+                }
+            }
+            cur[s] = best + nrv * cnt[s];
+            ch[s] = (int8_t)bo;
+        }
+    }
+}
+
+template <int SP>
 __global__ void __launch_bounds__(K4_THREADS) k_vanish(Dev d) {
     extern __shared__ double sh4[];
     const int f = blockIdx.x;
@@ -691,10 +797,18 @@ __global__ void __launch_bounds__(K4_THREADS) k_vanish(Dev d) {
 #pragma unroll
     for (int o = 0; o < 11; ++o)
         pen[o] = d.paper_sign ? d.lambda_x * offs[o] : d.lambda_x * abs(offs[o]);
+    int pen_i[11];
+#pragma unroll
+    for (int o = 0; o < 11; ++o) pen_i[o] = (int)pen[o];
     for (int c = threadIdx.x; c < C; c += blockDim.x) cnt[c] = 0;
     if (threadIdx.x == 0) s_votes = 0;
     __syncthreads();
     const double nrv = -d.rho_vote;
+    // exact int32 path: integral lambda_x / rho_vote and |energies| < 2^25
+    const double lx = d.lambda_x, rv = d.rho_vote;
+    const bool use_int = SP > 0 && lx == floor(lx) && rv == floor(rv) && lx < 1e6 && rv < 1e6 &&
+                         (double)nrows * (rv * (double)d.aux[f].votes + 5.0 * lx) < 33554432.0;
+    const int nrv_i = use_int ? -(int)rv : 0;
     int top_cur = v_max + 1, bot_cur = v_max;
     int my_votes = 0;
     for (int stg = 0; stg < nrows; ++stg) {
@@ -733,7 +847,16 @@ __global__ void __launch_bounds__(K4_THREADS) k_vanish(Dev d) {
             for (int c = threadIdx.x; c < C; c += blockDim.x) arow[c] = nrv * cnt[c];
         }
         if (stg == 0) {
-            for (int c = threadIdx.x; c < C; c += blockDim.x) prev[c] = nrv * cnt[c];
+            if (use_int)
+                for (int c = threadIdx.x; c < C; c += blockDim.x) ((int*)prev)[c] = nrv_i * cnt[c];
+            else
+                for (int c = threadIdx.x; c < C; c += blockDim.x) prev[c] = nrv * cnt[c];
+        } else if (SP > 0) {
+            int8_t* ch = choice + (size_t)stg * C;
+            if (use_int)
+                upath_stage<(SP > 0 ? SP : 1), true>(prev, cur, cnt, ch, C, pen, pen_i, nrv, nrv_i);
+            else
+                upath_stage<(SP > 0 ? SP : 1), false>(prev, cur, cnt, ch, C, pen, pen_i, nrv, nrv_i);
         } else {
             int8_t* ch = choice + (size_t)stg * C;
             for (int s = threadIdx.x; s < C; s += blockDim.x) {
@@ -764,13 +887,15 @@ __global__ void __launch_bounds__(K4_THREADS) k_vanish(Dev d) {
     if ((threadIdx.x & 31) == 0 && my_votes) atomicAdd(&s_votes, my_votes);
     double mv = __longlong_as_double(0x7ff0000000000000LL);
     int mi = 0x7fffffff;
-    for (int s = threadIdx.x; s < C; s += blockDim.x)
-        if (prev[s] < mv) {
-            mv = prev[s];
+    for (int s = threadIdx.x; s < C; s += blockDim.x) {
+        const double e = use_int ? (double)((const int*)prev)[s] : prev[s];
+        if (e < mv) {
+            mv = e;
             mi = s;
         }
+    }
     const int term = block_argmin(mv, mi, sv, si);
-    const double energy = prev[term];
+    const double energy = use_int ? (double)((const int*)prev)[term] : prev[term];
     // backtrack (dp.hpp:67-71) in windows of BT_CHUNK stages staged in smem
     int p = term;
     if (threadIdx.x == 0) {
@@ -909,6 +1034,20 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
     const int W = d.W, H = d.H, nu = d.nu, vs = d.varsigma;
     const int u0 = blockIdx.x * M_TW, v0 = blockIdx.y * tile_h;
     const int v_top = (int)d.rep[f].horizon, v_max = H - 1;
+    // w_g is zero above v_top, so m1 vanishes on rows < v_top - vs - 1. Without
+    // hooks only rows >= v_top are ever read (energy, threshold): skip the rest.
+    const int first_row = d.hooks ? 0 : v_top;
+    if (v0 + tile_h <= first_row) return;
+    if (d.hooks && v0 + tile_h <= v_top - vs - 1) {
+        for (int i = threadIdx.x; i < tile_h * M_TW; i += blockDim.x) {
+            const int v = v0 + i / M_TW, u = u0 + i % M_TW;
+            if (v >= H || u >= W) continue;
+            const size_t gi = (size_t)f * d.px + (size_t)v * W + u;
+            d.m1[gi] = 0.0;
+            d.m0[gi] = 0.0;
+        }
+        return;
+    }
     // wg region rows [v0-1-vs, v0+tile_h+vs], cols [u0-1-nu, u0+M_TW+nu]
     const int gr0 = v0 - 1 - vs, gc0 = u0 - 1 - nu;
     const int GH = tile_h + 2 + 2 * vs, GW = M_TW + 2 + 2 * nu;
@@ -932,42 +1071,43 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
         }
     }
     __syncthreads();
+    // box sum, y-major / x-minor (lanes.hpp:46-60). Positions outside the image
+    // hold zeros in gw: adding +-0.0 to a running sum that starts at +0.0 never
+    // changes it, so summing them instead of skipping is bit-identical.
     for (int i = threadIdx.x; i < MH * MW; i += blockDim.x) {
         const int r = i / MW, c = i - r * MW;
-        const int v = v0 - 1 + r, u = u0 - 1 + c;
+        const double* g0 = gw + r * GW + c;  // row v-vs, col u-nu
         double s = 0.0;
-        if (v >= 0 && v < H && u >= 0 && u < W) {
-            for (int y = -vs; y <= vs; ++y) {
-                const int vv = v + y;
-                if (vv < 0 || vv >= H) continue;
-                const double* grow = gw + (vv - gr0) * GW;
-                for (int x = -nu; x <= nu; ++x) {
-                    const int uu = u + x;
-                    if (uu < 0 || uu >= W) continue;
-                    s += grow[uu - gc0];
-                }
-            }
-        }
+        for (int y = 0; y <= 2 * vs; ++y)
+            for (int x = 0; x <= 2 * nu; ++x) s += g0[y * GW + x];
         m0[i] = s;
     }
     __syncthreads();
     const int t_lo = max(0, v_top), t_hi = min(H - 1, v_max);
+    const int lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < tile_h * M_TW; i += blockDim.x) {
         const int r = i / M_TW, c = i - r * M_TW;
         const int v = v0 + r, u = u0 + c;
-        if (v >= H || u >= W) continue;
+        const bool live = v < H && u < W && v >= first_row;
         double m1 = 0.0;
-        if (v >= 1 && v < H - 1 && u >= 1 && u < W - 1) {
-            const double* a = m0 + r * MW + c;            // row v-1, col u-1
-            const double* b = a + MW;                      // row v
-            const double* cc = b + MW;                     // row v+1
+        if (live && v >= 1 && v < H - 1 && u >= 1 && u < W - 1) {
+            const double* a = m0 + r * MW + c;  // row v-1, col u-1
+            const double* b = a + MW;            // row v
+            const double* cc = b + MW;           // row v+1
             m1 = (a[2] - a[0]) + 2 * (b[2] - b[0]) + (cc[2] - cc[0]);
         }
-        const size_t gi = (size_t)f * d.px + (size_t)v * W + u;
-        d.m1[gi] = m1;
-        if (d.hooks) d.m0[gi] = m0[(r + 1) * MW + c + 1];
-        if (want_hist && v >= t_lo && v <= t_hi)
-            atomicAdd(&hist[(unsigned long long)__double_as_longlong(fabs(m1)) >> 52], 1u);
+        if (live) {
+            const size_t gi = (size_t)f * d.px + (size_t)v * W + u;
+            d.m1[gi] = m1;
+            if (d.hooks) d.m0[gi] = m0[(r + 1) * MW + c + 1];
+        }
+        if (want_hist) {
+            const bool in = live && v >= t_lo && v <= t_hi;
+            const unsigned bin = (unsigned)((unsigned long long)__double_as_longlong(fabs(m1)) >> 52);
+            const unsigned zb = __ballot_sync(__activemask(), in && bin == 0);
+            if (lane == 0 && zb) atomicAdd(&hist[0], (unsigned)__popc(zb));
+            if (in && bin != 0) atomicAdd(&hist[bin], 1u);
+        }
     }
     if (want_hist) {
         __syncthreads();
@@ -1278,10 +1418,20 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     else
         k_bilateral<-1><<<bg, 256, lp.bf_smem, s>>>(d);
     mark(9);
-    k_sobel_edges<<<dim3(d.H, n), 256, 0, s>>>(d);
-    k_edge_emit<<<dim3(d.H, n), 256, 0, s>>>(d);
+    k_sobel_edges<<<dim3((d.W + SB_TW - 1) / SB_TW, (d.H + SB_TH - 1) / SB_TH, n), 256, 0, s>>>(d);
+    k_edge_scan<<<n, 1024, 0, s>>>(d);
+    k_edge_emit<<<dim3((d.H * d.n_seg + 7) / 8, n), 256, 0, s>>>(d);
     mark(10);
-    k_vanish<<<n, K4_THREADS, lp.vanish_smem, s>>>(d);
+    switch (lp.upath_sp) {
+        case 1: k_vanish<1><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
+        case 2: k_vanish<2><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
+        case 3: k_vanish<3><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
+        case 4: k_vanish<4><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
+        case 5: k_vanish<5><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
+        case 6: k_vanish<6><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
+        case 8: k_vanish<8><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
+        default: k_vanish<0><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
+    }
     k_gamma_fit<<<n, 256, lp.gamma_smem, s>>>(d);
     mark(11);
     const bool auto_tr = isnan(d.tr_lpv);
@@ -1299,7 +1449,7 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     return cudaGetLastError();
 }
 
-int launches_per_batch(const Dev& d) { return isnan(d.tr_lpv) ? 15 : 12; }
+int launches_per_batch(const Dev& d) { return isnan(d.tr_lpv) ? 16 : 13; }
 
 cudaError_t configure_kernels(const LaunchPlan& lp) {
     cudaError_t e;
@@ -1315,9 +1465,11 @@ cudaError_t configure_kernels(const LaunchPlan& lp) {
     if ((e = cudaFuncSetAttribute(k_bilateral<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lp.bf_smem)))
         return e;
-    if ((e = cudaFuncSetAttribute(k_vanish, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  lp.vanish_smem)))
-        return e;
+    for (auto fn : {k_vanish<0>, k_vanish<1>, k_vanish<2>, k_vanish<3>, k_vanish<4>, k_vanish<5>,
+                    k_vanish<6>, k_vanish<8>})
+        if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      lp.vanish_smem)))
+            return e;
     if ((e = cudaFuncSetAttribute(k_gamma_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lp.gamma_smem)))
         return e;

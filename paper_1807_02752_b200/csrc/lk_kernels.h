@@ -15,6 +15,7 @@ constexpr int K4_THREADS = 1024;        // V_px CTA
 constexpr int BT_CHUNK = 32;            // u-path backtrack: stages per window
 constexpr int BT_SPAN = 5 * BT_CHUNK;   // max drift inside a window (|offset| <= 5)
 constexpr int M_TW = 128;               // m0/m1 tile width
+constexpr int SB_TW = 128, SB_TH = 8;   // Sobel tile; SB_TW is the edge-list segment width
 
 // 11x11 spatial weights exp(-ds*inv_s2), passed by value (constant bank)
 struct WsParam {
@@ -30,6 +31,7 @@ struct LaunchPlan {
     size_t bf_smem;
     size_t bt_smem;
     size_t vanish_smem;
+    int upath_sp;             // u-path DP states per thread (0 = strided fallback)
     size_t gamma_smem;
     size_t m_smem;
     int m_tile_h;
