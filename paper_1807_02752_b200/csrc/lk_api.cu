@@ -374,7 +374,8 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
             for (int i = 0; i < 121; ++i) lp.ws.w[i] = ws[i];
     }
     lp.vanish_smem = (size_t)2 * C * 8 + (size_t)C * 4 + (size_t)2 * H * 4 +
-                     (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 16;
+                     (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 8 + (size_t)(H + 1) * 4 +
+                     (size_t)lkg::K4_VOTE_CAP * 2 + 16;
     lp.upath_sp = (C + lkg::K4_THREADS - 1) / lkg::K4_THREADS;
     if (lp.upath_sp == 7) lp.upath_sp = 8;
     if (lp.upath_sp > 8) lp.upath_sp = 0;

@@ -525,9 +525,24 @@ __global__ void __launch_bounds__(256) k_sobel_edges(Dev d) {
     const int W = d.W, H = d.H;
     const int u0 = blockIdx.x * SB_TW, v0 = blockIdx.y * SB_TH;
     const double* img = d.smoothed + (size_t)f * d.px;
-    for (int i = threadIdx.x; i < (SB_TH + 2) * SW; i += blockDim.x) {
-        const int r = i / SW, c = i - r * SW;
-        s_img[i] = img[(size_t)mirror(v0 - 1 + r, H) * W + mirror(u0 - 1 + c, W)];
+    __shared__ int s_col[SW];
+    __shared__ int s_row[SB_TH + 2];
+    for (int i = threadIdx.x; i < SW; i += blockDim.x) s_col[i] = mirror(u0 - 1 + i, W);
+    if (threadIdx.x < SB_TH + 2) s_row[threadIdx.x] = mirror(v0 - 1 + threadIdx.x, H) * W;
+    __syncthreads();
+    {  // all loads in flight before the stores
+        constexpr int NE = ((SB_TH + 2) * SW + 255) / 256;
+        double t[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int i = threadIdx.x + k * 256;
+            if (i < (SB_TH + 2) * SW) t[k] = img[(size_t)s_row[i / SW] + s_col[i % SW]];
+        }
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int i = threadIdx.x + k * 256;
+            if (i < (SB_TH + 2) * SW) s_img[i] = t[k];
+        }
     }
     if (threadIdx.x < SB_TH) s_seg[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_tot[threadIdx.x] = 0;
@@ -772,7 +787,7 @@ __device__ __forceinline__ void upath_stage(const void* prevv, void* curv, const
 }
 
 template <int SP>
-__global__ void __launch_bounds__(K4_THREADS) k_vanish(Dev d) {
+__global__ void __launch_bounds__(K4_THREADS, 2) k_vanish(Dev d) {
     extern __shared__ double sh4[];
     const int f = blockIdx.x;
     if (frame_failed(d, f)) return;
@@ -786,12 +801,24 @@ __global__ void __launch_bounds__(K4_THREADS) k_vanish(Dev d) {
     int* px = cnt + C;
     int* pv = px + H;
     int8_t* win = (int8_t*)(pv + H);  // [BT_CHUNK][2*BT_SPAN+1]
+    int* s_roff = (int*)(win + BT_CHUNK * (2 * BT_SPAN + 1) + 4 - (BT_CHUNK * (2 * BT_SPAN + 1)) % 4);
+    uint16_t* s_vcol = (uint16_t*)(s_roff + H + 1);  // [K4_VOTE_CAP] vote column - ext_lo
     __shared__ double sv[32];
     __shared__ int si[32];
     __shared__ int s_votes;
-    const int32_t* roff = d.row_off + (size_t)f * (H + 1);
+    const int32_t* groff = d.row_off + (size_t)f * (H + 1);
     const int32_t* ecol = d.e_col + (size_t)f * d.px;
     int8_t* choice = d.uchoice + (size_t)f * H * C;
+    // per-row vote lists staged once (the band updates of every stage read them)
+    const int e_first = groff[v_top], n_edges_in = groff[H] - e_first;
+    const bool staged = n_edges_in <= K4_VOTE_CAP;
+    for (int r = threadIdx.x; r <= H; r += blockDim.x) s_roff[r] = groff[r];
+    if (staged)
+        for (int e = threadIdx.x; e < n_edges_in; e += blockDim.x) {
+            const int c = ecol[e_first + e];
+            s_vcol[e] = c == kSkipCol ? (uint16_t)0xffff : (uint16_t)(c - d.ext_lo);
+        }
+    const int* roff = s_roff;
     double pen[11];
     const int offs[11] = {0, -1, 1, -2, 2, -3, 3, -4, 4, -5, 5};
 #pragma unroll
@@ -826,9 +853,10 @@ __global__ void __launch_bounds__(K4_THREADS) k_vanish(Dev d) {
         }
         if (bt < top_cur) {  // rows entering at the top: [bt, top_cur)
             for (int e = roff[bt] + threadIdx.x; e < roff[top_cur]; e += blockDim.x) {
-                const int c = ecol[e];
-                if (c != kSkipCol) {
-                    atomicAdd(&cnt[c - d.ext_lo], 1);
+                const int c = staged ? (int)s_vcol[e - e_first]
+                                     : (ecol[e] == kSkipCol ? 0xffff : ecol[e] - d.ext_lo);
+                if (c != 0xffff) {
+                    atomicAdd(&cnt[c], 1);
                     ++my_votes;
                 }
             }
@@ -836,8 +864,9 @@ __global__ void __launch_bounds__(K4_THREADS) k_vanish(Dev d) {
         top_cur = bt;
         if (bb < bot_cur) {  // rows leaving at the bottom: (bb, bot_cur]
             for (int e = roff[bb + 1] + threadIdx.x; e < roff[bot_cur + 1]; e += blockDim.x) {
-                const int c = ecol[e];
-                if (c != kSkipCol) atomicSub(&cnt[c - d.ext_lo], 1);
+                const int c = staged ? (int)s_vcol[e - e_first]
+                                     : (ecol[e] == kSkipCol ? 0xffff : ecol[e] - d.ext_lo);
+                if (c != 0xffff) atomicSub(&cnt[c], 1);
             }
         }
         bot_cur = bb;
@@ -942,7 +971,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_vanish(Dev d) {
 // (:276-281), then the w_g edge weights of build_m0 (lanes.hpp:35-44).
 // One CTA per frame; warp 0 runs the RANSAC.
 // =====================================================================
-__global__ void __launch_bounds__(256) k_gamma_fit(Dev d) {
+__global__ void __launch_bounds__(256, 4) k_gamma_fit(Dev d) {
     extern __shared__ int sh_g[];
     const int f = blockIdx.x;
     if (frame_failed(d, f)) return;

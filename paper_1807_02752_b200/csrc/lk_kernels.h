@@ -11,7 +11,8 @@ constexpr int K1_ROWS = 8;              // rows per v-disparity CTA
 constexpr int BF_TW = 32, BF_TH = 8;    // bilateral tile (generic window)
 constexpr int BT_W = 64, BT_H = 16, BT_R = 4;  // bilateral tile (11x11), outputs per thread
 constexpr int BT_TRI_N = 128;           // max distinct values per tile for the smem sub-table
-constexpr int K4_THREADS = 1024;        // V_px CTA
+constexpr int K4_THREADS = 512;         // V_px CTA (2 per SM)
+constexpr int K4_VOTE_CAP = 8192;       // edges whose vote columns are staged in smem
 constexpr int BT_CHUNK = 32;            // u-path backtrack: stages per window
 constexpr int BT_SPAN = 5 * BT_CHUNK;   // max drift inside a window (|offset| <= 5)
 constexpr int M_TW = 128;               // m0/m1 tile width
