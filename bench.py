@@ -188,7 +188,9 @@ def run_reference(args):
         "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": dt / steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": desc.replace(f"batch of {B}", f"sample of {per_step}"),
+        "config": {"workload": desc.replace(f"batch of {B}", f"sample of {per_step}").replace(
+                       "stages 5-12 in one CUDA graph",
+                       "stages 5-12 by the reference's CPU code (lanekit headers)"),
                    "frames_per_step": per_step, "width": W, "height": H,
                    "parallelism": f"frame-parallel on {cores} host threads"},
         "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": kind,
@@ -271,15 +273,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)
 
-    if world > 1:
-        import torch.distributed as dist
+    from paper_1807_02752_b200 import shard
 
-        t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms, e2e_ms = float(t[0]), float(t[1])
-        f = torch.tensor([failed], dtype=torch.int64)
-        dist.all_reduce(f)
-        failed = int(f[0])
+    dev_ms, e2e_ms = shard.max_over_ranks([dev_ms, e2e_ms])  # slowest GPU sets the time
+    (failed,) = shard.sum_over_ranks([failed])
 
     fps = world * B * args.steps / (dev_ms * 1e-3)
     e2e_fps = world * B * e2_steps / (e2e_ms * 1e-3)

@@ -1,6 +1,9 @@
 // oracle_capi.cpp — TEST INFRASTRUCTURE ONLY. C entry points of the CPU
 // restatement (liblk_oracle.so) for the pytest parity suite (ctypes).
+#include <algorithm>
 #include <atomic>
+#include <climits>
+#include <cmath>
 #include <vector>
 
 #include "lk_oracle.hpp"
@@ -73,6 +76,166 @@ void orc_lane_track(double u, const double* vpx, const double* vpy, int v_top, i
 
 double orc_auto_lane_threshold(const double* m1, int W, int H, int v_top, int v_max) {
     return orc::auto_lane_threshold(m1, W, H, v_top, v_max);
+}
+
+}  // extern "C"
+
+// ---- more unit-level restatements for the known-answer tests
+namespace {
+
+// road_profile.hpp:161-176
+int horizon_row(const double* b, int rows, int* in_range) {
+    double root;
+    *in_range = 0;
+    if (b[2] == 0) {
+        if (b[1] <= 0) return 0;
+        root = -b[0] / b[1];
+    } else {
+        const double disc = b[1] * b[1] - 4 * b[2] * b[0];
+        if (disc <= 0) return 0;
+        root = (-b[1] + std::sqrt(disc)) / (2 * b[2]);
+    }
+    const long long r = std::llround(root);
+    if (r < 0 || r >= rows) return 0;
+    *in_range = 1;
+    return static_cast<int>(r);
+}
+
+}  // namespace
+
+extern "C" {
+
+int orc_horizon_row(const double* beta, int rows, int32_t* in_range) {
+    int ir = 0;
+    const int r = horizon_row(beta, rows, &ir);
+    *in_range = ir;
+    return r;
+}
+
+// road_profile.hpp:184-199
+void orc_vpy_profile(const double* b, int rows, double* value, uint8_t* singular) {
+    for (int v = 0; v < rows; ++v) {
+        const double vv = static_cast<double>(v);
+        const double fp = b[1] + 2 * b[2] * vv;
+        if (std::abs(fp) < 1e-12) {
+            singular[v] = 1;
+            value[v] = vv;
+            continue;
+        }
+        singular[v] = 0;
+        value[v] = vv - (b[0] + b[1] * vv + b[2] * vv * vv) / fp;
+    }
+}
+
+// vanish.hpp:24-30
+int orc_extended_col_lo(double xi, int width) {
+    return -static_cast<int>(std::llround(xi * width));
+}
+int orc_extended_col_count(double xi, int width) {
+    return static_cast<int>(std::llround((2 * xi + 1) * width));
+}
+
+// vanish.hpp:49-70 for explicit edges (u, v, gx, gy); returns the vote count,
+// cols_out[i] = vote column or INT32_MIN for a skipped edge.
+int orc_sparse_vpx(const int32_t* uv, const double* g, int n, const double* vpy,
+                   const uint8_t* singular, int rows, double xi, int width, int32_t* cols_out) {
+    const int lo = orc_extended_col_lo(xi, width);
+    const int hi = lo + orc_extended_col_count(xi, width) - 1;
+    int votes = 0;
+    for (int i = 0; i < n; ++i) {
+        const int u = uv[2 * i], v = uv[2 * i + 1];
+        const double gx = g[2 * i], gy = g[2 * i + 1];
+        if (v < 0 || v >= rows || singular[v] || std::abs(gx) < 1e-3) {
+            cols_out[i] = INT32_MIN;
+            continue;
+        }
+        const double col = u + (v - vpy[v]) * (gy / gx);
+        const long long c = std::llround(col);
+        cols_out[i] = static_cast<int>(std::clamp(c, static_cast<long long>(lo),
+                                                  static_cast<long long>(hi)));
+        ++votes;
+    }
+    return votes;
+}
+
+// vanish.hpp:113-148 (sliding band) for explicit votes (col, row); acc is
+// [(v_max - v_top + 1)][ext_cols].
+void orc_accumulate(const int32_t* col_row, int n, int ext_lo, int ext_cols, int v_top,
+                    int v_max, int chi, double rho_vote, double* acc) {
+    const int nrows = v_max - v_top + 1;
+    std::vector<std::vector<int>> by_row(nrows);
+    for (int i = 0; i < n; ++i) {
+        const int c = col_row[2 * i], r = col_row[2 * i + 1];
+        if (r < v_top || r > v_max) continue;
+        by_row[r - v_top].push_back(c - ext_lo);
+    }
+    std::vector<int32_t> cnt(ext_cols, 0);
+    int top_cur = v_max + 1, bot_cur = v_max;
+    for (int v = v_max; v >= v_top; --v) {
+        int bt, bb;
+        if (v > v_max - chi - 1) {
+            bt = v;
+            bb = v_max;
+        } else if (v >= v_top + chi) {
+            bt = v - chi;
+            bb = v + chi;
+        } else {
+            bt = v_top;
+            bb = v + chi;
+        }
+        for (int r = bt; r < top_cur; ++r)
+            for (int c : by_row[r - v_top]) ++cnt[c];
+        top_cur = bt;
+        for (int r = bb + 1; r <= bot_cur; ++r)
+            for (int c : by_row[r - v_top]) --cnt[c];
+        bot_cur = bb;
+        double* row = acc + static_cast<size_t>(v - v_top) * ext_cols;
+        for (int c = 0; c < ext_cols; ++c) row[c] = -rho_vote * cnt[c];
+    }
+}
+
+// lanes.hpp:106-129 on an explicit m1 map and V_p profile.
+void orc_aggregate_energy(const double* m1, int W, int H, const double* vpx, const double* vpy,
+                          int v_top, int v_max, double xi, double lambda_g, double* out) {
+    const int lo = orc_extended_col_lo(xi, W), cols = orc_extended_col_count(xi, W);
+    std::vector<double> track(v_max - v_top + 1);
+    for (int ci = 0; ci < cols; ++ci) {
+        orc::lane_track(static_cast<double>(lo + ci), vpx, vpy, v_top, v_max, track.data());
+        double e = 0;
+        for (int v = v_max; v >= v_top; --v) {
+            double contrib = 0;
+            const double tu = track[v - v_top];
+            if (!std::isnan(tu)) {
+                const long long r = std::llround(tu);
+                if (r >= 0 && r < W && v >= 0 && v < H)
+                    contrib = m1[static_cast<size_t>(v) * W + static_cast<int>(r)];
+            }
+            e = contrib + lambda_g * e;
+        }
+        out[ci] = e;
+    }
+}
+
+// lanes.hpp:144-178 minus the polylines: kept histogram indices, strongest first.
+int orc_select_lanes(const double* h, int n, double tr, int min_sep, int32_t* kept_out) {
+    std::vector<int> cand;
+    for (int i = 1; i + 1 < n; ++i)
+        if (h[i] < h[i - 1] && h[i] < h[i + 1] && h[i] < tr) cand.push_back(i);
+    std::sort(cand.begin(), cand.end(), [&](int a, int b) {
+        if (h[a] != h[b]) return h[a] < h[b];
+        return a < b;
+    });
+    int nk = 0;
+    for (int i : cand) {
+        bool close = false;
+        for (int k = 0; k < nk; ++k)
+            if (std::abs(i - kept_out[k]) < min_sep) {
+                close = true;
+                break;
+            }
+        if (!close) kept_out[nk++] = i;
+    }
+    return nk;
 }
 
 }  // extern "C"

@@ -146,6 +146,67 @@ class Checker:
         return self.lib.orc_auto_lane_threshold(np.ascontiguousarray(m1, np.float64), W, H,
                                                 v_top, v_max)
 
+    def horizon_row(self, beta, rows):
+        ir = C.c_int32(0)
+        f = self.lib.orc_horizon_row
+        f.argtypes = [_f64p, C.c_int, C.POINTER(C.c_int32)]
+        r = f(np.asarray(beta, np.float64), rows, C.byref(ir))
+        return r, bool(ir.value)
+
+    def vpy_profile(self, beta, rows):
+        val = np.zeros(rows, np.float64)
+        sing = np.zeros(rows, np.uint8)
+        f = self.lib.orc_vpy_profile
+        f.argtypes = [_f64p, C.c_int, _f64p, np.ctypeslib.ndpointer(np.uint8)]
+        f(np.asarray(beta, np.float64), rows, val, sing)
+        return val, sing
+
+    def extended_cols(self, xi, width):
+        self.lib.orc_extended_col_lo.argtypes = [C.c_double, C.c_int]
+        self.lib.orc_extended_col_count.argtypes = [C.c_double, C.c_int]
+        return self.lib.orc_extended_col_lo(xi, width), self.lib.orc_extended_col_count(xi, width)
+
+    def sparse_vpx(self, edges, vpy, singular, xi, width):
+        """edges: [(u, v, gx, gy)] -> (vote columns (None = skipped), votes)."""
+        uv = np.ascontiguousarray([[e[0], e[1]] for e in edges], np.int32)
+        g = np.ascontiguousarray([[e[2], e[3]] for e in edges], np.float64)
+        out = np.zeros(len(edges), np.int32)
+        f = self.lib.orc_sparse_vpx
+        f.argtypes = [_i32p, _f64p, C.c_int, _f64p, np.ctypeslib.ndpointer(np.uint8), C.c_int,
+                      C.c_double, C.c_int, _i32p]
+        n = f(uv, g, len(edges), np.asarray(vpy, np.float64),
+              np.ascontiguousarray(singular, np.uint8), len(vpy), xi, width, out)
+        cols = [None if c == np.iinfo(np.int32).min else int(c) for c in out]
+        return cols, n
+
+    def accumulate(self, votes, ext_lo, ext_cols, v_top, v_max, chi, rho_vote):
+        cr = np.ascontiguousarray(votes, np.int32).reshape(-1, 2)
+        acc = np.zeros((v_max - v_top + 1, ext_cols), np.float64)
+        f = self.lib.orc_accumulate
+        f.argtypes = [_i32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                      _f64p]
+        f(cr, len(cr), ext_lo, ext_cols, v_top, v_max, chi, rho_vote, acc)
+        return acc
+
+    def aggregate_energy(self, m1, vpx, vpy, v_top, v_max, xi, lambda_g):
+        H, W = m1.shape
+        lo, n = self.extended_cols(xi, W)
+        out = np.zeros(n, np.float64)
+        f = self.lib.orc_aggregate_energy
+        f.argtypes = [_f64p, C.c_int, C.c_int, _f64p, _f64p, C.c_int, C.c_int, C.c_double,
+                      C.c_double, _f64p]
+        f(np.ascontiguousarray(m1, np.float64), W, H, np.asarray(vpx, np.float64),
+          np.asarray(vpy, np.float64), v_top, v_max, xi, lambda_g, out)
+        return lo, out
+
+    def select_lanes(self, h, tr, min_sep):
+        h = np.ascontiguousarray(h, np.float64)
+        kept = np.zeros(len(h), np.int32)
+        f = self.lib.orc_select_lanes
+        f.argtypes = [_f64p, C.c_int, C.c_double, C.c_int, _i32p]
+        k = f(h, len(h), tr, min_sep, kept)
+        return kept[:k].tolist()
+
 
 class CheckerResult:
     def __init__(self, chk: Checker, handle, W, H, cfg):

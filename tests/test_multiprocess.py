@@ -1,0 +1,74 @@
+"""The N>1 path on CPU: two gloo ranks shard the frames, each processes its
+contiguous range (with the CPU oracle standing in for the GPU, which this
+container does not have), timings are max-reduced and the lane records are
+gathered on rank 0 — and must equal a single-process run frame for frame."""
+import os
+import socket
+import sys
+from pathlib import Path
+
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n_frames, out_path):
+    sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import json
+
+    import torch.distributed as dist
+
+    from checkers import Checker
+    from paper_1807_02752_b200 import lanekit, scenes, shard
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard.shard_range(n_frames, rank, world)
+    params = [scenes.acceptance_scene(i) for i in range(lo, hi)]
+    grey, disp = lanekit.synth_batch(params, threads=2)
+    reps = Checker("oracle").run_batch(grey, disp, scenes.acceptance_config(), threads=2)
+    recs = shard.gather_records([shard.lane_record(r) for r in reps])
+    t = shard.max_over_ranks([float(rank + 1), 10.0 * (world - rank)])
+    f = shard.sum_over_ranks([sum(r.status != 0 for r in reps), hi - lo])
+    if rank == 0:
+        Path(out_path).write_text(json.dumps({"records": recs, "t": t, "f": f}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_ranges_partition():
+    from paper_1807_02752_b200 import shard
+
+    for n in (1, 7, 256, 65536):
+        for world in (1, 2, 4, 8):
+            ranges = [shard.shard_range(n, g, world) for g in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+
+
+def test_two_rank_gloo_shards_match_single_process(tmp_path):
+    import json
+
+    from checkers import Checker
+    from paper_1807_02752_b200 import lanekit, scenes, shard
+
+    n = 6
+    out = tmp_path / "rank0.json"
+    mp.spawn(_worker, args=(2, _free_port(), n, str(out)), nprocs=2, join=True)
+    got = json.loads(out.read_text())
+    params = [scenes.acceptance_scene(i) for i in range(n)]
+    grey, disp = lanekit.synth_batch(params, threads=2)
+    reps = Checker("oracle").run_batch(grey, disp, scenes.acceptance_config(), threads=2)
+    want = [shard.lane_record(r) for r in reps]
+    assert json.loads(json.dumps(want)) == got["records"]
+    assert got["t"] == [2.0, 20.0]      # max over ranks
+    assert got["f"] == [0, n]           # failures summed, frames summed
