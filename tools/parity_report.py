@@ -58,8 +58,13 @@ def main():
                     print(f"   {name:14s} n={len(g)}/{len(ov)} exact={same}")
                     continue
                 ex = exact_fraction(g, ov) if g.shape == ov.shape else -1
+                rel = 0.0
+                if g.shape == ov.shape and g.dtype.kind == "f":
+                    a, b = np.asarray(g, float), np.asarray(ov, float)
+                    m = ~(np.isnan(a) | np.isnan(b)) & (b != 0)
+                    rel = float(np.max(np.abs(a[m] - b[m]) / np.abs(b[m]))) if m.any() else 0.0
                 print(f"   {name:14s} shape {g.shape} vs {ov.shape} exact {ex:.6f} "
-                      f"close {close(g, ov) if g.shape == ov.shape else False}")
+                      f"max_rel {rel:.3e} close {close(g, ov) if g.shape == ov.shape else False}")
 
 
 if __name__ == "__main__":
