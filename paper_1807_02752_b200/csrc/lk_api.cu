@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -369,7 +370,10 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     {
         const size_t twh = lkg::BT_W + 10, thh = lkg::BT_H + 10, npx = twh * thh;
         const size_t tri = (size_t)lkg::BT_TRI_N * (lkg::BT_TRI_N + 1) / 2;
-        lp.bt_smem = tri * 8 + npx * 8 + npx * 4 + 2 * 256 * 4 + npx + 256 + 16;
+        const char* m = std::getenv("LK_BILATERAL_MODE");
+        lp.bt_mode = m ? std::atoi(m) : 0;
+        const bool table = lp.bt_mode == 0 || lp.bt_mode == 3;
+        lp.bt_smem = (table ? tri * 8 : 0) + npx * 8 + npx * 4 + 2 * 256 * 4 + npx + 256 + 16;
         if (win == 11)
             for (int i = 0; i < 121; ++i) lp.ws.w[i] = ws[i];
     }
@@ -402,6 +406,18 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         return s;
     }
     cudaError_t e = lkg::configure_kernels(lp);
+    if (e == cudaSuccess) {  // texture view of the exact weight table (TEX-pipe gathers)
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeLinear;
+        rd.res.linear.devPtr = d_wr;
+        rd.res.linear.desc = cudaCreateChannelDesc<int2>();
+        rd.res.linear.sizeInBytes = wr.size() * 8;
+        cudaTextureDesc td{};
+        td.readMode = cudaReadModeElementType;
+        cudaTextureObject_t tex = 0;
+        e = cudaCreateTextureObject(&tex, &rd, &td, nullptr);
+        d.wr_tex = tex;
+    }
     if (e == cudaSuccess) e = cudaMemcpy(d_ws, ws.data(), ws.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d_wr, wr.data(), wr.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d_val, val.data(), val.size() * 8, cudaMemcpyHostToDevice);
@@ -421,6 +437,7 @@ lk_status lk_destroy(lk_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    if (c->d.wr_tex) cudaDestroyTextureObject((cudaTextureObject_t)c->d.wr_tex);
     for (cudaEvent_t e : c->ev)
         if (e) cudaEventDestroy(e);
     for (void* p : c->allocs) cudaFree(p);

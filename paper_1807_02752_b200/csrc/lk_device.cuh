@@ -47,6 +47,7 @@ struct Dev {
     // tables built on the host with the reference's libm
     const double* ws;       // [win*win] exp(-ds*inv_s2)
     const double* wr;       // [256][256] exp(-dr*dr*inv_r2)
+    unsigned long long wr_tex;  // texture object over wr (int2 texels)
     const double* val;      // [256] k/255.0
     const uint64_t* rng;    // mt19937_64(seed) outputs 0..max_iter*5-1
     // outputs / intermediates
@@ -120,8 +121,12 @@ __device__ __forceinline__ void fail_frame(const Dev& d, int f, int stage, int m
     r.err_row = row;
 }
 
+// Rounds up to 8-byte alignment by pointer arithmetic (not an integer
+// round-trip), so the compiler keeps the shared-memory address space and
+// emits LDS/STS rather than generic LD/ST.
 __device__ __forceinline__ double* align8(void* p) {
-    return (double*)(((uintptr_t)p + 7) & ~(uintptr_t)7);
+    char* c = (char*)p;
+    return (double*)(c + ((8 - ((uintptr_t)c & 7)) & 7));
 }
 
 // Ordered double -> u64 key (total order equal to '<' for non-NaN values).

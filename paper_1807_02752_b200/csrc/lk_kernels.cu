@@ -360,7 +360,11 @@ __global__ void __launch_bounds__(256) k_bilateral(Dev d) {
 // (conflict-free, consecutive lanes) and folded into every output whose
 // window contains it, still in the reference's j-major / i-minor order.
 // ---------------------------------------------------------------------
-template <int RHO, bool SMEM_TABLE>
+// Table-lookup mode of the tiled bilateral (a profiling experiment kept as a
+// switch): 0 = exact sub-table in shared memory (LSU pipe); 1 = the full
+// table via __ldg; 2 = the full table via tex1Dfetch (TEX pipe); 3 = hybrid,
+// even taps from shared memory, odd taps through the texture path.
+template <int RHO, int MODE>
 __device__ __forceinline__ void bilateral_rows(const Dev& d, const WsParam& ws,
                                                const double* s_sub, const int* s_map,
                                                const double* s_v, const uint32_t* s_kt,
@@ -368,14 +372,13 @@ __device__ __forceinline__ void bilateral_rows(const Dev& d, const WsParam& ws,
     constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO;
     const int tx = threadIdx.x % BT_W, ty = threadIdx.x / BT_W;
     const int r0 = ty * BT_R;
-    int ca[BT_R], ta[BT_R];
-    const double* grow[BT_R];
+    int ca[BT_R], ta[BT_R], craw[BT_R];
 #pragma unroll
     for (int r = 0; r < BT_R; ++r) {
         const int kc = s_g[(r0 + r + RHO) * TWh + tx + RHO];
-        ca[r] = SMEM_TABLE ? s_map[kc] : kc;
+        craw[r] = kc * 256;
+        ca[r] = (MODE == 0 || MODE == 3) ? s_map[kc] : 0;
         ta[r] = (ca[r] * (ca[r] + 1)) >> 1;
-        grow[r] = d.wr + kc * 256;
     }
     double num[BT_R], den[BT_R];
 #pragma unroll
@@ -396,13 +399,17 @@ __device__ __forceinline__ void bilateral_rows(const Dev& d, const WsParam& ws,
             if (dj < 0 || dj >= WIN) continue;
 #pragma unroll
             for (int i = 0; i < WIN; ++i) {
-                const int b = (int)(kt[i] & 0xffu);
+                const int b = (int)(kt[i] & 0xffu);            // local index
+                const int raw = (int)((kt[i] >> 8) & 0xffu);   // 8-bit value
                 double wrv;
-                if (SMEM_TABLE) {
-                    const int tb = (int)(kt[i] >> 8);
+                if (MODE == 0 || (MODE == 3 && (i & 1) == 0)) {
+                    const int tb = (int)(kt[i] >> 16);
                     wrv = s_sub[b <= ca[r] ? ta[r] + b : tb + ca[r]];
+                } else if (MODE == 1) {
+                    wrv = __ldg(d.wr + craw[r] + raw);
                 } else {
-                    wrv = __ldg(grow[r] + b);
+                    const int2 t = tex1Dfetch<int2>((cudaTextureObject_t)d.wr_tex, craw[r] + raw);
+                    wrv = __hiloint2double(t.y, t.x);
                 }
                 const double w = ws.w[dj * WIN + i] * wrv;
                 num[r] += w * vv[i];
@@ -418,19 +425,18 @@ __device__ __forceinline__ void bilateral_rows(const Dev& d, const WsParam& ws,
     }
 }
 
-template <int RHO>
+template <int RHO, int MODE>
 __global__ void __launch_bounds__(256, 2) k_bilateral_tile(Dev d, WsParam ws) {
     constexpr int TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
     constexpr int NPX = TWh * THh;
-    constexpr int TRI = BT_TRI_N * (BT_TRI_N + 1) / 2;
     extern __shared__ double sm_bt[];
-    double* s_sub = sm_bt;                       // [TRI] symmetric exact sub-table
-    double* s_v = s_sub + TRI;                   // [NPX] neighbour values k/255.0
-    uint32_t* s_kt = (uint32_t*)(s_v + NPX);     // [NPX] local index | tri(index) << 8
+    double* s_v = sm_bt;                         // [NPX] neighbour values k/255.0
+    uint32_t* s_kt = (uint32_t*)(s_v + NPX);     // [NPX] local | value << 8 | tri(local) << 16
     int* s_map = (int*)(s_kt + NPX);             // [256] value -> local index
     int* s_inv = s_map + 256;                    // [256] local index -> value
     uint8_t* s_g = (uint8_t*)(s_inv + 256);      // [NPX] raw 8-bit grey
     uint8_t* s_fv = s_g + NPX;                   // [256] value present
+    double* s_sub = align8(s_fv + 256);          // [TRI] symmetric exact sub-table (MODE 0/3)
     __shared__ int s_warp[8];
     __shared__ int s_n;
     const int f = blockIdx.z;
@@ -448,6 +454,12 @@ __global__ void __launch_bounds__(256, 2) k_bilateral_tile(Dev d, WsParam ws) {
         s_fv[k] = 1;  // benign race: every writer stores 1
     }
     __syncthreads();
+    if (MODE == 1 || MODE == 2) {
+        for (int i = threadIdx.x; i < NPX; i += blockDim.x) s_kt[i] = (uint32_t)s_g[i] << 8;
+        __syncthreads();
+        bilateral_rows<RHO, MODE>(d, ws, s_sub, s_map, s_v, s_kt, s_g, f, u0, v0);
+        return;
+    }
     {  // exclusive scan of the presence vector -> value <-> local index
         const int t = threadIdx.x, lane = t & 31, w = t >> 5;
         const int fv = s_fv[t];
@@ -467,8 +479,7 @@ __global__ void __launch_bounds__(256, 2) k_bilateral_tile(Dev d, WsParam ws) {
     }
     __syncthreads();
     const int nv = s_n;
-    const bool smem_table = nv <= BT_TRI_N;
-    if (smem_table) {
+    if (nv <= BT_TRI_N) {
         const int ntri = nv * (nv + 1) / 2;
         for (int e = threadIdx.x; e < ntri; e += blockDim.x) {
             // e = b(b+1)/2 + a, a <= b
@@ -479,17 +490,16 @@ __global__ void __launch_bounds__(256, 2) k_bilateral_tile(Dev d, WsParam ws) {
             s_sub[e] = __ldg(d.wr + s_inv[a] * 256 + s_inv[b]);
         }
         for (int i = threadIdx.x; i < NPX; i += blockDim.x) {
-            const uint32_t b = (uint32_t)s_map[s_g[i]];
-            s_kt[i] = b | (((b * (b + 1)) >> 1) << 8);
+            const uint32_t raw = s_g[i], b = (uint32_t)s_map[raw];
+            s_kt[i] = b | (raw << 8) | (((b * (b + 1)) >> 1) << 16);
         }
-    } else {
-        for (int i = threadIdx.x; i < NPX; i += blockDim.x) s_kt[i] = s_g[i];
+        __syncthreads();
+        bilateral_rows<RHO, MODE>(d, ws, s_sub, s_map, s_v, s_kt, s_g, f, u0, v0);
+    } else {  // more than BT_TRI_N values in this tile: full table through L1
+        for (int i = threadIdx.x; i < NPX; i += blockDim.x) s_kt[i] = (uint32_t)s_g[i] << 8;
+        __syncthreads();
+        bilateral_rows<RHO, 1>(d, ws, s_sub, s_map, s_v, s_kt, s_g, f, u0, v0);
     }
-    __syncthreads();
-    if (smem_table)
-        bilateral_rows<RHO, true>(d, ws, s_sub, s_map, s_v, s_kt, s_g, f, u0, v0);
-    else
-        bilateral_rows<RHO, false>(d, ws, s_sub, s_map, s_v, s_kt, s_g, f, u0, v0);
 }
 
 // Sobel taps on the smoothed image with mirrored borders (preprocess.hpp:71-81).
@@ -1442,8 +1452,15 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     mark(8);  // road mask is fused into the Sobel pass (stage 10)
     const dim3 bg((d.W + BF_TW - 1) / BF_TW, (d.H + BF_TH - 1) / BF_TH, n);
     if (d.rho == 5)
-        k_bilateral_tile<5><<<dim3((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n), 256,
-                               lp.bt_smem, s>>>(d, lp.ws);
+    {
+        const dim3 g((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n);
+        switch (lp.bt_mode) {
+            case 1: k_bilateral_tile<5, 1><<<g, 256, lp.bt_smem, s>>>(d, lp.ws); break;
+            case 2: k_bilateral_tile<5, 2><<<g, 256, lp.bt_smem, s>>>(d, lp.ws); break;
+            case 3: k_bilateral_tile<5, 3><<<g, 256, lp.bt_smem, s>>>(d, lp.ws); break;
+            default: k_bilateral_tile<5, 0><<<g, 256, lp.bt_smem, s>>>(d, lp.ws); break;
+        }
+    }
     else
         k_bilateral<-1><<<bg, 256, lp.bf_smem, s>>>(d);
     mark(9);
@@ -1488,9 +1505,10 @@ cudaError_t configure_kernels(const LaunchPlan& lp) {
     if ((e = cudaFuncSetAttribute(k_road_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lp.road_smem)))
         return e;
-    if ((e = cudaFuncSetAttribute(k_bilateral_tile<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  lp.bt_smem)))
-        return e;
+    for (auto fn : {k_bilateral_tile<5, 0>, k_bilateral_tile<5, 1>, k_bilateral_tile<5, 2>,
+                    k_bilateral_tile<5, 3>})
+        if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, lp.bt_smem)))
+            return e;
     if ((e = cudaFuncSetAttribute(k_bilateral<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lp.bf_smem)))
         return e;

@@ -31,6 +31,7 @@ struct LaunchPlan {
     size_t road_smem;
     size_t bf_smem;
     size_t bt_smem;
+    int bt_mode;              // bilateral table path (see k_bilateral_tile)
     size_t vanish_smem;
     int upath_sp;             // u-path DP states per thread (0 = strided fallback)
     size_t gamma_smem;

@@ -30,9 +30,12 @@ def library() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not LIB.exists():
-        raise RuntimeError(f"{LIB} is not built; run `python -m paper_1807_02752_b200.build`")
-    L = C.CDLL(str(LIB))
+    import os
+
+    path = os.environ.get("LK_LIBRARY", str(LIB))  # A/B builds of the same sources
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is not built; run `python -m paper_1807_02752_b200.build`")
+    L = C.CDLL(path)
     P, I, U32, SZ = C.c_void_p, C.c_int, C.c_uint32, C.c_size_t
     cfgp = C.POINTER(abi.LkConfig)
     repp = C.POINTER(abi.LkFrameReport)
