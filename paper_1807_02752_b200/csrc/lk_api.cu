@@ -392,6 +392,11 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     };
     while (lp.m_tile_h > 1 && m_bytes(lp.m_tile_h) > 96 * 1024) lp.m_tile_h /= 2;
     lp.m_smem = m_bytes(lp.m_tile_h);
+    d.m_tile_shift = 0;
+    while ((1 << d.m_tile_shift) < lp.m_tile_h) ++d.m_tile_shift;
+    d.m_ntx = (W + lkg::M_TW - 1) / lkg::M_TW;
+    d.m_nty = (H + lp.m_tile_h - 1) / lp.m_tile_h;
+    A(&d.m1_nz, (size_t)B * d.m_ntx * d.m_nty);
     lp.collect_blocks = 32;
     lp.sort_cap = sort_cap;
     lp.select_smem = (size_t)sort_cap * 12;
@@ -619,7 +624,19 @@ lk_status lk_get_stage(lk_ctx* c, int frame, int stage, void* dst, size_t capaci
             break;
         case LK_STAGE_VPX: s = grab(d.vpx + f * H, H * 8); break;
         case LK_STAGE_M0: s = grab(d.m0 + f * px, px * 8); break;
-        case LK_STAGE_M1: s = grab(d.m1 + f * px, px * 8); break;
+        case LK_STAGE_M1: {
+            s = grab(d.m1 + f * px, px * 8);
+            if (s != LK_OK || d.hooks) break;
+            // without hooks only the non-zero tiles on road rows are written
+            std::vector<uint8_t> nz((size_t)d.m_nty * d.m_ntx);
+            CU(cudaMemcpy(nz.data(), d.m1_nz + f * nz.size(), nz.size(), cudaMemcpyDeviceToHost));
+            double* m = (double*)buf.data();
+            for (int v = 0; v < d.H; ++v)
+                for (int u = 0; u < d.W; ++u)
+                    if (v < rep.horizon || !nz[(v >> d.m_tile_shift) * d.m_ntx + (u / lkg::M_TW)])
+                        m[(size_t)v * d.W + u] = 0.0;
+            break;
+        }
         case LK_STAGE_ENERGY: s = grab(d.energy + f * C, C * 8); break;
         case LK_STAGE_LANES:
             s = grab(d.lanes + f * d.lane_cap, (size_t)rep.lane_count * sizeof(lk_lane));

@@ -76,7 +76,9 @@ struct Dev {
     int8_t* uchoice;        // [B][H][ext_cols]
     int32_t* upath;         // [B][H][2]
     int32_t* gamma_inl;     // [B][H][2]
-    double* m1;             // [B][H][W]
+    double* m1;             // [B][H][W] (only tiles flagged in m1_nz are written)
+    uint8_t* m1_nz;         // [B][m_nty][m_ntx] m0/m1 tile has a non-zero
+    int m_tile_shift, m_ntx, m_nty;  // m0/m1 tile: (1 << m_tile_shift) rows x M_TW cols
     unsigned int* p99hist;  // [B][2048]
     unsigned long long* p99cand;  // [B][px]
     double* energy;         // [B][ext_cols]

@@ -534,6 +534,12 @@ __global__ void __launch_bounds__(256) k_sobel_edges(Dev d) {
     }
     const int W = d.W, H = d.H;
     const int u0 = blockIdx.x * SB_TW, v0 = blockIdx.y * SB_TH;
+    const int horizon = (int)d.rep[f].horizon;
+    if (!d.hooks && v0 + SB_TH <= horizon) {  // the mask is empty above the horizon
+        if (threadIdx.x < SB_TH && v0 + threadIdx.x < H)
+            d.seg_cnt[((size_t)f * H + v0 + threadIdx.x) * d.n_seg + blockIdx.x] = 0;
+        return;
+    }
     const double* img = d.smoothed + (size_t)f * d.px;
     __shared__ int s_col[SW];
     __shared__ int s_row[SB_TH + 2];
@@ -557,7 +563,6 @@ __global__ void __launch_bounds__(256) k_sobel_edges(Dev d) {
     if (threadIdx.x < SB_TH) s_seg[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_tot[threadIdx.x] = 0;
     __syncthreads();
-    const int horizon = (int)d.rep[f].horizon;
     const int lane = threadIdx.x & 31;
     int n_edge = 0, n_mask = 0;
 #pragma unroll
@@ -669,6 +674,7 @@ __global__ void __launch_bounds__(256) k_edge_emit(Dev d) {
     const int seg = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int W = d.W, H = d.H;
     if (seg >= H * d.n_seg) return;
+    if (d.seg_cnt[(size_t)f * H * d.n_seg + seg] == 0) return;  // empty segment
     const int v = seg / d.n_seg, sx = seg - v * d.n_seg;
     const int base = d.seg_off[(size_t)f * H * d.n_seg + seg];
     const double* img = d.smoothed + (size_t)f * d.px;
@@ -1102,14 +1108,40 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
     const int32_t* roff = d.row_off + (size_t)f * (H + 1);
     const size_t eb = (size_t)f * d.px;
     const int r_lo = max(max(gr0, 0), v_top), r_hi = min(gr0 + GH - 1, v_max);
+    int nonzero = 0;
     if (r_lo <= r_hi) {
         for (int e = roff[r_lo] + threadIdx.x; e < roff[r_hi + 1]; e += blockDim.x) {
             const int uv = d.e_uv[eb + e];
             const int u = uv & 0xffff, v = uv >> 16;
-            if (u >= gc0 && u < gc0 + GW) gw[(v - gr0) * GW + (u - gc0)] = d.e_wg[eb + e];
+            if (u >= gc0 && u < gc0 + GW) {
+                const double w = d.e_wg[eb + e];
+                gw[(v - gr0) * GW + (u - gc0)] = w;
+                nonzero |= w != 0.0;
+            }
         }
     }
-    __syncthreads();
+    // A tile without a non-zero w_g in reach has m0 = m1 = +0 everywhere: it
+    // is flagged instead of written (readers of m1 consult the flag).
+    nonzero = __syncthreads_or(nonzero);
+    const int t_lo = max(0, v_top), t_hi = min(H - 1, v_max);
+    if (threadIdx.x == 0)
+        d.m1_nz[((size_t)f * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = (uint8_t)nonzero;
+    if (!nonzero) {
+        if (d.hooks)
+            for (int i = threadIdx.x; i < tile_h * M_TW; i += blockDim.x) {
+                const int v = v0 + i / M_TW, u = u0 + i % M_TW;
+                if (v >= H || u >= W) continue;
+                const size_t gi = (size_t)f * d.px + (size_t)v * W + u;
+                d.m1[gi] = 0.0;
+                d.m0[gi] = 0.0;
+            }
+        if (want_hist && threadIdx.x == 0) {
+            const int rows = max(0, min(v0 + tile_h - 1, t_hi) - max(v0, t_lo) + 1);
+            const int cols = min(M_TW, W - u0);
+            if (rows > 0) atomicAdd(&d.p99hist[(size_t)f * 2048], (unsigned)(rows * cols));
+        }
+        return;
+    }
     // box sum, y-major / x-minor (lanes.hpp:46-60). Positions outside the image
     // hold zeros in gw: adding +-0.0 to a running sum that starts at +0.0 never
     // changes it, so summing them instead of skipping is bit-identical.
@@ -1122,7 +1154,6 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
         m0[i] = s;
     }
     __syncthreads();
-    const int t_lo = max(0, v_top), t_hi = min(H - 1, v_max);
     const int lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < tile_h * M_TW; i += blockDim.x) {
         const int r = i / M_TW, c = i - r * M_TW;
@@ -1202,10 +1233,15 @@ __global__ void __launch_bounds__(256) k_p99_collect(Dev d) {
     const size_t n = (size_t)(t_hi - t_lo + 1) * d.W;
     const unsigned bucket = d.aux[f].p99_bucket;
     const double* m1 = d.m1 + (size_t)f * d.px + (size_t)t_lo * d.W;
+    const uint8_t* nz = d.m1_nz + (size_t)f * d.m_nty * d.m_ntx;  // unwritten tiles are zero
     unsigned long long* out = d.p99cand + (size_t)f * d.px;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (size_t)gridDim.x * blockDim.x) {
-        const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(m1[i]));
+        const int v = t_lo + (int)(i / d.W), u = (int)(i % d.W);
+        const bool live = nz[(v >> d.m_tile_shift) * d.m_ntx + (u >> 7)] != 0;
+        if (!live && bucket != 0) continue;  // a zero can only be a candidate of bucket 0
+        const unsigned long long b =
+            live ? (unsigned long long)__double_as_longlong(fabs(m1[i])) : 0ULL;
         const bool hit = (b >> 52) == bucket;
         const unsigned bal = __ballot_sync(__activemask(), hit);
         if (!bal) continue;
@@ -1280,6 +1316,7 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
     const double* vpx = d.vpx + (size_t)f * H;
     const double* vpy = d.vpy + (size_t)f * H;
     const double* m1 = d.m1 + (size_t)f * d.px;
+    const uint8_t* nz = d.m1_nz + (size_t)f * d.m_nty * d.m_ntx;  // unwritten tiles are zero
     const double lg = d.lambda_g;
     double u = (double)(d.ext_lo + ci);
     bool alive = true;
@@ -1297,7 +1334,9 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
         double contrib = 0.0;
         if (alive && !isnan(u)) {
             const long long r = llround_ref(u);
-            if (r >= 0 && r < W && v >= 0 && v < H) contrib = m1[(size_t)v * W + (int)r];
+            if (r >= 0 && r < W && v >= 0 && v < H &&
+                nz[(v >> d.m_tile_shift) * d.m_ntx + ((int)r >> 7)])
+                contrib = m1[(size_t)v * W + (int)r];
         }
         e = contrib + lg * e;
     }
