@@ -330,6 +330,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     A(&d.gamma_inl, (size_t)B * H * 2);
     A(&d.m1, (size_t)B * d.px);
     A(&d.p99hist, (size_t)B * 2048);
+    A(&d.p99hist2, (size_t)B * 4096);
     A(&d.p99cand, (size_t)B * d.px);
     A(&d.energy, (size_t)B * C);
     int sort_cap = 1;
@@ -380,8 +381,12 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     lp.vanish_smem = (size_t)2 * C * 8 + (size_t)C * 4 + (size_t)2 * H * 4 +
                      (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 8 + (size_t)(H + 1) * 4 +
                      (size_t)lkg::K4_VOTE_CAP * 2 + 16;
-    lp.upath_sp = (C + lkg::K4_THREADS - 1) / lkg::K4_THREADS;
+    // u-path DP shape: 512 threads (2 CTAs / SM) up to 4096 extended columns,
+    // else 1024 threads; SP consecutive states per thread (0 = strided fallback)
+    lp.upath_nt = C <= 512 * 8 ? 512 : 1024;
+    lp.upath_sp = (C + lp.upath_nt - 1) / lp.upath_nt;
     if (lp.upath_sp == 7) lp.upath_sp = 8;
+    if (lp.upath_nt == 1024 && lp.upath_sp < 5) lp.upath_sp = 5;
     if (lp.upath_sp > 8) lp.upath_sp = 0;
     lp.gamma_smem = (size_t)12 * H * 4 + 8 + (size_t)H * 8 + 16;
     lp.m_tile_h = 16;
@@ -399,7 +404,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     A(&d.m1_nz, (size_t)B * d.m_ntx * d.m_nty);
     lp.collect_blocks = 32;
     lp.sort_cap = sort_cap;
-    lp.select_smem = (size_t)sort_cap * 12;
+    lp.select_smem = (size_t)sort_cap * 12 + (size_t)((C + 31) / 32) * 4 + 16;
     const size_t smem_cap = prop.sharedMemPerBlockOptin;
     if (lp.vpath_smem > smem_cap || lp.road_smem > smem_cap || lp.bf_smem > smem_cap || lp.bt_smem > smem_cap ||
         lp.vanish_smem > smem_cap || lp.gamma_smem > smem_cap || lp.m_smem > smem_cap || lp.select_smem > smem_cap) {
@@ -466,8 +471,10 @@ static lk_status enqueue_direct(lk_ctx* c, int n, bool timed) {
     const Dev& d = c->d;
     CU(cudaMemsetAsync(d.rep, 0, (size_t)n * sizeof(lk_frame_report), c->stream));
     CU(cudaMemsetAsync(d.aux, 0, (size_t)n * sizeof(FrameAux), c->stream));
-    if (std::isnan(d.tr_lpv))
+    if (std::isnan(d.tr_lpv)) {
         CU(cudaMemsetAsync(d.p99hist, 0, (size_t)n * 2048 * sizeof(unsigned), c->stream));
+        CU(cudaMemsetAsync(d.p99hist2, 0, (size_t)n * 4096 * sizeof(unsigned), c->stream));
+    }
     CU(lkg::launch_pipeline(d, c->lp, n, c->stream, timed ? c->ev : nullptr));
     return LK_OK;
 }

@@ -22,6 +22,11 @@ struct FrameAux {
     unsigned long long skipped;
     unsigned int p99_cands;         // candidates in the p99 exponent bucket
     unsigned int p99_bucket;
+    unsigned int p99_bucket2;      // next 12 bits inside the exponent bucket
+    unsigned int p99_done;         // the percentile is exactly +0 (rank among the zeros)
+    unsigned int p99_level2;       // bucket too large: narrowed by a second histogram
+    unsigned int pad3;
+    unsigned long long p99_zeros;  // |m1| values that are exactly zero
     unsigned long long p99_rank;    // rank of the percentile inside the bucket
     double tr;                      // tr_lpv used
     int lanes;                      // kept lanes
@@ -80,6 +85,7 @@ struct Dev {
     uint8_t* m1_nz;         // [B][m_nty][m_ntx] m0/m1 tile has a non-zero
     int m_tile_shift, m_ntx, m_nty;  // m0/m1 tile: (1 << m_tile_shift) rows x M_TW cols
     unsigned int* p99hist;  // [B][2048]
+    unsigned int* p99hist2; // [B][4096]
     unsigned long long* p99cand;  // [B][px]
     double* energy;         // [B][ext_cols]
     lk_lane* lanes;         // [B][lane_cap]

@@ -802,8 +802,8 @@ __device__ __forceinline__ void upath_stage(const void* prevv, void* curv, const
     }
 }
 
-template <int SP>
-__global__ void __launch_bounds__(K4_THREADS, 2) k_vanish(Dev d) {
+template <int SP, int NT>
+__global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
     extern __shared__ double sh4[];
     const int f = blockIdx.x;
     if (frame_failed(d, f)) return;
@@ -1138,7 +1138,10 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
         if (want_hist && threadIdx.x == 0) {
             const int rows = max(0, min(v0 + tile_h - 1, t_hi) - max(v0, t_lo) + 1);
             const int cols = min(M_TW, W - u0);
-            if (rows > 0) atomicAdd(&d.p99hist[(size_t)f * 2048], (unsigned)(rows * cols));
+            if (rows > 0) {
+                atomicAdd(&d.p99hist[(size_t)f * 2048], (unsigned)(rows * cols));
+                atomicAdd(&d.aux[f].p99_zeros, (unsigned long long)(rows * cols));
+            }
         }
         return;
     }
@@ -1175,7 +1178,9 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
             const bool in = live && v >= t_lo && v <= t_hi;
             const unsigned bin = (unsigned)((unsigned long long)__double_as_longlong(fabs(m1)) >> 52);
             const unsigned zb = __ballot_sync(__activemask(), in && bin == 0);
+            const unsigned z0 = __ballot_sync(__activemask(), in && m1 == 0.0);
             if (lane == 0 && zb) atomicAdd(&hist[0], (unsigned)__popc(zb));
+            if (lane == 0 && z0) atomicAdd(&d.aux[f].p99_zeros, (unsigned long long)__popc(z0));
             if (in && bin != 0) atomicAdd(&hist[bin], 1u);
         }
     }
@@ -1190,59 +1195,135 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
 // =====================================================================
 // auto_lane_threshold (lanes.hpp:182-193): the k-th smallest |m1|,
 // k = floor(0.99*(n-1)), selected EXACTLY on the IEEE bit patterns
-// (non-negative doubles order like their bits): exponent histogram (K5a),
-// bucket pick, candidate gather, then MSB radix select inside the bucket.
+// (non-negative doubles order like their bits). Level 1: exponent histogram
+// (fused into K5a) -> bucket; level 2: histogram of the next 12 bits inside
+// that bucket -> sub-bucket; the few values sharing those 24 leading bits are
+// gathered and the remaining 40 bits resolved by MSB radix select.
 // =====================================================================
-__global__ void __launch_bounds__(256) k_p99_bucket(Dev d) {
-    const int f = blockIdx.x;
-    if (frame_failed(d, f)) return;
-    __shared__ unsigned long long s_part[256];
-    const unsigned int* h = d.p99hist + (size_t)f * 2048;
+__device__ __forceinline__ unsigned long long p99_n(const Dev& d, int f, int* t_lo) {
     const int v_top = (int)d.rep[f].horizon, v_max = d.H - 1;
-    const int t_lo = max(0, v_top), t_hi = min(d.H - 1, v_max);
-    const unsigned long long n = (unsigned long long)(t_hi - t_lo + 1) * d.W;
-    const unsigned long long k = (unsigned long long)floor(0.99 * (double)(n - 1));
-    // each thread owns 8 consecutive bins
+    *t_lo = max(0, v_top);
+    const int t_hi = min(d.H - 1, v_max);
+    return (unsigned long long)(t_hi - *t_lo + 1) * d.W;
+}
+
+// Picks the bin holding rank `rank` among nb bins (blockDim = 256).
+__device__ void pick_bin(const unsigned int* h, int nb, unsigned long long rank, int* bin_out,
+                         unsigned long long* rank_out) {
+    __shared__ unsigned long long s_part[256];
+    const int per = nb / 256;
     unsigned long long mine = 0;
-    for (int b = 0; b < 8; ++b) mine += h[threadIdx.x * 8 + b];
+    for (int b = 0; b < per; ++b) mine += h[threadIdx.x * per + b];
     s_part[threadIdx.x] = mine;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long run = 0;
         int t = 0;
-        for (; t < 256; ++t) {
-            if (run + s_part[t] > k) break;
+        for (; t < 255; ++t) {
+            if (run + s_part[t] > rank) break;
             run += s_part[t];
         }
-        int b = t * 8;
-        for (;; ++b) {
-            if (run + h[b] > k) break;
+        int b = t * per;
+        for (; b < (t + 1) * per - 1; ++b) {
+            if (run + h[b] > rank) break;
             run += h[b];
         }
+        *bin_out = b;
+        *rank_out = rank - run;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_p99_bucket(Dev d) {
+    const int f = blockIdx.x;
+    if (frame_failed(d, f)) return;
+    int t_lo;
+    const unsigned long long n = p99_n(d, f, &t_lo);
+    const unsigned long long k = (unsigned long long)floor(0.99 * (double)(n - 1));
+    int b;
+    unsigned long long r;
+    pick_bin(d.p99hist + (size_t)f * 2048, 2048, k, &b, &r);
+    if (threadIdx.x == 0) {
         d.aux[f].p99_bucket = b;
-        d.aux[f].p99_rank = k - run;
+        d.aux[f].p99_rank = r;
         d.aux[f].p99_cands = 0;
+        // +0 is the smallest |m1|: a rank among the zeros settles it (common when
+        // fewer than 1% of the road pixels respond, e.g. 2560x1024 with lambda_g 1)
+        const bool zero = b == 0 && r < d.aux[f].p99_zeros;
+        d.aux[f].p99_done = zero;
+        // a small bucket is gathered directly; a large one is narrowed first by
+        // a second histogram level (12 more bits)
+        d.aux[f].p99_level2 = d.p99hist[(size_t)f * 2048 + b] > 65536u;
+        d.aux[f].p99_bucket2 = 0;
+        if (zero) {
+            const int v_top = (int)d.rep[f].horizon, v_max = d.H - 1;
+            const double tr = -0.15 * (double)(v_max - v_top + 1) * 0.0;
+            d.aux[f].tr = tr;
+            d.rep[f].tr_lpv_used = tr;
+        }
+    }
+}
+
+// |m1| bits of road-row pixel i (unwritten tiles are +0).
+__device__ __forceinline__ unsigned long long m1_bits(const Dev& d, int f, int t_lo, size_t i,
+                                                      bool* live) {
+    const int v = t_lo + (int)(i / d.W), u = (int)(i % d.W);
+    *live = d.m1_nz[((size_t)f * d.m_nty + (v >> d.m_tile_shift)) * d.m_ntx + (u >> 7)] != 0;
+    return *live ? (unsigned long long)__double_as_longlong(
+                       fabs(d.m1[(size_t)f * d.px + (size_t)v * d.W + u]))
+                 : 0ULL;
+}
+
+__global__ void __launch_bounds__(256) k_p99_hist2(Dev d) {
+    const int f = blockIdx.y;
+    if (frame_failed(d, f) || d.aux[f].p99_done || !d.aux[f].p99_level2) return;
+    __shared__ unsigned int h[4096];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    int t_lo;
+    const size_t n = p99_n(d, f, &t_lo);
+    const unsigned bucket = d.aux[f].p99_bucket;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        bool live;
+        const unsigned long long b = m1_bits(d, f, t_lo, i, &live);
+        if (!live && bucket != 0) continue;
+        if ((b >> 52) == bucket) atomicAdd(&h[(b >> 40) & 0xfff], 1u);
+    }
+    __syncthreads();
+    unsigned int* gh = d.p99hist2 + (size_t)f * 4096;
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x)
+        if (h[i]) atomicAdd(&gh[i], h[i]);
+}
+
+__global__ void __launch_bounds__(256) k_p99_bucket2(Dev d) {
+    const int f = blockIdx.x;
+    if (frame_failed(d, f) || d.aux[f].p99_done || !d.aux[f].p99_level2) return;
+    int b;
+    unsigned long long r;
+    pick_bin(d.p99hist2 + (size_t)f * 4096, 4096, d.aux[f].p99_rank, &b, &r);
+    if (threadIdx.x == 0) {
+        d.aux[f].p99_bucket2 = b;
+        d.aux[f].p99_rank = r;
     }
 }
 
 __global__ void __launch_bounds__(256) k_p99_collect(Dev d) {
     const int f = blockIdx.y;
-    if (frame_failed(d, f)) return;
-    const int v_top = (int)d.rep[f].horizon, v_max = d.H - 1;
-    const int t_lo = max(0, v_top), t_hi = min(d.H - 1, v_max);
-    const size_t n = (size_t)(t_hi - t_lo + 1) * d.W;
-    const unsigned bucket = d.aux[f].p99_bucket;
-    const double* m1 = d.m1 + (size_t)f * d.px + (size_t)t_lo * d.W;
-    const uint8_t* nz = d.m1_nz + (size_t)f * d.m_nty * d.m_ntx;  // unwritten tiles are zero
+    if (frame_failed(d, f) || d.aux[f].p99_done) return;
+    int t_lo;
+    const size_t n = p99_n(d, f, &t_lo);
+    const bool l2 = d.aux[f].p99_level2;
+    const int ksh = l2 ? 40 : 52;  // leading bits fixed by the histogram level(s)
+    const unsigned long long key = l2 ? ((unsigned long long)d.aux[f].p99_bucket << 12) |
+                                            d.aux[f].p99_bucket2
+                                      : (unsigned long long)d.aux[f].p99_bucket;
     unsigned long long* out = d.p99cand + (size_t)f * d.px;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (size_t)gridDim.x * blockDim.x) {
-        const int v = t_lo + (int)(i / d.W), u = (int)(i % d.W);
-        const bool live = nz[(v >> d.m_tile_shift) * d.m_ntx + (u >> 7)] != 0;
-        if (!live && bucket != 0) continue;  // a zero can only be a candidate of bucket 0
-        const unsigned long long b =
-            live ? (unsigned long long)__double_as_longlong(fabs(m1[i])) : 0ULL;
-        const bool hit = (b >> 52) == bucket;
+        bool live;
+        const unsigned long long b = m1_bits(d, f, t_lo, i, &live);
+        if (!live && key != 0) continue;  // a zero can only be a candidate of key 0
+        const bool hit = (b >> ksh) == key;
         const unsigned bal = __ballot_sync(__activemask(), hit);
         if (!bal) continue;
         const int lane = threadIdx.x & 31;
@@ -1256,19 +1337,20 @@ __global__ void __launch_bounds__(256) k_p99_collect(Dev d) {
 
 __global__ void __launch_bounds__(256) k_p99_select(Dev d) {
     const int f = blockIdx.x;
-    if (frame_failed(d, f)) return;
+    if (frame_failed(d, f) || d.aux[f].p99_done) return;
     __shared__ unsigned int hist[256];
     __shared__ unsigned long long s_prefix, s_rank;
     const unsigned ncand = d.aux[f].p99_cands;
     const unsigned long long* c = d.p99cand + (size_t)f * d.px;
-    unsigned long long prefix = (unsigned long long)d.aux[f].p99_bucket << 52;
-    unsigned long long mask = 0xFFF0000000000000ULL;
+    const bool l2 = d.aux[f].p99_level2;
+    int bits_left = l2 ? 40 : 52;  // bits below the histogram-fixed prefix
+    unsigned long long prefix = ((unsigned long long)d.aux[f].p99_bucket << 52) |
+                                ((unsigned long long)d.aux[f].p99_bucket2 << 40);
+    unsigned long long mask = ~0ULL << bits_left;
     unsigned long long rank = d.aux[f].p99_rank;
-    const int shifts[7] = {44, 36, 28, 20, 12, 4, 0};
-    const int widths[7] = {8, 8, 8, 8, 8, 8, 4};
-    for (int pass = 0; pass < 7; ++pass) {
-        const int sh = shifts[pass];
-        const unsigned dm = (1u << widths[pass]) - 1u;
+    while (bits_left > 0) {
+        const int w = min(8, bits_left), sh = bits_left - w;
+        const unsigned dm = (1u << w) - 1u;
         for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
         __syncthreads();
         for (unsigned i = threadIdx.x; i < ncand; i += blockDim.x) {
@@ -1279,7 +1361,7 @@ __global__ void __launch_bounds__(256) k_p99_select(Dev d) {
         if (threadIdx.x == 0) {
             unsigned long long run = 0;
             unsigned dg = 0;
-            for (; dg <= dm; ++dg) {
+            for (; dg < dm; ++dg) {
                 if (run + hist[dg] > rank) break;
                 run += hist[dg];
             }
@@ -1290,6 +1372,7 @@ __global__ void __launch_bounds__(256) k_p99_select(Dev d) {
         prefix = s_prefix;
         rank = s_rank;
         mask |= (unsigned long long)dm << sh;
+        bits_left = sh;
         __syncthreads();
     }
     if (threadIdx.x == 0) {
@@ -1401,17 +1484,30 @@ __global__ void __launch_bounds__(256) k_select(Dev d, int sort_cap) {
             __syncthreads();
         }
     lk_lane* lanes = d.lanes + (size_t)f * d.lane_cap;
+    // greedy suppression (lanes.hpp:158-166) against a bitmap of kept columns:
+    // "some kept k with |i - k| < min_sep" is a test of the bits in
+    // [i - min_sep + 1, i + min_sep - 1], in the same candidate order
+    unsigned int* kbits = (unsigned int*)(cols + sort_cap);
+    const int nwords = (n + 31) >> 5;
+    for (int i = threadIdx.x; i < nwords; i += blockDim.x) kbits[i] = 0;
+    __syncthreads();
     if (threadIdx.x == 0) {
         int kept = 0;
+        const int sep = d.min_lane_sep;
         for (int q = 0; q < m; ++q) {
             const int i = cols[q];
             bool close = false;
-            for (int k = 0; k < kept; ++k)
-                if (abs(i - (lanes[k].bottom_col - d.ext_lo)) < d.min_lane_sep) {
-                    close = true;
-                    break;
+            if (sep > 0) {
+                const int lo = max(0, i - sep + 1), hi = min(n - 1, i + sep - 1);
+                for (int w = lo >> 5; w <= (hi >> 5) && !close; ++w) {
+                    unsigned int bits = kbits[w];
+                    if (w == (lo >> 5)) bits &= ~0u << (lo & 31);
+                    if (w == (hi >> 5)) bits &= ~0u >> (31 - (hi & 31));
+                    close = bits != 0;
                 }
+            }
             if (close) continue;
+            kbits[i >> 5] |= 1u << (i & 31);
             if (kept < d.lane_cap) {
                 lanes[kept].bottom_col = d.ext_lo + i;
                 lanes[kept].energy = h[i];
@@ -1507,16 +1603,27 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     k_edge_scan<<<n, 1024, 0, s>>>(d);
     k_edge_emit<<<dim3((d.H * d.n_seg + 7) / 8, n), 256, 0, s>>>(d);
     mark(10);
-    switch (lp.upath_sp) {
-        case 1: k_vanish<1><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
-        case 2: k_vanish<2><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
-        case 3: k_vanish<3><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
-        case 4: k_vanish<4><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
-        case 5: k_vanish<5><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
-        case 6: k_vanish<6><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
-        case 8: k_vanish<8><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
-        default: k_vanish<0><<<n, K4_THREADS, lp.vanish_smem, s>>>(d); break;
+    // u-path DP: NT threads x SP consecutive states each (SP = 0: strided fallback)
+#define LK_VANISH(SP, NT) k_vanish<SP, NT><<<n, NT, lp.vanish_smem, s>>>(d)
+    if (lp.upath_nt == 512) {
+        switch (lp.upath_sp) {
+            case 1: LK_VANISH(1, 512); break;
+            case 2: LK_VANISH(2, 512); break;
+            case 3: LK_VANISH(3, 512); break;
+            case 4: LK_VANISH(4, 512); break;
+            case 5: LK_VANISH(5, 512); break;
+            case 6: LK_VANISH(6, 512); break;
+            default: LK_VANISH(8, 512); break;
+        }
+    } else {
+        switch (lp.upath_sp) {
+            case 5: LK_VANISH(5, 1024); break;
+            case 6: LK_VANISH(6, 1024); break;
+            case 8: LK_VANISH(8, 1024); break;
+            default: LK_VANISH(0, 1024); break;
+        }
     }
+#undef LK_VANISH
     k_gamma_fit<<<n, 256, lp.gamma_smem, s>>>(d);
     mark(11);
     const bool auto_tr = isnan(d.tr_lpv);
@@ -1524,6 +1631,8 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
               lp.m_smem, s>>>(d, lp.m_tile_h, auto_tr ? 1 : 0);
     if (auto_tr) {
         k_p99_bucket<<<n, 256, 0, s>>>(d);
+        k_p99_hist2<<<dim3(lp.collect_blocks, n), 256, 0, s>>>(d);
+        k_p99_bucket2<<<n, 256, 0, s>>>(d);
         k_p99_collect<<<dim3(lp.collect_blocks, n), 256, 0, s>>>(d);
         k_p99_select<<<n, 256, 0, s>>>(d);
     }
@@ -1534,7 +1643,7 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     return cudaGetLastError();
 }
 
-int launches_per_batch(const Dev& d) { return isnan(d.tr_lpv) ? 16 : 13; }
+int launches_per_batch(const Dev& d) { return isnan(d.tr_lpv) ? 18 : 13; }
 
 cudaError_t configure_kernels(const LaunchPlan& lp) {
     cudaError_t e;
@@ -1551,8 +1660,9 @@ cudaError_t configure_kernels(const LaunchPlan& lp) {
     if ((e = cudaFuncSetAttribute(k_bilateral<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lp.bf_smem)))
         return e;
-    for (auto fn : {k_vanish<0>, k_vanish<1>, k_vanish<2>, k_vanish<3>, k_vanish<4>, k_vanish<5>,
-                    k_vanish<6>, k_vanish<8>})
+    for (auto fn : {k_vanish<1, 512>, k_vanish<2, 512>, k_vanish<3, 512>, k_vanish<4, 512>,
+                    k_vanish<5, 512>, k_vanish<6, 512>, k_vanish<8, 512>, k_vanish<5, 1024>,
+                    k_vanish<6, 1024>, k_vanish<8, 1024>, k_vanish<0, 1024>})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       lp.vanish_smem)))
             return e;

@@ -34,6 +34,7 @@ struct LaunchPlan {
     int bt_mode;              // bilateral table path (see k_bilateral_tile)
     size_t vanish_smem;
     int upath_sp;             // u-path DP states per thread (0 = strided fallback)
+    int upath_nt;             // u-path DP threads per CTA (512 or 1024)
     size_t gamma_smem;
     size_t m_smem;
     int m_tile_h;

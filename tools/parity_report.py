@@ -24,6 +24,9 @@ def main():
         params = [scenes.probe_scene()]
     elif kind == "batch":
         params = [scenes.batch_scene(i) for i in range(count)]
+    elif kind == "hires":
+        params = [scenes.hires_scene(i) for i in range(count)]
+        cfg = scenes.hires_config()
     elif kind == "stress":
         params = [scenes.stress_scene(i) for i in range(count)]
     else:
