@@ -242,6 +242,10 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     d.min_lane_sep = cfg->min_lane_sep;
     d.paper_sign = cfg->paper_sign ? 1 : 0;
     d.max_iter = kMaxIter;
+    {  // both selection paths are exact; the switch only trades a pass for a gather
+        const char* e = std::getenv("LK_P99_L2_MIN");
+        d.p99_l2_min = e ? (unsigned)std::strtoul(e, nullptr, 10) : 65536u;
+    }
     if (d.ext_cols < 1) {
         delete c;
         return fail(LK_ERR_CONFIG, "extended column axis is empty");

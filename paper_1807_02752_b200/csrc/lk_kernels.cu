@@ -1252,7 +1252,7 @@ __global__ void __launch_bounds__(256) k_p99_bucket(Dev d) {
         d.aux[f].p99_done = zero;
         // a small bucket is gathered directly; a large one is narrowed first by
         // a second histogram level (12 more bits)
-        d.aux[f].p99_level2 = d.p99hist[(size_t)f * 2048 + b] > 65536u;
+        d.aux[f].p99_level2 = d.p99hist[(size_t)f * 2048 + b] > d.p99_l2_min;
         d.aux[f].p99_bucket2 = 0;
         if (zero) {
             const int v_top = (int)d.rep[f].horizon, v_max = d.H - 1;

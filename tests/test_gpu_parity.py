@@ -86,6 +86,18 @@ def test_paper_sign_and_manual_threshold(oracle):
     assert not problems, "\n".join(problems)
 
 
+@pytest.mark.parametrize("l2_min", ["0", "4294967295"])
+def test_p99_selection_paths(oracle, monkeypatch, l2_min):
+    """The exact p99 (lanes.hpp:182-193) through both GPU selection paths:
+    always with the second histogram level, and never."""
+    monkeypatch.setenv("LK_P99_L2_MIN", l2_min)
+    params = [scenes.batch_scene(i) for i in (3, 11)] + [scenes.acceptance_scene(5)]
+    for p, cfg in [(params[:2], abi.default_config(sobel_threshold=20.0, nu=3)),
+                   (params[2:], scenes.acceptance_config())]:
+        reps, problems = _run_and_compare(oracle, p, cfg, hooks=False)
+        assert not problems, "\n".join(problems)
+
+
 def test_stage6_no_road_evidence(oracle):
     """Identical views -> empty disparity -> StageError 6 (test_pipeline.cpp:119-127)."""
     grey, disp = lanekit.synth_batch([scenes.acceptance_scene(0)])
