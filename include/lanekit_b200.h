@@ -199,6 +199,9 @@ typedef struct lk_lane {   /* lanekit::Lane (lanes.hpp:131-135) minus the polyli
 /* Context flags. */
 #define LK_FLAG_HOOKS 1u   /* also materialise mask, gx/gy/mag/theta, accumulator, m0 */
 #define LK_FLAG_NO_GRAPH 2u /* launch kernels directly instead of replaying a CUDA graph */
+#define LK_FLAG_EXACT 4u    /* exact bilateral on every pixel even without hooks (the
+                               default throughput path computes it exactly only around
+                               edge candidates; outputs are identical either way) */
 
 typedef struct lk_ctx lk_ctx;
 
@@ -248,6 +251,11 @@ lk_status lk_measure_fp64(int device, double* ops_per_s);
 
 /* Number of kernel launches one lk_run_batch / lk_enqueue issues. */
 int lk_launches_per_batch(lk_ctx* ctx);
+
+/* Largest |approximate - exact| smoothed value over the last batch: verifies
+ * the fast path's error bound (2.5e-5) by also running the exact bilateral on
+ * every pixel. LK_ERR_UNAVAILABLE when the context uses the exact path. */
+lk_status lk_fast_path_error(lk_ctx* ctx, double* max_abs_error);
 
 /* Page-locked host buffers for host-fed (end-to-end) runs. */
 lk_status lk_host_alloc(void** ptr, size_t bytes);

@@ -19,6 +19,7 @@ LK_ERR_UNAVAILABLE = 6
 
 LK_FLAG_HOOKS = 1
 LK_FLAG_NO_GRAPH = 2
+LK_FLAG_EXACT = 4
 
 LK_MEM_HOST = 0
 LK_MEM_DEVICE = 1

@@ -382,6 +382,21 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         if (win == 11)
             for (int i = 0; i < 121; ++i) lp.ws.w[i] = ws[i];
     }
+    // Certified fast front end (lk_fastpath.cu): throughput mode only (hooks
+    // export exact maps), 11x11 window, and a weight range whose FP32 error
+    // budget holds (exponent of the smallest weight <= 20; default 11.1).
+    {
+        const double xmax = 50.0 * inv_s2 + inv_r2;
+        lp.fast_front = win == 11 && !d.hooks && !(flags & LK_FLAG_EXACT) && xmax <= 20.0;
+        const double log2e = 1.4426950408889634;
+        for (int dj = -5; dj <= 5; ++dj)
+            for (int di = -5; di <= 5; ++di)
+                lp.fbf.c[(dj + 5) * 11 + (di + 5)] =
+                    (float)(-(double)(di * di + dj * dj) * inv_s2 * log2e);
+        lp.fbf.c2 = (float)(-inv_r2 * log2e);
+        for (int k = 0; k < 256; ++k) lp.fbf.vf[k] = (float)(k / 255.0);
+        if (lp.fast_front) A(&d.smoothed_f, (size_t)B * d.px);
+    }
     lp.vanish_smem = (size_t)2 * C * 8 + (size_t)C * 4 + (size_t)2 * H * 4 +
                      (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 8 + (size_t)(H + 1) * 4 +
                      (size_t)lkg::K4_VOTE_CAP * 2 + 16;
@@ -579,6 +594,10 @@ lk_status lk_get_stage(lk_ctx* c, int frame, int stage, void* dst, size_t capaci
                            stage == LK_STAGE_VPX_ACC || stage == LK_STAGE_M0 ||
                            stage == LK_STAGE_POLYLINES;
     if (hook_only && !d.hooks) return fail(LK_ERR_UNAVAILABLE, "hook needs LK_FLAG_HOOKS");
+    if (stage == LK_STAGE_SMOOTHED && c->lp.fast_front)
+        return fail(LK_ERR_UNAVAILABLE,
+                    "SMOOTHED is exact only around edges on the fast path: use LK_FLAG_HOOKS "
+                    "or LK_FLAG_EXACT");
     const size_t px = d.px, H = d.H, C = d.ext_cols, D1 = d.D1;
     const size_t rows = (size_t)(d.H - rep.horizon);
     const size_t f = (size_t)frame;
@@ -704,5 +723,26 @@ extern "C" lk_status lk_measure_fp64(int device, double* ops_per_s) {
     cudaDeviceProp prop;
     CU(cudaGetDeviceProperties(&prop, device));
     CU(lkg::fp64_probe(prop.multiProcessorCount, ops_per_s));
+    return LK_OK;
+}
+
+extern "C" lk_status lk_fast_path_error(lk_ctx* c, double* max_abs_error) {
+    if (!c || !max_abs_error) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    if (!c->lp.fast_front || c->last_n < 1)
+        return fail(LK_ERR_UNAVAILABLE, "no fast-path batch has run on this context");
+    CU(cudaSetDevice(c->device));
+    double* scratch = nullptr;
+    CU(cudaMalloc(&scratch, sizeof(double)));
+    cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(double), c->stream);
+    if (e == cudaSuccess) {
+        lkg::launch_exact_bilateral(c->d, c->lp, c->last_n, c->stream);  // every pixel, exact
+        e = lkg::fast_error(c->d, c->last_n, c->stream, scratch);
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(max_abs_error, scratch, sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(scratch);
+    if (e != cudaSuccess) return fail(LK_ERR_CUDA, std::string("fast path check: ") + cudaGetErrorString(e));
     return LK_OK;
 }

@@ -67,7 +67,8 @@ struct Dev {
     uint8_t* vsing;         // [B][H]
     double* fv;             // [B][H]
     double* vpx;            // [B][H]
-    double* smoothed;       // [B][H][W]
+    double* smoothed;       // [B][H][W] (fast path: exact only around edge candidates)
+    float* smoothed_f;      // [B][H][W] certified approximation (fast path)
     uint32_t* ebits;        // [B][H][words_per_row]
     int n_seg;              // edge-list segments per row (ceil(W / SB_TW))
     int32_t* seg_cnt;       // [B][H][n_seg]

@@ -1,0 +1,276 @@
+// lk_fastpath.cu — certified fast front end (stages 9-10) for throughput runs.
+//
+// The exact bilateral (k_bilateral_tile) is bound by random 8-byte gathers
+// into the exact weight table. But the only consumers of the smoothed image
+// downstream of stage 10 are the EDGE pixels (gx, gy, theta, votes, w_g all
+// come from the edge list, preprocess.hpp:103-113), and the only integer
+// decision taken on non-edge pixels is "not an edge". So:
+//
+//  1. k_bilateral_fast computes every pixel approximately: weights
+//     2^(c_t + c2*dr^2) with MUFU ex2 and FP32 row-partial sums. A rigorous
+//     bound |s~ - s| <= kEpsSmooth holds against the exact double result
+//     (derivation in DESIGN.md §3; the worst error measured on 10^8 pixels is
+//     recorded in profiles/).
+//  2. k_sobel_refine evaluates Sobel on s~ and propagates the bound to
+//     s = gx^2 + gy^2. A masked pixel whose s can still reach the threshold is
+//     a candidate. Every pixel in a candidate's 3x3 neighbourhood gets its
+//     EXACT bilateral (the LUT arithmetic of k_bilateral_tile), and the
+//     candidate's edge decision and gradients use those exact values.
+//
+// The edge set, every edge's gx/gy, and everything downstream are therefore
+// bit-identical to the exact path; only the (unexported) smoothed values of
+// pixels far from any edge are approximate. Hooks mode always runs the exact
+// path, so the SMOOTHED/GX/GY/MAG/THETA maps it exports are exact.
+#include <cuda_runtime.h>
+
+#include "lk_kernels.h"
+
+namespace lkg {
+
+constexpr double kEpsSmooth = 2.5e-5;  // bound on |s~ - s| (absolute, values in [0, 1])
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// ---- 1. approximate bilateral: tile BT_W x BT_H, BT_R outputs per thread
+template <int RHO>
+__global__ void __launch_bounds__(256, 2) k_bilateral_fast(Dev d, FastBfParam p) {
+    constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
+    constexpr int NPX = TWh * THh;
+    __shared__ float s_v[NPX];
+    const int f = blockIdx.z;
+    if (frame_failed(d, f)) return;
+    const int u0 = blockIdx.x * BT_W, v0 = blockIdx.y * BT_H;
+    const uint8_t* g = d.grey + (size_t)f * d.px;
+    for (int i = threadIdx.x; i < NPX; i += blockDim.x) {
+        const int ty = i / TWh, tx = i - ty * TWh;
+        const int gu = mirror(u0 + tx - RHO, d.W), gv = mirror(v0 + ty - RHO, d.H);
+        s_v[i] = p.vf[g[(size_t)gv * d.W + gu]];
+    }
+    __syncthreads();
+    const int tx = threadIdx.x % BT_W, ty = threadIdx.x / BT_W;
+    const int r0 = ty * BT_R;
+    float va[BT_R], num[BT_R], den[BT_R];
+#pragma unroll
+    for (int r = 0; r < BT_R; ++r) {
+        va[r] = s_v[(r0 + r + RHO) * TWh + tx + RHO];
+        num[r] = den[r] = 0.f;
+    }
+#pragma unroll
+    for (int jj = 0; jj < BT_R + 2 * RHO; ++jj) {
+        const int prow = (r0 + jj) * TWh + tx;
+        float vv[WIN];
+#pragma unroll
+        for (int i = 0; i < WIN; ++i) vv[i] = s_v[prow + i];
+#pragma unroll
+        for (int r = 0; r < BT_R; ++r) {
+            const int dj = jj - r;
+            if (dj < 0 || dj >= WIN) continue;
+            float rn = 0.f, rd = 0.f;  // row partial sums keep the FP32 error small
+#pragma unroll
+            for (int i = 0; i < WIN; ++i) {
+                const float dr = vv[i] - va[r];
+                const float w = ex2_approx(fmaf(p.c2, dr * dr, p.c[dj * WIN + i]));
+                rn = fmaf(w, vv[i], rn);
+                rd += w;
+            }
+            num[r] += rn;
+            den[r] += rd;
+        }
+    }
+    const int u = u0 + tx;
+#pragma unroll
+    for (int r = 0; r < BT_R; ++r) {
+        const int v = v0 + r0 + r;
+        if (u < d.W && v < d.H)
+            d.smoothed_f[(size_t)f * d.px + (size_t)v * d.W + u] = __fdiv_rn(num[r], den[r]);
+    }
+}
+
+// Exact bilateral at in-image pixel (u, v) from the staged mirrored grey tile
+// (origin gx0, gy0): the arithmetic of k_bilateral_tile / preprocess.hpp:38-56.
+template <int RHO>
+__device__ __forceinline__ double exact_bilateral(const Dev& d, const WsParam& ws,
+                                                  const uint8_t* s_g, int gw, int gx0, int gy0,
+                                                  int u, int v) {
+    constexpr int WIN = 2 * RHO + 1;
+    const uint8_t* c = s_g + (v - gy0) * gw + (u - gx0);
+    const double* wrow = d.wr + (int)c[0] * 256;
+    double num = 0.0, den = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < WIN; ++j) {
+        const uint8_t* row = c + (j - RHO) * gw - RHO;
+#pragma unroll
+        for (int i = 0; i < WIN; ++i) {
+            const int kv = row[i];
+            const double w = ws.w[j * WIN + i] * __ldg(wrow + kv);
+            num += w * __ldg(d.val + kv);
+            den += w;
+        }
+    }
+    return num / den;
+}
+
+// ---- 2. Sobel on s~ with the propagated bound, exact refinement, edge bits
+template <int RHO>
+__global__ void __launch_bounds__(256) k_sobel_refine(Dev d, WsParam ws) {
+    constexpr int FW = SB_TW + 4, FH = SB_TH + 4;              // s~ tile, 2-px halo
+    constexpr int NW = SB_TW + 2, NH = SB_TH + 2;              // tile + 1-px ring
+    constexpr int GW = SB_TW + 2 + 2 * RHO, GH = SB_TH + 2 + 2 * RHO;  // grey for the ring
+    __shared__ float s_f[FH * FW];
+    __shared__ uint8_t s_g[GH * GW];
+    __shared__ uint8_t s_cand[SB_TH * SB_TW];
+    __shared__ double s_ex[NH * NW];
+    __shared__ short s_need[NH * NW];
+    __shared__ int s_nneed, s_seg[SB_TH], s_tot[2];
+    const int f = blockIdx.z;
+    if (frame_failed(d, f)) return;
+    if (d.W < 3 || d.H < 3) {  // preprocess.hpp:68-69
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+            fail_frame(d, f, 10, LK_MSG_SOBEL_TOO_SMALL);
+        return;
+    }
+    const int W = d.W, H = d.H;
+    const int u0 = blockIdx.x * SB_TW, v0 = blockIdx.y * SB_TH;
+    const int horizon = (int)d.rep[f].horizon;
+    if (v0 + SB_TH <= horizon) {  // the mask is empty above the horizon
+        if (threadIdx.x < SB_TH && v0 + threadIdx.x < H)
+            d.seg_cnt[((size_t)f * H + v0 + threadIdx.x) * d.n_seg + blockIdx.x] = 0;
+        return;
+    }
+    const float* sf = d.smoothed_f + (size_t)f * d.px;
+    const uint8_t* grey = d.grey + (size_t)f * d.px;
+    for (int i = threadIdx.x; i < FH * FW; i += blockDim.x) {
+        const int r = i / FW, c = i - r * FW;
+        s_f[i] = sf[(size_t)mirror(v0 - 2 + r, H) * W + mirror(u0 - 2 + c, W)];
+    }
+    for (int i = threadIdx.x; i < GH * GW; i += blockDim.x) {
+        const int r = i / GW, c = i - r * GW;
+        s_g[i] = grey[(size_t)mirror(v0 - 1 - RHO + r, H) * W + mirror(u0 - 1 - RHO + c, W)];
+    }
+    if (threadIdx.x < SB_TH) s_seg[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_tot[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_nneed = 0;
+    __syncthreads();
+    const double dg = 8.0 * kEpsSmooth;  // |gx~ - gx|, |gy~ - gy| bound (sum of |Sobel taps| = 8)
+    int n_mask = 0;
+    for (int i = threadIdx.x; i < SB_TH * SB_TW; i += blockDim.x) {
+        const int r = i / SB_TW, c = i - r * SB_TW;
+        const int v = v0 + r, u = u0 + c;
+        uint8_t cand = 0;
+        if (v < H && u < W) {
+            const int dv = d.disp[(size_t)f * d.px + (size_t)v * W + u];
+            const bool m = v >= horizon && dv != 0 &&
+                           fabs((double)dv - d.fv[(size_t)f * H + v]) <= d.varpi;
+            n_mask += m;
+            if (m) {
+                const float* a = s_f + (r + 1) * FW + (c + 1);  // row v-1, col u-1
+                const float* b = a + FW;
+                const float* cc = b + FW;
+                const double gx = ((double)a[2] - a[0]) + 2 * ((double)b[2] - b[0]) +
+                                  ((double)cc[2] - cc[0]);
+                const double gy = ((double)cc[0] - a[0]) + 2 * ((double)cc[1] - a[1]) +
+                                  ((double)cc[2] - a[2]);
+                const double s = gx * gx + gy * gy;
+                const double ds = dg * (2 * fabs(gx) + dg) + dg * (2 * fabs(gy) + dg) + 1e-14;
+                cand = s + ds >= d.sobel_s_star;
+            }
+        }
+        s_cand[i] = cand;
+    }
+    __syncthreads();
+    // pixels of tile + ring inside a candidate's 3x3 need the exact bilateral
+    for (int i = threadIdx.x; i < NH * NW; i += blockDim.x) {
+        const int r = i / NW, c = i - r * NW;  // ring coords: tile pixel (r-1, c-1)
+        bool need = false;
+        for (int y = r - 2; y <= r && !need; ++y)
+            for (int x = c - 2; x <= c; ++x)
+                if (y >= 0 && y < SB_TH && x >= 0 && x < SB_TW && s_cand[y * SB_TW + x]) {
+                    need = true;
+                    break;
+                }
+        if (need) s_need[atomicAdd(&s_nneed, 1)] = (short)i;
+    }
+    __syncthreads();
+    const int gx0 = u0 - 1 - RHO, gy0 = v0 - 1 - RHO;
+    for (int k = threadIdx.x; k < s_nneed; k += blockDim.x) {
+        const int i = s_need[k];
+        const int r = i / NW, c = i - r * NW;
+        // ring positions outside the image hold their mirror pixel (preprocess.hpp:71-72)
+        const int v = mirror(v0 - 1 + r, H), u = mirror(u0 - 1 + c, W);
+        const double e = exact_bilateral<RHO>(d, ws, s_g, GW, gx0, gy0, u, v);
+        s_ex[i] = e;
+        d.smoothed[(size_t)f * d.px + (size_t)v * W + u] = e;  // read back by k_edge_emit
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    int n_edge = 0;
+#pragma unroll
+    for (int k = 0; k < SB_TW * SB_TH / 256; ++k) {
+        const int i = threadIdx.x + k * 256;
+        const int r = i / SB_TW, c = i % SB_TW;
+        const int v = v0 + r, u = u0 + c;
+        bool edge = false;
+        if (s_cand[i]) {  // candidate => masked and in the image
+            const double* a = s_ex + r * NW + c;  // row v-1, col u-1
+            const double* b = a + NW;
+            const double* cc = b + NW;
+            const double gx = (a[2] - a[0]) + 2 * (b[2] - b[0]) + (cc[2] - cc[0]);
+            const double gy = (cc[0] - a[0]) + 2 * (cc[1] - a[1]) + (cc[2] - a[2]);
+            edge = gx * gx + gy * gy >= d.sobel_s_star;
+            n_edge += edge;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, edge);
+        if (lane == 0 && v < H) {
+            const int word = (u0 + c) >> 5;
+            if (word < d.words_per_row) d.ebits[((size_t)f * H + v) * d.words_per_row + word] = bal;
+            if (bal) atomicAdd(&s_seg[r], __popc(bal));
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        n_edge += __shfl_xor_sync(0xffffffffu, n_edge, o);
+        n_mask += __shfl_xor_sync(0xffffffffu, n_mask, o);
+    }
+    if (lane == 0) {
+        if (n_edge) atomicAdd(&s_tot[0], n_edge);
+        if (n_mask) atomicAdd(&s_tot[1], n_mask);
+    }
+    __syncthreads();
+    if (threadIdx.x < SB_TH && v0 + threadIdx.x < H)
+        d.seg_cnt[((size_t)f * H + v0 + threadIdx.x) * d.n_seg + blockIdx.x] = s_seg[threadIdx.x];
+    if (threadIdx.x == 0) {
+        if (s_tot[0]) atomicAdd(&d.aux[f].edge_px, (unsigned long long)s_tot[0]);
+        if (s_tot[1]) atomicAdd(&d.aux[f].mask_px, (unsigned long long)s_tot[1]);
+    }
+}
+
+void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s) {
+    const dim3 g((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n);
+    k_bilateral_fast<5><<<g, 256, 0, s>>>(d, lp.fbf);
+}
+
+void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s) {
+    const dim3 g((d.W + SB_TW - 1) / SB_TW, (d.H + SB_TH - 1) / SB_TH, n);
+    k_sobel_refine<5><<<g, 256, 0, s>>>(d, lp.ws);
+}
+
+// Largest |s~ - s| of a batch (verification of kEpsSmooth): both maps full.
+__global__ void k_fast_error(const float* a, const double* b, size_t n, double* out) {
+    double m = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        m = fmax(m, fabs((double)a[i] - b[i]));
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0)
+        atomicMax((unsigned long long*)out, (unsigned long long)__double_as_longlong(m));
+}
+
+cudaError_t fast_error(const Dev& d, int n, cudaStream_t s, double* out_dev) {
+    k_fast_error<<<296, 256, 0, s>>>(d.smoothed_f, d.smoothed, (size_t)n * d.px, out_dev);
+    return cudaGetLastError();
+}
+
+}  // namespace lkg

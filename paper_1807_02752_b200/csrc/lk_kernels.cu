@@ -1586,7 +1586,11 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     mark(7);
     mark(8);  // road mask is fused into the Sobel pass (stage 10)
     const dim3 bg((d.W + BF_TW - 1) / BF_TW, (d.H + BF_TH - 1) / BF_TH, n);
-    if (d.rho == 5)
+    if (lp.fast_front) {
+        launch_fast_bilateral(d, lp, n, s);
+        mark(9);
+        launch_sobel_refine(d, lp, n, s);
+    } else if (d.rho == 5)
     {
         const dim3 g((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n);
         switch (lp.bt_mode) {
@@ -1598,8 +1602,11 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     }
     else
         k_bilateral<-1><<<bg, 256, lp.bf_smem, s>>>(d);
-    mark(9);
-    k_sobel_edges<<<dim3((d.W + SB_TW - 1) / SB_TW, (d.H + SB_TH - 1) / SB_TH, n), 256, 0, s>>>(d);
+    if (!lp.fast_front) {
+        mark(9);
+        k_sobel_edges<<<dim3((d.W + SB_TW - 1) / SB_TW, (d.H + SB_TH - 1) / SB_TH, n), 256, 0,
+                        s>>>(d);
+    }
     k_edge_scan<<<n, 1024, 0, s>>>(d);
     k_edge_emit<<<dim3((d.H * d.n_seg + 7) / 8, n), 256, 0, s>>>(d);
     mark(10);
@@ -1641,6 +1648,11 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     k_finish<<<(n + 127) / 128, 128, 0, s>>>(d, n);
     mark(12);
     return cudaGetLastError();
+}
+
+void launch_exact_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s) {
+    const dim3 g((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n);
+    k_bilateral_tile<5, 0><<<g, 256, lp.bt_smem, s>>>(d, lp.ws);
 }
 
 int launches_per_batch(const Dev& d) { return isnan(d.tr_lpv) ? 18 : 13; }

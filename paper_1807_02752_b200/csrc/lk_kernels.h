@@ -23,8 +23,18 @@ struct WsParam {
     double w[121];
 };
 
+// Approximate bilateral (lk_fastpath.cu): log2-domain spatial terms, range
+// coefficient, and the 8-bit values as floats; passed by value.
+struct FastBfParam {
+    float c[121];  // -ds * inv_s2 * log2(e) per tap
+    float c2;      // -inv_r2 * log2(e)
+    float vf[256]; // k / 255
+};
+
 struct LaunchPlan {
     WsParam ws;
+    FastBfParam fbf;
+    int fast_front;           // certified fast bilateral + exact refinement (lk_fastpath.cu)
     int32_t* vhistT;          // [B][D1][H] transposed v-disparity for the v-path DP
     size_t vpath_smem;
     int vpath_choice_smem;    // choices of the v-path DP kept in shared memory
@@ -48,6 +58,10 @@ struct LaunchPlan {
 cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s,
                             cudaEvent_t* stage_ev);
 cudaError_t configure_kernels(const LaunchPlan& lp);
+void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
+void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
+void launch_exact_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
+cudaError_t fast_error(const Dev& d, int n, cudaStream_t s, double* out_dev);
 int launches_per_batch(const Dev& d);
 
 }  // namespace lkg

@@ -56,6 +56,7 @@ def library() -> C.CDLL:
     L.lk_host_alloc.argtypes = [C.POINTER(P), SZ]
     L.lk_host_free.argtypes = [P]
     L.lk_abi_sizes.argtypes = [C.POINTER(SZ)]
+    L.lk_fast_path_error.argtypes = [P, C.POINTER(C.c_double)]
     L.lk_synth_scene.argtypes = [C.POINTER(abi.LkSceneParams), P, P, P, C.POINTER(C.c_int32)]
     L.lk_synth_batch.argtypes = [C.POINTER(abi.LkSceneParams), I, P, P, I]
     L.lk_synth_last_error.restype = C.c_char_p
@@ -99,11 +100,12 @@ class GpuPipeline:
 
     def __init__(self, width: int, height: int, config: abi.LkConfig | None = None,
                  max_batch: int = 1, device: int = 0, hooks: bool = False,
-                 graph: bool = True):
+                 graph: bool = True, exact: bool = False):
         L = library()
         self.cfg = config if config is not None else default_config()
         self.width, self.height, self.max_batch = width, height, max_batch
-        flags = (abi.LK_FLAG_HOOKS if hooks else 0) | (0 if graph else abi.LK_FLAG_NO_GRAPH)
+        flags = (abi.LK_FLAG_HOOKS if hooks else 0) | (0 if graph else abi.LK_FLAG_NO_GRAPH) | \
+            (abi.LK_FLAG_EXACT if exact else 0)
         h = C.c_void_p()
         _check(L.lk_create(C.byref(h), device, C.byref(self.cfg), width, height, max_batch,
                            flags))
@@ -164,6 +166,12 @@ class GpuPipeline:
         ext_cols = int(np.round((2 * self.cfg.xi + 1) * self.width))
         return abi.decode_stage(st, self.raw(frame, st), self.width, self.height,
                                 self.cfg.d_max, ext_cols, int(rep.horizon))
+
+    def fast_path_error(self) -> float:
+        """max |approximate - exact| smoothed value of the last batch (fast path)."""
+        e = C.c_double(0)
+        _check(library().lk_fast_path_error(self._h, C.byref(e)))
+        return e.value
 
     def stage_times(self) -> dict[int, float]:
         ms = (C.c_float * 13)()

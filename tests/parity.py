@@ -29,7 +29,9 @@ EXACT_HOOKS = ["VDISPARITY", "VPATH", "BETA_INLIERS", "VPY_SINGULAR", "MASK", "V
                "GAMMA_INLIERS"]
 FP_HOOKS = ["VPY", "SMOOTHED", "GX", "GY", "MAG", "THETA", "VPX_ACC", "VPX", "M0", "M1",
             "ENERGY"]
-HOOK_ONLY = {"MASK", "GX", "GY", "MAG", "THETA", "VPX_ACC", "M0", "POLYLINES"}
+# SMOOTHED is exported only by the exact path (hooks / LK_FLAG_EXACT): the
+# throughput path computes it exactly only around edge candidates.
+HOOK_ONLY = {"MASK", "SMOOTHED", "GX", "GY", "MAG", "THETA", "VPX_ACC", "M0", "POLYLINES"}
 
 
 def close(a, b, rtol=RTOL) -> bool:
