@@ -143,20 +143,21 @@ __global__ void __launch_bounds__(256) k_sobel_refine(Dev d, WsParam ws) {
     }
     const float* sf = d.smoothed_f + (size_t)f * d.px;
     const uint8_t* grey = d.grey + (size_t)f * d.px;
+    // mirrored row offsets / columns of the grey halo (the s~ halo is its inner part)
+    __shared__ int s_rowg[GH], s_colg[GW];
+    for (int i = threadIdx.x; i < GH; i += blockDim.x) s_rowg[i] = mirror(v0 - 1 - RHO + i, H) * W;
+    for (int i = threadIdx.x; i < GW; i += blockDim.x) s_colg[i] = mirror(u0 - 1 - RHO + i, W);
+    __syncthreads();
     for (int i = threadIdx.x; i < FH * FW; i += blockDim.x) {
-        const int r = i / FW, c = i - r * FW;
-        s_f[i] = sf[(size_t)mirror(v0 - 2 + r, H) * W + mirror(u0 - 2 + c, W)];
-    }
-    for (int i = threadIdx.x; i < GH * GW; i += blockDim.x) {
-        const int r = i / GW, c = i - r * GW;
-        s_g[i] = grey[(size_t)mirror(v0 - 1 - RHO + r, H) * W + mirror(u0 - 1 - RHO + c, W)];
+        const int r = i / FW, c = i - r * FW;  // s~ row v0-2+r = grey row index r + RHO - 1
+        s_f[i] = sf[(size_t)s_rowg[r + RHO - 1] + s_colg[c + RHO - 1]];
     }
     if (threadIdx.x < SB_TH) s_seg[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_tot[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_nneed = 0;
     __syncthreads();
     const double dg = 8.0 * kEpsSmooth;  // |gx~ - gx|, |gy~ - gy| bound (sum of |Sobel taps| = 8)
-    int n_mask = 0;
+    int n_mask = 0, any_cand = 0;
     for (int i = threadIdx.x; i < SB_TH * SB_TW; i += blockDim.x) {
         const int r = i / SB_TW, c = i - r * SB_TW;
         const int v = v0 + r, u = u0 + c;
@@ -180,8 +181,20 @@ __global__ void __launch_bounds__(256) k_sobel_refine(Dev d, WsParam ws) {
             }
         }
         s_cand[i] = cand;
+        any_cand |= cand;
     }
-    __syncthreads();
+    if (!__syncthreads_or(any_cand)) {  // no edge can exist in this tile (most tiles)
+        for (int o = 16; o; o >>= 1) n_mask += __shfl_xor_sync(0xffffffffu, n_mask, o);
+        if ((threadIdx.x & 31) == 0 && n_mask)
+            atomicAdd(&d.aux[f].mask_px, (unsigned long long)n_mask);
+        if (threadIdx.x < SB_TH && v0 + threadIdx.x < H)
+            d.seg_cnt[((size_t)f * H + v0 + threadIdx.x) * d.n_seg + blockIdx.x] = 0;
+        return;
+    }
+    for (int i = threadIdx.x; i < GH * GW; i += blockDim.x) {
+        const int r = i / GW, c = i - r * GW;
+        s_g[i] = grey[(size_t)s_rowg[r] + s_colg[c]];
+    }
     // pixels of tile + ring inside a candidate's 3x3 need the exact bilateral
     for (int i = threadIdx.x; i < NH * NW; i += blockDim.x) {
         const int r = i / NW, c = i - r * NW;  // ring coords: tile pixel (r-1, c-1)

@@ -23,7 +23,7 @@
 
 namespace lkg {
 
-constexpr int RS_MAX_WARPS = 8;
+constexpr int RS_MAX_WARPS = 16;
 
 struct RansacState {  // lives in shared memory
     double model[5];

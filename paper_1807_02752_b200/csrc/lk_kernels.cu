@@ -987,7 +987,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
 // (:276-281), then the w_g edge weights of build_m0 (lanes.hpp:35-44).
 // One CTA per frame; warp 0 runs the RANSAC.
 // =====================================================================
-__global__ void __launch_bounds__(256, 4) k_gamma_fit(Dev d) {
+__global__ void __launch_bounds__(512, 2) k_gamma_fit(Dev d) {
     extern __shared__ int sh_g[];
     const int f = blockIdx.x;
     if (frame_failed(d, f)) return;
@@ -995,7 +995,7 @@ __global__ void __launch_bounds__(256, 4) k_gamma_fit(Dev d) {
     lk_frame_report& rep = d.rep[f];
     const int v_top = (int)rep.horizon, v_max = H - 1;
     const int nrows = v_max - v_top + 1;
-    constexpr int NW = 8;  // 256 threads
+    constexpr int NW = 16;  // 512 threads: 16 speculative RANSAC iterations per round
     int* px = sh_g;
     int* pv = px + H;
     int* bufs[NW + 2];
@@ -1404,24 +1404,39 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
     double u = (double)(d.ext_lo + ci);
     bool alive = true;
     double e = 0.0;
-    for (int v = v_max; v >= v_top; --v) {
-        if (v < v_max && alive) {
-            const double py = vpy[v + 1];
-            const double denom = (double)(v + 1) - py;
-            if (fabs(denom) < 0.5) {
-                alive = false;
-            } else {
-                u = (vpx[v + 1] + v * u - py * u) / denom;
+    // Chunks of EC rows: the track recursion (a pure division chain) yields EC
+    // gather indices, the EC m1 loads are then all in flight together, and the
+    // decayed sum consumes them in row order (same arithmetic, same order).
+    constexpr int EC = 8;
+    for (int vc = v_max; vc >= v_top; vc -= EC) {
+        int idx[EC];
+#pragma unroll
+        for (int k = 0; k < EC; ++k) {
+            const int v = vc - k;
+            idx[k] = -1;
+            if (v < v_top) continue;
+            if (v < v_max && alive) {
+                const double py = vpy[v + 1];
+                const double denom = (double)(v + 1) - py;
+                if (fabs(denom) < 0.5) {
+                    alive = false;
+                } else {
+                    u = (vpx[v + 1] + v * u - py * u) / denom;
+                }
+            }
+            if (alive && !isnan(u)) {
+                const long long r = llround_ref(u);
+                if (r >= 0 && r < W && v >= 0 && v < H &&
+                    nz[(v >> d.m_tile_shift) * d.m_ntx + ((int)r >> 7)])
+                    idx[k] = v * W + (int)r;  // < W*H <= 2^31
             }
         }
-        double contrib = 0.0;
-        if (alive && !isnan(u)) {
-            const long long r = llround_ref(u);
-            if (r >= 0 && r < W && v >= 0 && v < H &&
-                nz[(v >> d.m_tile_shift) * d.m_ntx + ((int)r >> 7)])
-                contrib = m1[(size_t)v * W + (int)r];
-        }
-        e = contrib + lg * e;
+        double c[EC];
+#pragma unroll
+        for (int k = 0; k < EC; ++k) c[k] = idx[k] >= 0 ? m1[idx[k]] : 0.0;
+#pragma unroll
+        for (int k = 0; k < EC; ++k)
+            if (vc - k >= v_top) e = c[k] + lg * e;
     }
     d.energy[(size_t)f * d.ext_cols + ci] = e;
 }
@@ -1631,7 +1646,7 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
         }
     }
 #undef LK_VANISH
-    k_gamma_fit<<<n, 256, lp.gamma_smem, s>>>(d);
+    k_gamma_fit<<<n, 512, lp.gamma_smem, s>>>(d);
     mark(11);
     const bool auto_tr = isnan(d.tr_lpv);
     k_m0_m1<<<dim3((d.W + M_TW - 1) / M_TW, (d.H + lp.m_tile_h - 1) / lp.m_tile_h, n), 256,
