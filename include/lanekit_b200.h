@@ -243,13 +243,20 @@ lk_status lk_get_stage(lk_ctx* ctx, int frame, int stage, void* dst, size_t capa
 /* Device milliseconds of the last batch per pipeline stage 5..12 (ms[5..12]),
  * from CUDA events recorded on the context stream around each stage's kernels
  * (event-record nodes inside the CUDA graph); ms[0] is the whole batch.
- * Stage 8 (road mask) is fused into stage 10's Sobel pass and reads ~0. */
+ * Stage 8 (road mask) is fused into stage 10's Sobel pass and reads ~0.
+ * A captured batch runs as up to LK_BRANCHES (env, default 2) concurrent
+ * frame ranges; the events time the first range (lk_timed_frames frames)
+ * while the others overlap it. ms[0] is then that range's span. */
 lk_status lk_stage_times(lk_ctx* ctx, float ms[13]);
+
+/* Frames of the last batch covered by lk_stage_times. */
+int lk_timed_frames(lk_ctx* ctx);
 
 /* Measured FP64 add+mul issue rate of this device (ops/s), for rooflines. */
 lk_status lk_measure_fp64(int device, double* ops_per_s);
 
-/* Number of kernel launches one lk_run_batch / lk_enqueue issues. */
+/* Number of kernel launches one lk_run_batch / lk_enqueue issues (all
+ * branches of the last batch size, else of max_batch). */
 int lk_launches_per_batch(lk_ctx* ctx);
 
 /* Largest |approximate - exact| smoothed value over the last batch: verifies

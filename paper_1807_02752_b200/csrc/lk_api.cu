@@ -78,6 +78,9 @@ const char* config_problem(const lk_config& c) {
 }
 
 constexpr int kMaxIter = 200;  // pipeline.hpp:198, 244
+constexpr int kMaxBranches = 4;       // concurrent frame ranges in a captured batch
+constexpr int kMinBranchFrames = 16;  // smallest range worth a branch
+constexpr int kFastTableDefault = 27;  // tap pairs of the fast bilateral served by the range table
 
 }  // namespace
 
@@ -90,6 +93,10 @@ struct lk_ctx {
     LaunchPlan lp{};
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[13] = {};
+    int branches = 1;
+    cudaStream_t side[kMaxBranches - 1] = {};
+    cudaEvent_t fork = nullptr, join[kMaxBranches - 1] = {};
+    int timed_frames = 0;
     bool timed = false;
     std::vector<void*> allocs;
     std::map<int, cudaGraphExec_t> graphs;
@@ -300,6 +307,8 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         if (s == LK_OK) s = c->alloc(p, n);
     };
     double *d_ws, *d_wr, *d_val;
+    float* d_ft = nullptr;
+    std::vector<float> fast_tab;
     uint64_t* d_rng;
     A(&d_ws, ws.size());
     A(&d_wr, wr.size());
@@ -369,7 +378,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     lp.vpath_choice_smem = vp_base + (size_t)D1 * H <= 160 * 1024;
     lp.vpath_smem = vp_base + (lp.vpath_choice_smem ? (size_t)D1 * H : 0);
     if (!lp.vpath_choice_smem) A(&d.vchoice, (size_t)B * D1 * H);
-    lp.road_smem = (size_t)(8 * D1 + 2) * 4 + (size_t)D1 * 8 + 16;
+    lp.road_smem = (size_t)(8 * D1 + 2) * 4 + (size_t)4 * D1 * 8 + 16;  // tbuf: (K+1) rows
     lp.bf_smem = (size_t)(256 + win * win) * 8 +
                  (size_t)(lkg::BF_TH + 2 * rho) * (lkg::BF_TW + 2 * rho) + 16;
     {
@@ -393,9 +402,26 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
             for (int di = -5; di <= 5; ++di)
                 lp.fbf.c[(dj + 5) * 11 + (di + 5)] =
                     (float)(-(double)(di * di + dj * dj) * inv_s2 * log2e);
+        for (int dj = 0; dj < 11; ++dj)
+            for (int q = 0; q < 5; ++q)
+                lp.fbf.cp[dj][q] = make_float2(lp.fbf.c[dj * 11 + 2 * q], lp.fbf.c[dj * 11 + 2 * q + 1]);
         lp.fbf.c2 = (float)(-inv_r2 * log2e);
         for (int k = 0; k < 256; ++k) lp.fbf.vf[k] = (float)(k / 255.0);
+        for (int dj = -5; dj <= 5; ++dj)
+            for (int q = 0; q < 5; ++q) {
+                auto sf = [&](int di) { return (float)std::exp(-(double)(di * di + dj * dj) * inv_s2); };
+                lp.fbf.sp[dj + 5][q] = make_float2(sf(2 * q - 5), sf(2 * q - 4));
+            }
+        fast_tab.resize(256 + 512);
+        for (int k = 0; k < 256; ++k) fast_tab[k] = lp.fbf.vf[k];
+        for (int i = 0; i < 512; ++i) {
+            const double dr = (i - 255) / 255.0;
+            fast_tab[256 + i] = i < 511 ? (float)std::exp(-dr * dr * inv_r2) : 0.f;
+        }
+        const char* m = std::getenv("LK_BF_TABLE");
+        lp.fast_table = m ? std::atoi(m) & 31 : kFastTableDefault;
         if (lp.fast_front) A(&d.smoothed_f, (size_t)B * d.px);
+        A(&d_ft, fast_tab.size());
     }
     lp.vanish_smem = (size_t)2 * C * 8 + (size_t)C * 4 + (size_t)2 * H * 4 +
                      (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 8 + (size_t)(H + 1) * 4 +
@@ -407,7 +433,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     if (lp.upath_sp == 7) lp.upath_sp = 8;
     if (lp.upath_nt == 1024 && lp.upath_sp < 5) lp.upath_sp = 5;
     if (lp.upath_sp > 8) lp.upath_sp = 0;
-    lp.gamma_smem = (size_t)20 * H * 4 + 8 + (size_t)H * 8 + 16;  // px, pv, NW+2 lists, t
+    lp.gamma_smem = (size_t)20 * H * 4 + 8 + (size_t)6 * H * 8 + 16;  // px, pv, NW+2 lists, basis rows
     lp.m_tile_h = 16;
     auto m_bytes = [&](int th) {
         const size_t GH = th + 2 + 2 * cfg->varsigma, GW = lkg::M_TW + 2 + 2 * cfg->nu;
@@ -451,8 +477,21 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     if (e == cudaSuccess) e = cudaMemcpy(d_wr, wr.data(), wr.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d_val, val.data(), val.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d_rng, rng.data(), rng.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_ft, fast_tab.data(), fast_tab.size() * 4, cudaMemcpyHostToDevice);
+    d.fast_tab = d_ft;
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     for (int i = 0; i < 13 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    {
+        const char* b = std::getenv("LK_BRANCHES");
+        c->branches = b ? std::atoi(b) : 2;
+        if (c->branches < 1) c->branches = 1;
+        if (c->branches > kMaxBranches) c->branches = kMaxBranches;
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+    for (int i = 0; i < c->branches - 1 && e == cudaSuccess; ++i) {
+        e = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join[i], cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) {
         lk_destroy(c);
         return fail(LK_ERR_CUDA, std::string("context setup: ") + cudaGetErrorString(e));
@@ -469,6 +508,14 @@ lk_status lk_destroy(lk_ctx* c) {
     if (c->d.wr_tex) cudaDestroyTextureObject((cudaTextureObject_t)c->d.wr_tex);
     for (cudaEvent_t e : c->ev)
         if (e) cudaEventDestroy(e);
+    if (c->fork) cudaEventDestroy(c->fork);
+    for (int i = 0; i < kMaxBranches - 1; ++i) {
+        if (c->join[i]) cudaEventDestroy(c->join[i]);
+        if (c->side[i]) {
+            cudaStreamSynchronize(c->side[i]);
+            cudaStreamDestroy(c->side[i]);
+        }
+    }
     for (void* p : c->allocs) cudaFree(p);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -477,7 +524,14 @@ lk_status lk_destroy(lk_ctx* c) {
 
 void* lk_stream(lk_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
-int lk_launches_per_batch(lk_ctx* c) { return c ? lkg::launches_per_batch(c->d) : 0; }
+static int branch_count(const lk_ctx* c, int n);
+
+int lk_launches_per_batch(lk_ctx* c) {
+    return c ? lkg::launches_per_batch(c->d) * branch_count(c, c->last_n ? c->last_n : c->max_batch)
+             : 0;
+}
+
+int lk_timed_frames(lk_ctx* c) { return c ? c->timed_frames : 0; }
 
 lk_status lk_device_inputs(lk_ctx* c, uint8_t** grey, uint8_t** disparity) {
     if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
@@ -486,15 +540,107 @@ lk_status lk_device_inputs(lk_ctx* c, uint8_t** grey, uint8_t** disparity) {
     return LK_OK;
 }
 
-static lk_status enqueue_direct(lk_ctx* c, int n, bool timed) {
+// View of frames [f0, f0 + ...) of every frame-major buffer: the same kernels
+// run on a sub-batch without knowing it (layouts are frame-major throughout).
+static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     const Dev& d = c->d;
-    CU(cudaMemsetAsync(d.rep, 0, (size_t)n * sizeof(lk_frame_report), c->stream));
-    CU(cudaMemsetAsync(d.aux, 0, (size_t)n * sizeof(FrameAux), c->stream));
+    v = d;
+    lp = c->lp;
+    const size_t H = d.H, px = d.px, C = d.ext_cols, D1 = d.D1;
+    auto sh = [&](auto& p, size_t per) {
+        if (p) p += f0 * per;
+    };
+    sh(v.grey, px);
+    sh(v.disp, px);
+    sh(v.rep, 1);
+    sh(v.aux, 1);
+    sh(v.vhist, H * D1);
+    sh(lp.vhistT, H * D1);
+    sh(v.vchoice, D1 * H);
+    sh(v.vpath, D1 * 2);
+    sh(v.beta_inl, D1 * 2);
+    sh(v.vpy, H);
+    sh(v.vsing, H);
+    sh(v.fv, H);
+    sh(v.vpx, H);
+    sh(v.smoothed, px);
+    sh(v.smoothed_f, px);
+    sh(v.ebits, H * d.words_per_row);
+    sh(v.seg_cnt, H * d.n_seg);
+    sh(v.seg_off, H * d.n_seg);
+    sh(v.row_off, H + 1);
+    sh(v.e_uv, px);
+    sh(v.e_gx, px);
+    sh(v.e_gy, px);
+    sh(v.e_th, px);
+    sh(v.e_wg, px);
+    sh(v.e_col, px);
+    sh(v.uchoice, H * C);
+    sh(v.upath, H * 2);
+    sh(v.gamma_inl, H * 2);
+    sh(v.m1, px);
+    sh(v.m1_nz, (size_t)d.m_ntx * d.m_nty);
+    sh(v.p99hist, 2048);
+    sh(v.p99hist2, 4096);
+    sh(v.p99cand, px);
+    sh(v.energy, C);
+    sh(v.lanes, (size_t)d.lane_cap);
+    sh(v.polylines, (size_t)d.lane_cap * H);
+    sh(v.mask, px);
+    sh(v.gx, px);
+    sh(v.gy, px);
+    sh(v.mag, px);
+    sh(v.theta, px);
+    sh(v.acc, H * C);
+    sh(v.m0, px);
+}
+
+static lk_status enqueue_range(lk_ctx* c, size_t f0, int n, cudaStream_t st, cudaEvent_t* ev) {
+    Dev d;
+    LaunchPlan lp;
+    frame_view(c, f0, d, lp);
+    CU(cudaMemsetAsync(d.rep, 0, (size_t)n * sizeof(lk_frame_report), st));
+    CU(cudaMemsetAsync(d.aux, 0, (size_t)n * sizeof(FrameAux), st));
     if (std::isnan(d.tr_lpv)) {
-        CU(cudaMemsetAsync(d.p99hist, 0, (size_t)n * 2048 * sizeof(unsigned), c->stream));
-        CU(cudaMemsetAsync(d.p99hist2, 0, (size_t)n * 4096 * sizeof(unsigned), c->stream));
+        CU(cudaMemsetAsync(d.p99hist, 0, (size_t)n * 2048 * sizeof(unsigned), st));
+        CU(cudaMemsetAsync(d.p99hist2, 0, (size_t)n * 4096 * sizeof(unsigned), st));
     }
-    CU(lkg::launch_pipeline(d, c->lp, n, c->stream, timed ? c->ev : nullptr));
+    CU(lkg::launch_pipeline(d, lp, n, st, ev));
+    return LK_OK;
+}
+
+// Graph mode splits the batch into up to kMaxBranches frame ranges captured
+// on forked streams: one range's latency-bound per-frame kernels (DP,
+// RANSAC, selection) then overlap another range's throughput-bound
+// bilateral/Sobel passes instead of leaving most SMs idle. Stage events
+// time branch 0 (lk_timed_frames frames).
+static int branch_count(const lk_ctx* c, int n) {
+    if (c->flags & LK_FLAG_NO_GRAPH) return 1;
+    int b = c->branches;
+    while (b > 1 && n / b < kMinBranchFrames) --b;
+    return b;
+}
+
+static lk_status enqueue_direct(lk_ctx* c, int n, bool timed) {
+    const int nb = branch_count(c, n);
+    if (nb == 1) {
+        c->timed_frames = n;
+        return enqueue_range(c, 0, n, c->stream, timed ? c->ev : nullptr);
+    }
+    CU(cudaEventRecord(c->fork, c->stream));
+    size_t f0 = 0;
+    for (int b = 0; b < nb; ++b) {
+        const int nf = n / nb + (b < n % nb);
+        cudaStream_t st = b == 0 ? c->stream : c->side[b - 1];
+        if (b) CU(cudaStreamWaitEvent(st, c->fork, 0));
+        if (b == 0) c->timed_frames = nf;
+        if (lk_status s = enqueue_range(c, f0, nf, st, (timed && b == 0) ? c->ev : nullptr)) return s;
+        f0 += nf;
+    }
+    for (int b = 1; b < nb; ++b) {
+        CU(cudaEventRecord(c->join[b - 1], c->side[b - 1]));
+        CU(cudaStreamWaitEvent(c->stream, c->join[b - 1], 0));
+    }
     return LK_OK;
 }
 

@@ -69,6 +69,7 @@ struct Dev {
     double* vpx;            // [B][H]
     double* smoothed;       // [B][H][W] (fast path: exact only around edge candidates)
     float* smoothed_f;      // [B][H][W] certified approximation (fast path)
+    const float* fast_tab;  // [256] k/255 as float, then [512] range factor of dr = (i-255)/255
     uint32_t* ebits;        // [B][H][words_per_row]
     int n_seg;              // edge-list segments per row (ceil(W / SB_TW))
     int32_t* seg_cnt;       // [B][H][n_seg]

@@ -36,49 +36,90 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 // ---- 1. approximate bilateral: tile BT_W x BT_H, BT_R outputs per thread
-template <int RHO>
-__global__ void __launch_bounds__(256, 2) k_bilateral_fast(Dev d, FastBfParam p) {
+//
+// Taps (2q, 2q+1) of a window row are processed as one packed f32x2 lane pair
+// (FADD2 / FMUL2 / FFMA2), which halves the FP32 issue slots and leaves the
+// range factor as the limiter. Tap pairs in the mask TB take it from a
+// 511-entry shared-memory table instead of MUFU ex2, so the XU and the LSU
+// pipes share the work. The table index comes from the float difference
+// itself: dr*1020 is within 1e-4 of the integer 4(k_q - k_p), so one FFMA with
+// 1.5*2^23 rounds it into the low mantissa bits (no integer keys staged).
+// w = S_t * R[dr] rounds three times in FP32 (~2e-7 relative), inside the
+// ex2.approx error the bound in DESIGN.md already budgets.
+template <int RHO, int TB>
+__global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p) {
     constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
     constexpr int NPX = TWh * THh;
-    __shared__ float s_v[NPX];
+    static_assert(WIN == 11, "packed tap pairs assume an 11-wide window");
+    __shared__ float s_v[NPX], s_vf[256], s_R[512];
+    __shared__ int s_row[THh], s_col[TWh];
     const int f = blockIdx.z;
     if (frame_failed(d, f)) return;
     const int u0 = blockIdx.x * BT_W, v0 = blockIdx.y * BT_H;
     const uint8_t* g = d.grey + (size_t)f * d.px;
+    s_vf[threadIdx.x] = __ldg(d.fast_tab + threadIdx.x);
+    if (TB) {
+        s_R[threadIdx.x] = __ldg(d.fast_tab + 256 + threadIdx.x);
+        s_R[threadIdx.x + 256] = __ldg(d.fast_tab + 512 + threadIdx.x);
+    }
+    if (threadIdx.x < THh) s_row[threadIdx.x] = mirror(v0 + (int)threadIdx.x - RHO, d.H) * d.W;
+    if (threadIdx.x < TWh) s_col[threadIdx.x] = mirror(u0 + (int)threadIdx.x - RHO, d.W);
+    __syncthreads();
     for (int i = threadIdx.x; i < NPX; i += blockDim.x) {
         const int ty = i / TWh, tx = i - ty * TWh;
-        const int gu = mirror(u0 + tx - RHO, d.W), gv = mirror(v0 + ty - RHO, d.H);
-        s_v[i] = p.vf[g[(size_t)gv * d.W + gu]];
+        s_v[i] = s_vf[g[(size_t)s_row[ty] + s_col[tx]]];
     }
     __syncthreads();
     const int tx = threadIdx.x % BT_W, ty = threadIdx.x / BT_W;
     const int r0 = ty * BT_R;
     float va[BT_R], num[BT_R], den[BT_R];
+    float2 nva[BT_R];
 #pragma unroll
     for (int r = 0; r < BT_R; ++r) {
         va[r] = s_v[(r0 + r + RHO) * TWh + tx + RHO];
+        nva[r] = make_float2(-va[r], -va[r]);
         num[r] = den[r] = 0.f;
     }
+    const float2 c2 = make_float2(p.c2, p.c2);
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float + kMagic rounds to an integer
+    // t = dr*1020 + kMagic + 1020: its bit pattern is __float_as_int(kMagic) + the
+    // BYTE offset 4*(k_q - k_p + 255) of the table entry, so the LDS needs no
+    // address arithmetic beyond one add of a uniform base
+    const float2 k1020 = make_float2(1020.f, 1020.f), mg = make_float2(kMagic + 1020.f, kMagic + 1020.f);
+    const char* Rb = reinterpret_cast<const char*>(s_R) - __float_as_int(kMagic);
 #pragma unroll
     for (int jj = 0; jj < BT_R + 2 * RHO; ++jj) {
         const int prow = (r0 + jj) * TWh + tx;
-        float vv[WIN];
+        float2 vp[5];
 #pragma unroll
-        for (int i = 0; i < WIN; ++i) vv[i] = s_v[prow + i];
+        for (int q = 0; q < 5; ++q) vp[q] = make_float2(s_v[prow + 2 * q], s_v[prow + 2 * q + 1]);
+        const float vl = s_v[prow + 10];
 #pragma unroll
         for (int r = 0; r < BT_R; ++r) {
             const int dj = jj - r;
             if (dj < 0 || dj >= WIN) continue;
-            float rn = 0.f, rd = 0.f;  // row partial sums keep the FP32 error small
+            // row partial sums keep the FP32 error small (two interleaved chains)
+            float2 rn = make_float2(0.f, 0.f), rd = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int i = 0; i < WIN; ++i) {
-                const float dr = vv[i] - va[r];
-                const float w = ex2_approx(fmaf(p.c2, dr * dr, p.c[dj * WIN + i]));
-                rn = fmaf(w, vv[i], rn);
-                rd += w;
+            for (int q = 0; q < 5; ++q) {
+                const float2 dr = __fadd2_rn(vp[q], nva[r]);
+                float2 w;
+                if ((TB >> q) & 1) {
+                    const float2 t = __ffma2_rn(dr, k1020, mg);
+                    w = __fmul2_rn(p.sp[dj][q],
+                                   make_float2(*reinterpret_cast<const float*>(Rb + __float_as_int(t.x)),
+                                               *reinterpret_cast<const float*>(Rb + __float_as_int(t.y))));
+                } else {
+                    const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.cp[dj][q]);
+                    w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                }
+                rn = __ffma2_rn(w, vp[q], rn);
+                rd = __fadd2_rn(w, rd);
             }
-            num[r] += rn;
-            den[r] += rd;
+            const float dr = vl - va[r];
+            const float w = ex2_approx(fmaf(p.c2, dr * dr, p.c[dj * WIN + 10]));
+            num[r] += fmaf(w, vl, rn.x + rn.y);
+            den[r] += (rd.x + rd.y) + w;
         }
     }
     const int u = u0 + tx;
@@ -225,7 +266,7 @@ __global__ void __launch_bounds__(256) k_sobel_refine(Dev d, WsParam ws) {
     for (int k = 0; k < SB_TW * SB_TH / 256; ++k) {
         const int i = threadIdx.x + k * 256;
         const int r = i / SB_TW, c = i % SB_TW;
-        const int v = v0 + r, u = u0 + c;
+        const int v = v0 + r;
         bool edge = false;
         if (s_cand[i]) {  // candidate => masked and in the image
             const double* a = s_ex + r * NW + c;  // row v-1, col u-1
@@ -262,7 +303,13 @@ __global__ void __launch_bounds__(256) k_sobel_refine(Dev d, WsParam ws) {
 
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s) {
     const dim3 g((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n);
-    k_bilateral_fast<5><<<g, 256, 0, s>>>(d, lp.fbf);
+    switch (lp.fast_table) {
+#define LK_BF(M) \
+    case M: k_bilateral_fast<5, M><<<g, 256, 0, s>>>(d, lp.fbf); break;
+        LK_BF(0) LK_BF(2) LK_BF(10) LK_BF(14) LK_BF(21) LK_BF(27) LK_BF(31)
+#undef LK_BF
+        default: k_bilateral_fast<5, 10><<<g, 256, 0, s>>>(d, lp.fbf); break;
+    }
 }
 
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s) {

@@ -53,6 +53,9 @@ struct RansacState {  // lives in shared memory
     double best_model[5];
     double best_s;
     double w_s[RS_MAX_WARPS];
+#ifdef LK_GAMMA_PROF
+    long long t_loop;
+#endif
 };
 
 template <int K>
@@ -263,6 +266,10 @@ __device__ __forceinline__ bool lane_fit_sample(const int (&x)[K], const int (&v
 // Least-squares fit of the points idx[0..n) (indices into px/pv). Whole warp:
 // lane e < K*K accumulates a(e/K, e%K), lane K*K+i accumulates b(i), each
 // sequentially in point order. Result in st.fit_model / st.fit_s.
+// The basis values are first tabulated lane-parallel (tbuf rows: 1, phi_1 ..
+// phi_{K-1}, x; (K+1)*n doubles), so each accumulation chain is only loads,
+// an independent product and the dependent add: the reference's per-entry
+// summation order is unchanged.
 template <int K>
 __device__ bool warp_fit(const int* px, const int* pv, const int* idx, int n, double* tbuf,
                          RansacState& st) {
@@ -284,23 +291,32 @@ __device__ bool warp_fit(const int* px, const int* pv, const int* idx, int n, do
     double s = 1.0;  // max(1, max|v|): exact and order independent
     for (int i = lane; i < n; i += 32) s = fmax(s, fabs((double)pv[idx[i]]));
     for (int o = 16; o; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
-    for (int i = lane; i < n; i += 32) tbuf[i] = (double)pv[idx[i]] / s;
-    __syncwarp();
-    double acc = 0.0;
-    if (lane < K * K) {
-        const int ii = lane / K, jj = lane % K;
-        for (int p = 0; p < n; ++p) {
-            const double t = tbuf[p];
-            acc = acc + phi_k<K>(ii, t) * phi_k<K>(jj, t);
-        }
-    } else if (lane < K * K + K) {
-        const int ii = lane - K * K;
-        for (int p = 0; p < n; ++p) {
-            const double t = tbuf[p];
-            acc = acc + (double)px[idx[p]] * phi_k<K>(ii, t);
-        }
+    for (int p = lane; p < n; p += 32) {
+        const int id = idx[p];
+        const double t = (double)pv[id] / s;
+        tbuf[p] = 1.0;
+#pragma unroll
+        for (int i = 1; i < K; ++i) tbuf[i * n + p] = phi_k<K>(i, t);
+        tbuf[K * n + p] = (double)px[id];
     }
-    if (lane < K * K + K) st.ab[lane] = acc;
+    __syncwarp();
+    if (lane < K * K + K) {
+        // a(i, j) = sum phi_i * phi_j; b(i) = sum x * phi_i (vanish.hpp:226-229)
+        const int fa = lane < K * K ? lane / K : K, fb = lane < K * K ? lane % K : lane - K * K;
+        const double* ra = tbuf + fa * n;
+        const double* rb = tbuf + fb * n;
+        double acc = 0.0;
+        int p = 0;
+        for (; p + 8 <= n; p += 8) {
+            double pr[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pr[q] = ra[p + q] * rb[p + q];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc = acc + pr[q];
+        }
+        for (; p < n; ++p) acc = acc + ra[p] * rb[p];
+        st.ab[lane] = acc;
+    }
     __syncwarp();
     if (lane == 0) {
         double A[K][K], b[K];
@@ -340,7 +356,7 @@ __device__ int warp_classify(const int* px, const int* pv, const int* src, int n
 }
 
 // ransac_trim over points 0..n-1 by the first NW warps of the CTA (NW >= 3).
-// bufs: NW + 2 index lists of capacity n; tbuf: n doubles; all shared memory.
+// bufs: NW + 2 index lists of capacity n; tbuf: (K + 1) * n doubles; all shared memory.
 // Every thread of the CTA must call this (it contains __syncthreads).
 template <int K, int NW>
 __device__ void block_ransac(const int* px, const int* pv, int n, double tol, double eps,
@@ -458,6 +474,9 @@ __device__ void block_ransac(const int* px, const int* pv, int n, double tol, do
         }
         __syncthreads();
     }
+#ifdef LK_GAMMA_PROF
+    if (tid == 0) st.t_loop = clock64();
+#endif
     // final model and refits (ransac.hpp:88-118), warp 0
     if (warp == 0) {
         const int iterations = st.iterations_run;

@@ -1008,7 +1008,13 @@ __global__ void __launch_bounds__(512, 2) k_gamma_fit(Dev d) {
         pv[i] = up[2 * i + 1];
     }
     __syncthreads();
+#ifdef LK_GAMMA_PROF
+    const long long t0 = clock64();
+#endif
     block_ransac<5, NW>(px, pv, nrows, d.tr_x, d.eps_x, d.max_iter, d.rng, bufs, tbuf, st);
+#ifdef LK_GAMMA_PROF
+    const long long t1 = clock64();
+#endif
     if (st.msg) {
         if (threadIdx.x == 0) {
             rep.gamma_iterations = st.iterations;
@@ -1057,6 +1063,14 @@ __global__ void __launch_bounds__(512, 2) k_gamma_fit(Dev d) {
         }
         d.e_wg[eb + e] = wg;
     }
+#ifdef LK_GAMMA_PROF
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        rep.gamma_kappa = (double)(st.t_loop - t0);
+        rep.gamma_v_normalizer = (double)(t1 - st.t_loop);
+        rep.gamma_inlier_fraction = (double)(clock64() - t1);
+    }
+#endif
 }
 
 // =====================================================================

@@ -26,6 +26,8 @@ struct WsParam {
 // Approximate bilateral (lk_fastpath.cu): log2-domain spatial terms, range
 // coefficient, and the 8-bit values as floats; passed by value.
 struct FastBfParam {
+    float2 cp[11][5];  // c of taps (2q, 2q+1) of window row dj: packed f32x2 operands
+    float2 sp[11][5];  // the same taps' spatial factors 2^c (range-table taps)
     float c[121];  // -ds * inv_s2 * log2(e) per tap
     float c2;      // -inv_r2 * log2(e)
     float vf[256]; // k / 255
@@ -35,6 +37,7 @@ struct LaunchPlan {
     WsParam ws;
     FastBfParam fbf;
     int fast_front;           // certified fast bilateral + exact refinement (lk_fastpath.cu)
+    int fast_table;           // mask of tap pairs whose range factor comes from the smem table
     int32_t* vhistT;          // [B][D1][H] transposed v-disparity for the v-path DP
     size_t vpath_smem;
     int vpath_choice_smem;    // choices of the v-path DP kept in shared memory

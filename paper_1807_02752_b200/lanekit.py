@@ -47,6 +47,7 @@ def library() -> C.CDLL:
     L.lk_last_error.restype = C.c_char_p
     L.lk_validate_config.argtypes = [cfgp]
     L.lk_launches_per_batch.argtypes = [P]
+    L.lk_timed_frames.argtypes = [P]
     L.lk_device_inputs.argtypes = [P, C.POINTER(P), C.POINTER(P)]
     L.lk_enqueue.argtypes = [P, I]
     L.lk_fetch_reports.argtypes = [P, repp, I]
@@ -172,6 +173,11 @@ class GpuPipeline:
         e = C.c_double(0)
         _check(library().lk_fast_path_error(self._h, C.byref(e)))
         return e.value
+
+    @property
+    def timed_frames(self) -> int:
+        """Frames of the last batch that stage_times() covers (branch 0)."""
+        return library().lk_timed_frames(self._h)
 
     def stage_times(self) -> dict[int, float]:
         ms = (C.c_float * 13)()
