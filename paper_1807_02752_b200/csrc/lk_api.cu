@@ -249,6 +249,11 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     d.min_lane_sep = cfg->min_lane_sep;
     d.paper_sign = cfg->paper_sign ? 1 : 0;
     d.max_iter = kMaxIter;
+    for (int oi = 0; oi < 11; ++oi) {  // offsets {0, -1, 1, -2, 2, ...}: dp.hpp:43-51 scan order
+        const int off = (oi & 1) ? -((oi + 1) >> 1) : (oi >> 1);
+        d.upen[oi] = d.paper_sign ? cfg->lambda_x * off : cfg->lambda_x * std::abs(off);
+        d.upk[oi] = d.upen[oi] < 1e8 && d.upen[oi] > -1e8 ? (int)d.upen[oi] * 16 + oi : 0;
+    }
     {  // both selection paths are exact; the switch only trades a pass for a gather
         const char* e = std::getenv("LK_P99_L2_MIN");
         d.p99_l2_min = e ? (unsigned)std::strtoul(e, nullptr, 10) : 65536u;
@@ -423,7 +428,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         if (lp.fast_front) A(&d.smoothed_f, (size_t)B * d.px);
         A(&d_ft, fast_tab.size());
     }
-    lp.vanish_smem = (size_t)2 * C * 8 + (size_t)C * 4 + (size_t)2 * H * 4 +
+    lp.vanish_smem = (size_t)(2 * C + 32) * 8 + (size_t)2 * C * 4 + (size_t)2 * H * 4 +
                      (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 8 + (size_t)(H + 1) * 4 +
                      (size_t)lkg::K4_VOTE_CAP * 2 + 16;
     // u-path DP shape: 512 threads (2 CTAs / SM) up to 4096 extended columns,

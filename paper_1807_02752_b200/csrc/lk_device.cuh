@@ -45,6 +45,8 @@ struct Dev {
     double lambda_y, tr_y, eps_y, varpi, rho_vote, lambda_x, tr_x, eps_x, sigma_g, lambda_g,
         tr_lpv;
     int chi, nu, varsigma, min_lane_sep, paper_sign, max_iter;
+    double upen[11];  // u-path transition penalty per offset index (vanish.hpp:163-166)
+    int upk[11];      // exact-int path keys: (int)upen * 16 + index
     unsigned int p99_l2_min;  // bucket size above which the p99 uses a 2nd histogram level
     double sobel_s_star;  // smallest s with !(sqrt(s) < threshold): exact sqrt-free test
     // inputs

@@ -743,61 +743,66 @@ __device__ __forceinline__ double piecewise_weight(double te, double tv, double 
 // (energy << 4 | offset index), whose minimum is the smallest energy and,
 // among ties, the earliest offset in list order — the strict-'<' scan of
 // dp.hpp:43-51. Otherwise doubles with the reference's scan verbatim.
+// Offset of list entry oi in {0, -1, 1, -2, 2, ...} (dp.hpp:43-51 scan order).
+__device__ __forceinline__ int upath_off(int oi) { return (oi & 1) ? -((oi + 1) >> 1) : (oi >> 1); }
+
+// One DP stage over the thread's SP consecutive states, operands from a
+// register window prev[s0-5 .. s0+SP+4] (the rows carry 5 sentinel entries
+// on each side, so no bounds tests). INT: exact packed keys
+// (energy << 4 | offset index), whose minimum is the smallest energy and,
+// among ties, the earliest offset in list order — the strict-'<' scan of
+// dp.hpp:43-51; keys are prev * 16 + d.upk[oi] with upk = pen * 16 + oi from
+// the host (constant-bank operands), reduced with 3-input mins. Otherwise
+// doubles with the reference's scan verbatim. ch[s] receives the winning
+// offset INDEX (the backtrack maps it to the offset).
 template <int SP, bool INT>
-__device__ __forceinline__ void upath_stage(const void* prevv, void* curv, const int* cnt,
-                                            int8_t* ch, int C, const double* pen,
-                                            const int* pen_i, double nrv, int nrv_i) {
+__device__ __forceinline__ void upath_stage(const Dev& d, const void* prevv, void* curv,
+                                            const int* cnt, int8_t* ch, int C, double nrv,
+                                            int nrv_i) {
     const int s0 = threadIdx.x * SP;
     if (s0 >= C) return;
     if (INT) {
         const int* prev = (const int*)prevv;
         int* cur = (int*)curv;
-        int wv[SP + 10];
+        int w16[SP + 10];
 #pragma unroll
-        for (int k = 0; k < SP + 10; ++k) {
-            const int idx = s0 - 5 + k;
-            wv[k] = (idx >= 0 && idx < C) ? prev[idx] : (1 << 26);
-        }
+        for (int k = 0; k < SP + 10; ++k) w16[k] = prev[s0 - 5 + k] * 16;
 #pragma unroll
         for (int j = 0; j < SP; ++j) {
             const int s = s0 + j;
             if (s >= C) break;
-            int best = 0x7fffffff;
+            int key[11];
 #pragma unroll
-            for (int oi = 0; oi < 11; ++oi) {
-                const int off = (oi & 1) ? -((oi + 1) >> 1) : (oi >> 1);
-                best = min(best, (wv[j + 5 + off] + pen_i[oi]) * 16 + oi);
-            }
+            for (int oi = 0; oi < 11; ++oi) key[oi] = w16[j + 5 + upath_off(oi)] + d.upk[oi];
+            const int m0 = __vimin3_s32(key[0], key[1], key[2]);
+            const int m1 = __vimin3_s32(key[3], key[4], key[5]);
+            const int m2 = __vimin3_s32(key[6], key[7], key[8]);
+            const int best = __vimin3_s32(__vimin3_s32(m0, m1, m2), key[9], key[10]);
             cur[s] = (best >> 4) + nrv_i * cnt[s];
-            const int oi = best & 15;
-            ch[s] = (int8_t)((oi & 1) ? -((oi + 1) >> 1) : (oi >> 1));
+            ch[s] = (int8_t)(best & 15);
         }
     } else {
         const double* prev = (const double*)prevv;
         double* cur = (double*)curv;
         double wv[SP + 10];
 #pragma unroll
-        for (int k = 0; k < SP + 10; ++k) {
-            const int idx = s0 - 5 + k;
-            wv[k] = (idx >= 0 && idx < C) ? prev[idx] : __longlong_as_double(0x7ff0000000000000LL);
-        }
+        for (int k = 0; k < SP + 10; ++k) wv[k] = prev[s0 - 5 + k];
 #pragma unroll
         for (int j = 0; j < SP; ++j) {
             const int s = s0 + j;
             if (s >= C) break;
             double best = __longlong_as_double(0x7ff0000000000000LL);
-            int bo = 0;
+            int boi = 0;
 #pragma unroll
             for (int oi = 0; oi < 11; ++oi) {
-                const int off = (oi & 1) ? -((oi + 1) >> 1) : (oi >> 1);
-                const double e = wv[j + 5 + off] + pen[oi];
+                const double e = wv[j + 5 + upath_off(oi)] + d.upen[oi];
                 if (e < best) {
                     best = e;
-                    bo = off;
+                    boi = oi;
                 }
             }
             cur[s] = best + nrv * cnt[s];
-            ch[s] = (int8_t)bo;
+            ch[s] = (int8_t)boi;
         }
     }
 }
@@ -811,10 +816,11 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
     lk_frame_report& rep = d.rep[f];
     const int v_top = (int)rep.horizon, v_max = H - 1;
     const int nrows = v_max - v_top + 1;
-    double* prev = sh4;
-    double* cur = prev + C;
-    int* cnt = (int*)(cur + C);
-    int* px = cnt + C;
+    double* prev = sh4 + 8;  // DP rows with 8 pad slots on each side
+    double* cur = prev + C + 16;
+    int* const cnt0 = (int*)(cur + C + 8);  // band counts, double-buffered
+    int* const cnt1 = cnt0 + C;
+    int* px = cnt1 + C;
     int* pv = px + H;
     int8_t* win = (int8_t*)(pv + H);  // [BT_CHUNK][2*BT_SPAN+1]
     int* s_roff = (int*)(win + BT_CHUNK * (2 * BT_SPAN + 1) + 4 - (BT_CHUNK * (2 * BT_SPAN + 1)) % 4);
@@ -822,6 +828,10 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
     __shared__ double sv[32];
     __shared__ int si[32];
     __shared__ int s_votes;
+#ifdef LK_VANISH_PROF
+    const long long t0 = clock64();
+    long long t_band = 0, t_dp = 0;
+#endif
     const int32_t* groff = d.row_off + (size_t)f * (H + 1);
     const int32_t* ecol = d.e_col + (size_t)f * d.px;
     int8_t* choice = d.uchoice + (size_t)f * H * C;
@@ -835,28 +845,12 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
             s_vcol[e] = c == kSkipCol ? (uint16_t)0xffff : (uint16_t)(c - d.ext_lo);
         }
     const int* roff = s_roff;
-    double pen[11];
-    const int offs[11] = {0, -1, 1, -2, 2, -3, 3, -4, 4, -5, 5};
-#pragma unroll
-    for (int o = 0; o < 11; ++o)
-        pen[o] = d.paper_sign ? d.lambda_x * offs[o] : d.lambda_x * abs(offs[o]);
-    int pen_i[11];
-#pragma unroll
-    for (int o = 0; o < 11; ++o) pen_i[o] = (int)pen[o];
-    for (int c = threadIdx.x; c < C; c += blockDim.x) cnt[c] = 0;
+    for (int c = threadIdx.x; c < 2 * C; c += blockDim.x) cnt0[c] = 0;
     if (threadIdx.x == 0) s_votes = 0;
     __syncthreads();
-    const double nrv = -d.rho_vote;
-    // exact int32 path: integral lambda_x / rho_vote and |energies| < 2^25
-    const double lx = d.lambda_x, rv = d.rho_vote;
-    const bool use_int = SP > 0 && lx == floor(lx) && rv == floor(rv) && lx < 1e6 && rv < 1e6 &&
-                         (double)nrows * (rv * (double)d.aux[f].votes + 5.0 * lx) < 33554432.0;
-    const int nrv_i = use_int ? -(int)rv : 0;
-    int top_cur = v_max + 1, bot_cur = v_max;
-    int my_votes = 0;
-    for (int stg = 0; stg < nrows; ++stg) {
+    // vote_band (vanish.hpp:101-105) of stage stg: rows [bt, bb]
+    auto band = [&](int stg, int& bt, int& bb) {
         const int v = v_max - stg;
-        int bt, bb;  // vote_band (vanish.hpp:101-105)
         if (v > v_max - d.chi - 1) {
             bt = v;
             bb = v_max;
@@ -867,26 +861,58 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
             bt = v_top;
             bb = v + d.chi;
         }
-        if (bt < top_cur) {  // rows entering at the top: [bt, top_cur)
-            for (int e = roff[bt] + threadIdx.x; e < roff[top_cur]; e += blockDim.x) {
+    };
+    // moves counts cn from band [t0, b0] to band [t1, b1] (both slide upwards):
+    // rows [t1, t0) enter, rows (b1, b0] leave; exact integer +-1 updates
+    auto slide = [&](int* cn, int t0, int b0, int t1, int b1) {
+        if (t1 < t0)
+            for (int e = roff[t1] + threadIdx.x; e < roff[t0]; e += blockDim.x) {
                 const int c = staged ? (int)s_vcol[e - e_first]
                                      : (ecol[e] == kSkipCol ? 0xffff : ecol[e] - d.ext_lo);
-                if (c != 0xffff) {
-                    atomicAdd(&cnt[c], 1);
-                    ++my_votes;
-                }
+                if (c != 0xffff) atomicAdd(&cn[c], 1);
             }
-        }
-        top_cur = bt;
-        if (bb < bot_cur) {  // rows leaving at the bottom: (bb, bot_cur]
-            for (int e = roff[bb + 1] + threadIdx.x; e < roff[bot_cur + 1]; e += blockDim.x) {
+        if (b1 < b0)
+            for (int e = roff[b1 + 1] + threadIdx.x; e < roff[b0 + 1]; e += blockDim.x) {
                 const int c = staged ? (int)s_vcol[e - e_first]
                                      : (ecol[e] == kSkipCol ? 0xffff : ecol[e] - d.ext_lo);
-                if (c != 0xffff) atomicSub(&cnt[c], 1);
+                if (c != 0xffff) atomicSub(&cn[c], 1);
             }
+    };
+    const double nrv = -d.rho_vote;
+    // exact int32 path: integral lambda_x / rho_vote and |energies| < 2^25
+    const double lx = d.lambda_x, rv = d.rho_vote;
+    const bool use_int = SP > 0 && lx == floor(lx) && rv == floor(rv) && lx < 1e6 && rv < 1e6 &&
+                         (double)nrows * (rv * (double)d.aux[f].votes + 5.0 * lx) < 33554432.0;
+    const int nrv_i = use_int ? -(int)rv : 0;
+    if (threadIdx.x < 10) {  // sentinels: states outside [0, C) never win
+        const int k = threadIdx.x < 5 ? (int)threadIdx.x - 5 : C + (int)threadIdx.x - 5;
+        if (use_int) {
+            ((int*)prev)[k] = 1 << 26;
+            ((int*)cur)[k] = 1 << 26;
+        } else {
+            prev[k] = __longlong_as_double(0x7ff0000000000000LL);
+            cur[k] = __longlong_as_double(0x7ff0000000000000LL);
         }
-        bot_cur = bb;
-        __syncthreads();
+    }
+    int my_votes = 0;  // every row of [v_top, v_max] enters the band exactly once
+    for (int e = groff[v_top] + threadIdx.x; e < groff[H]; e += blockDim.x)
+        my_votes += (staged ? s_vcol[e - e_first] != 0xffff : ecol[e] != kSkipCol);
+    // Invariant at stage stg: cnt{stg & 1} holds band(stg) (read by the DP),
+    // the other buffer holds band(stg - 1) and is slid to band(stg + 1) during
+    // the same phase, so one barrier per stage covers both.
+    int tm1 = v_max + 1, bm1 = v_max, t0b, b0b;  // band(stg - 1) (empty before 0), band(stg)
+    band(0, t0b, b0b);
+    slide(cnt0, tm1, bm1, t0b, b0b);
+    __syncthreads();
+#ifdef LK_VANISH_PROF
+    const long long t1 = clock64();
+#endif
+    for (int stg = 0; stg < nrows; ++stg) {
+#ifdef LK_VANISH_PROF
+        const long long tb = clock64();
+#endif
+        const int v = v_max - stg;
+        const int* cnt = (stg & 1) ? cnt1 : cnt0;
         if (d.hooks) {
             double* arow = d.acc + ((size_t)f * H + (v - v_top)) * C;
             for (int c = threadIdx.x; c < C; c += blockDim.x) arow[c] = nrv * cnt[c];
@@ -899,29 +925,41 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
         } else if (SP > 0) {
             int8_t* ch = choice + (size_t)stg * C;
             if (use_int)
-                upath_stage<(SP > 0 ? SP : 1), true>(prev, cur, cnt, ch, C, pen, pen_i, nrv, nrv_i);
+                upath_stage<(SP > 0 ? SP : 1), true>(d, prev, cur, cnt, ch, C, nrv, nrv_i);
             else
-                upath_stage<(SP > 0 ? SP : 1), false>(prev, cur, cnt, ch, C, pen, pen_i, nrv, nrv_i);
+                upath_stage<(SP > 0 ? SP : 1), false>(d, prev, cur, cnt, ch, C, nrv, nrv_i);
         } else {
             int8_t* ch = choice + (size_t)stg * C;
             for (int s = threadIdx.x; s < C; s += blockDim.x) {
                 double best = __longlong_as_double(0x7ff0000000000000LL);
-                int bo = 0;
+                int boi = 0;
 #pragma unroll
                 for (int o = 0; o < 11; ++o) {
-                    const int ps = s + offs[o];
+                    const int ps = s + upath_off(o);
                     if (ps < 0 || ps >= C) continue;
-                    const double e = prev[ps] + pen[o];
+                    const double e = prev[ps] + d.upen[o];
                     if (e < best) {
                         best = e;
-                        bo = offs[o];
+                        boi = o;
                     }
                 }
                 cur[s] = best + nrv * cnt[s];
-                ch[s] = (int8_t)bo;
+                ch[s] = (int8_t)boi;
             }
         }
+        if (stg + 1 < nrows) {  // other buffer: band(stg - 1) -> band(stg + 1)
+            int t1b, b1b;
+            band(stg + 1, t1b, b1b);
+            slide((stg & 1) ? cnt0 : cnt1, tm1, bm1, t1b, b1b);
+            tm1 = t0b;
+            bm1 = b0b;
+            t0b = t1b;
+            b0b = b1b;
+        }
         __syncthreads();
+#ifdef LK_VANISH_PROF
+        t_dp += clock64() - tb;
+#endif
         if (stg > 0) {
             double* t = prev;
             prev = cur;
@@ -939,6 +977,9 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
             mi = s;
         }
     }
+#ifdef LK_VANISH_PROF
+    const long long t2 = clock64();
+#endif
     const int term = block_argmin(mv, mi, sv, si);
     const double energy = use_int ? (double)((const int*)prev)[term] : prev[term];
     // backtrack (dp.hpp:67-71) in windows of BT_CHUNK stages staged in smem
@@ -952,14 +993,26 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
         const int lo = max(1, hi - BT_CHUNK + 1);  // stages lo..hi are read
         const int c0 = p - BT_SPAN;
         __syncthreads();
-        for (int i = threadIdx.x; i < (hi - lo + 1) * span; i += blockDim.x) {
-            const int r = i / span, c = c0 + (i - r * span);
-            win[i] = (c >= 0 && c < C) ? choice[(size_t)(lo + r) * C + c] : 0;
+        {  // U independent loads in flight per thread before the stores
+            constexpr int U = 8;
+            const int total = (hi - lo + 1) * span;
+            for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
+                int8_t w[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    const int r = i / span, c = c0 + (i - r * span);
+                    w[u] = (i < total && c >= 0 && c < C) ? choice[(size_t)(lo + r) * C + c] : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (i0 + u * blockDim.x < total) win[i0 + u * blockDim.x] = w[u];
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             for (int stg = hi; stg >= lo; --stg) {
-                p += win[(stg - lo) * span + (p - c0)];
+                p += upath_off(win[(stg - lo) * span + (p - c0)]);
                 px[stg - 1] = d.ext_lo + p;
                 pv[stg - 1] = v_max - (stg - 1);
             }
@@ -976,6 +1029,13 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
     }
     if (threadIdx.x == 0) {
         rep.upath_energy = energy;
+#ifdef LK_VANISH_PROF
+        rep.gamma_kappa = (double)(t1 - t0);
+        rep.gamma_v_normalizer = (double)t_band;
+        rep.gamma_inlier_fraction = (double)t_dp;
+        rep.gamma[0] = (double)(t2 - t1);
+        rep.gamma[1] = (double)(clock64() - t2);
+#endif
         rep.upath_has_evidence = s_votes > 0;
         if (s_votes == 0) fail_frame(d, f, 11, LK_MSG_NO_EDGE_EVIDENCE);  // pipeline.hpp:238-239
     }
@@ -1035,11 +1095,15 @@ __global__ void __launch_bounds__(512, 2) k_gamma_fit(Dev d) {
         d.gamma_inl[((size_t)f * H + i) * 2 + 1] = pv[id];
     }
     if (threadIdx.x == 0) {
+#ifndef LK_VANISH_PROF
         for (int k = 0; k < 5; ++k) rep.gamma[k] = st.model[k];
         rep.gamma_kappa = 1.0;
         rep.gamma_v_normalizer = st.s;
+#endif
         rep.gamma_iterations = st.iterations;
+#ifndef LK_VANISH_PROF
         rep.gamma_inlier_fraction = st.fraction;
+#endif
         rep.gamma_degraded = st.degraded;
         rep.gamma_inlier_count = st.n_inl;
     }
