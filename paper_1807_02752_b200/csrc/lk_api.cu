@@ -886,6 +886,8 @@ extern "C" lk_status lk_fast_path_error(lk_ctx* c, double* max_abs_error) {
     CU(cudaMalloc(&scratch, sizeof(double)));
     cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(double), c->stream);
     if (e == cudaSuccess) {
+        // the pipeline computes s~ only near the road mask: recompute every tile
+        lkg::launch_fast_bilateral(c->d, c->lp, c->last_n, c->stream, 1);
         lkg::launch_exact_bilateral(c->d, c->lp, c->last_n, c->stream);  // every pixel, exact
         e = lkg::fast_error(c->d, c->last_n, c->stream, scratch);
     }

@@ -46,8 +46,14 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // 1.5*2^23 rounds it into the low mantissa bits (no integer keys staged).
 // w = S_t * R[dr] rounds three times in FP32 (~2e-7 relative), inside the
 // ex2.approx error the bound in DESIGN.md already budgets.
+//
+// all = 0 (the pipeline): s~ is consumed only by the Sobel of road-mask pixels
+// (k_sobel_refine), i.e. within one pixel of a masked pixel (mirroring at the
+// border stays within that pixel). Tiles whose one-pixel ring holds no masked
+// pixel are skipped; the test is the exact mask of k_sobel_refine
+// (road_mask, preprocess.hpp:14-25). all = 1 computes every tile (lk_fast_path_error).
 template <int RHO, int TB>
-__global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p) {
+__global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p, int all) {
     constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
     constexpr int NPX = TWh * THh;
     static_assert(WIN == 11, "packed tap pairs assume an 11-wide window");
@@ -56,6 +62,22 @@ __global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p)
     const int f = blockIdx.z;
     if (frame_failed(d, f)) return;
     const int u0 = blockIdx.x * BT_W, v0 = blockIdx.y * BT_H;
+    if (!all) {
+        const int horizon = (int)d.rep[f].horizon;
+        if (v0 + BT_H < horizon) return;  // ring rows all above the horizon
+        const uint8_t* dp = d.disp + (size_t)f * d.px;
+        const double* fv = d.fv + (size_t)f * d.H;
+        int any = 0;
+        for (int i = threadIdx.x; i < (BT_H + 2) * (BT_W + 2) && !any; i += blockDim.x) {
+            const int r = i / (BT_W + 2), c = i - r * (BT_W + 2);
+            const int v = v0 - 1 + r, u = u0 - 1 + c;
+            if (v >= horizon && v >= 0 && v < d.H && u >= 0 && u < d.W) {
+                const int dv = dp[(size_t)v * d.W + u];
+                any = dv != 0 && fabs((double)dv - fv[v]) <= d.varpi;
+            }
+        }
+        if (!__syncthreads_or(any)) return;
+    }
     const uint8_t* g = d.grey + (size_t)f * d.px;
     s_vf[threadIdx.x] = __ldg(d.fast_tab + threadIdx.x);
     if (TB) {
@@ -301,14 +323,14 @@ __global__ void __launch_bounds__(256) k_sobel_refine(Dev d, WsParam ws) {
     }
 }
 
-void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s) {
+void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all) {
     const dim3 g((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n);
     switch (lp.fast_table) {
 #define LK_BF(M) \
-    case M: k_bilateral_fast<5, M><<<g, 256, 0, s>>>(d, lp.fbf); break;
+    case M: k_bilateral_fast<5, M><<<g, 256, 0, s>>>(d, lp.fbf, all); break;
         LK_BF(0) LK_BF(2) LK_BF(10) LK_BF(14) LK_BF(21) LK_BF(27) LK_BF(31)
 #undef LK_BF
-        default: k_bilateral_fast<5, 10><<<g, 256, 0, s>>>(d, lp.fbf); break;
+        default: k_bilateral_fast<5, 10><<<g, 256, 0, s>>>(d, lp.fbf, all); break;
     }
 }
 

@@ -61,7 +61,7 @@ struct LaunchPlan {
 cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s,
                             cudaEvent_t* stage_ev);
 cudaError_t configure_kernels(const LaunchPlan& lp);
-void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
+void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all = 0);
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
 void launch_exact_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
 cudaError_t fast_error(const Dev& d, int n, cudaStream_t s, double* out_dev);
