@@ -301,6 +301,9 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
             std::memcpy(&d.sobel_s_star, &hi, 8);
         }
     }
+    d.sobel_s_star_lo = (float)d.sobel_s_star;
+    if ((double)d.sobel_s_star_lo > d.sobel_s_star)
+        d.sobel_s_star_lo = std::nextafter(d.sobel_s_star_lo, -std::numeric_limits<float>::infinity());
     std::vector<uint64_t> rng((size_t)kMaxIter * 5);
     {
         std::mt19937_64 eng(cfg->rng_seed);  // ransac.hpp:44

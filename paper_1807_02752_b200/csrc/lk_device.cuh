@@ -49,6 +49,7 @@ struct Dev {
     int upk[11];      // exact-int path keys: (int)upen * 16 + index
     unsigned int p99_l2_min;  // bucket size above which the p99 uses a 2nd histogram level
     double sobel_s_star;  // smallest s with !(sqrt(s) < threshold): exact sqrt-free test
+    float sobel_s_star_lo;  // largest float <= sobel_s_star (FP32 candidate screen)
     // inputs
     const uint8_t* grey;
     const uint8_t* disp;

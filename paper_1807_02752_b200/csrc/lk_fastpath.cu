@@ -154,40 +154,74 @@ __global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p,
 }
 
 // Exact bilateral at in-image pixel (u, v) from the staged mirrored grey tile
-// (origin gx0, gy0): the arithmetic of k_bilateral_tile / preprocess.hpp:38-56.
+// (origin gx0, gy0): the arithmetic of k_bilateral_tile / preprocess.hpp:38-56,
+// same j-major / i-minor accumulation. The weight-table gathers of row j+1
+// are issued before row j is accumulated (two-row software pipeline), so the
+// L1/L2 latency overlaps the dependent add chain; k/255 comes from smem.
 template <int RHO>
 __device__ __forceinline__ double exact_bilateral(const Dev& d, const WsParam& ws,
-                                                  const uint8_t* s_g, int gw, int gx0, int gy0,
-                                                  int u, int v) {
+                                                  const uint8_t* s_g, const double* s_val,
+                                                  int gw, int gx0, int gy0, int u, int v) {
     constexpr int WIN = 2 * RHO + 1;
     const uint8_t* c = s_g + (v - gy0) * gw + (u - gx0);
     const double* wrow = d.wr + (int)c[0] * 256;
     double num = 0.0, den = 0.0;
+    double wr_cur[WIN];
+    {
+        const uint8_t* row = c - RHO * gw - RHO;
+#pragma unroll
+        for (int i = 0; i < WIN; ++i) wr_cur[i] = __ldg(wrow + row[i]);
+    }
 #pragma unroll 1
     for (int j = 0; j < WIN; ++j) {
+        double wr_nxt[WIN];
+        if (j + 1 < WIN) {
+            const uint8_t* row = c + (j + 1 - RHO) * gw - RHO;
+#pragma unroll
+            for (int i = 0; i < WIN; ++i) wr_nxt[i] = __ldg(wrow + row[i]);
+        }
         const uint8_t* row = c + (j - RHO) * gw - RHO;
 #pragma unroll
         for (int i = 0; i < WIN; ++i) {
-            const int kv = row[i];
-            const double w = ws.w[j * WIN + i] * __ldg(wrow + kv);
-            num += w * __ldg(d.val + kv);
+            const double w = ws.w[j * WIN + i] * wr_cur[i];
+            num += w * s_val[row[i]];
             den += w;
         }
+#pragma unroll
+        for (int i = 0; i < WIN; ++i) wr_cur[i] = wr_nxt[i];
     }
     return num / den;
 }
 
 // ---- 2. Sobel on s~ with the propagated bound, exact refinement, edge bits
+//
+// Tile SB_TW x SB_TH, 256 threads; thread t owns pixels (row (t>>7) + 2k,
+// col t & 127), k < 4, so each warp covers 32 consecutive pixels of a row
+// and its ballot is a candidate / edge word directly.
+//
+// Candidate screening runs in FP32 on s~ (values in [0, 1]). Its rounding
+// error is folded into the certified bound: each FP32 Sobel component is
+// within 11 * 2^-24 < 1e-6 of the exact-arithmetic Sobel of s~, which is
+// within 8 * kEpsSmooth of the Sobel of the exact smoothed image; the
+// reference's FP64 evaluation of that Sobel adds < 1e-15. With D = 8 eps +
+// 1e-6, |s - s_f| <= D(2|gx_f| + D) + D(2|gy_f| + D) + 3 * 2^-24 * s_f, where
+// s_f = fl32(gx_f^2 + gy_f^2). ds below over-covers this (x1.001, +4e-7 s_f,
+// +1e-9) and the test uses s*_lo = the largest float <= s*, so every pixel
+// with s >= s* is a candidate.
 template <int RHO>
-__global__ void __launch_bounds__(256) k_sobel_refine(Dev d, WsParam ws) {
-    constexpr int FW = SB_TW + 4, FH = SB_TH + 4;              // s~ tile, 2-px halo
-    constexpr int NW = SB_TW + 2, NH = SB_TH + 2;              // tile + 1-px ring
+__global__ void __launch_bounds__(256, 3) k_sobel_refine(Dev d, WsParam ws) {
+    constexpr int FW = SB_TW + 2, FH = SB_TH + 2;               // tile + 1-px ring
     constexpr int GW = SB_TW + 2 + 2 * RHO, GH = SB_TH + 2 + 2 * RHO;  // grey for the ring
+    constexpr int NWORD = (FW + 31) / 32;                       // ring row bitmap words
+    constexpr int TWORD = SB_TW / 32;                           // tile row bitmap words
+    constexpr int NF = (FH * FW + 255) / 256, NG = (GH * GW + 255) / 256;
+    static_assert(SB_TW == 128 && SB_TH == 8, "pixel ownership assumes a 128 x 8 tile");
     __shared__ float s_f[FH * FW];
     __shared__ uint8_t s_g[GH * GW];
-    __shared__ uint8_t s_cand[SB_TH * SB_TW];
-    __shared__ double s_ex[NH * NW];
-    __shared__ short s_need[NH * NW];
+    __shared__ double s_ex[FH * FW];
+    __shared__ double s_val[256];
+    __shared__ short s_need[FH * FW];
+    __shared__ unsigned s_cw[SB_TH][TWORD];
     __shared__ int s_nneed, s_seg[SB_TH], s_tot[2];
     const int f = blockIdx.z;
     if (frame_failed(d, f)) return;
@@ -196,104 +230,141 @@ __global__ void __launch_bounds__(256) k_sobel_refine(Dev d, WsParam ws) {
             fail_frame(d, f, 10, LK_MSG_SOBEL_TOO_SMALL);
         return;
     }
-    const int W = d.W, H = d.H;
+    const int W = d.W, H = d.H, tid = threadIdx.x, lane = tid & 31;
     const int u0 = blockIdx.x * SB_TW, v0 = blockIdx.y * SB_TH;
     const int horizon = (int)d.rep[f].horizon;
     if (v0 + SB_TH <= horizon) {  // the mask is empty above the horizon
-        if (threadIdx.x < SB_TH && v0 + threadIdx.x < H)
-            d.seg_cnt[((size_t)f * H + v0 + threadIdx.x) * d.n_seg + blockIdx.x] = 0;
+        if (tid < SB_TH && v0 + tid < H)
+            d.seg_cnt[((size_t)f * H + v0 + tid) * d.n_seg + blockIdx.x] = 0;
         return;
     }
     const float* sf = d.smoothed_f + (size_t)f * d.px;
     const uint8_t* grey = d.grey + (size_t)f * d.px;
-    // mirrored row offsets / columns of the grey halo (the s~ halo is its inner part)
-    __shared__ int s_rowg[GH], s_colg[GW];
-    for (int i = threadIdx.x; i < GH; i += blockDim.x) s_rowg[i] = mirror(v0 - 1 - RHO + i, H) * W;
-    for (int i = threadIdx.x; i < GW; i += blockDim.x) s_colg[i] = mirror(u0 - 1 - RHO + i, W);
-    __syncthreads();
-    for (int i = threadIdx.x; i < FH * FW; i += blockDim.x) {
-        const int r = i / FW, c = i - r * FW;  // s~ row v0-2+r = grey row index r + RHO - 1
-        s_f[i] = sf[(size_t)s_rowg[r + RHO - 1] + s_colg[c + RHO - 1]];
+    const int pc = tid & (SB_TW - 1), pr0 = tid >> 7;  // owned pixels: (pr0 + 2k, pc)
+    // independent loads first: disparity and profile of the owned pixels, s~ tile
+    int dv[4];
+    double fvv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int v = v0 + pr0 + 2 * k, u = u0 + pc;
+        const bool in = v < H && u < W;
+        dv[k] = in ? d.disp[(size_t)f * d.px + (size_t)v * W + u] : 0;
+        fvv[k] = in ? d.fv[(size_t)f * H + v] : 0.0;
     }
-    if (threadIdx.x < SB_TH) s_seg[threadIdx.x] = 0;
-    if (threadIdx.x < 2) s_tot[threadIdx.x] = 0;
-    if (threadIdx.x == 0) s_nneed = 0;
-    __syncthreads();
-    const double dg = 8.0 * kEpsSmooth;  // |gx~ - gx|, |gy~ - gy| bound (sum of |Sobel taps| = 8)
-    int n_mask = 0, any_cand = 0;
-    for (int i = threadIdx.x; i < SB_TH * SB_TW; i += blockDim.x) {
-        const int r = i / SB_TW, c = i - r * SB_TW;
-        const int v = v0 + r, u = u0 + c;
-        uint8_t cand = 0;
-        if (v < H && u < W) {
-            const int dv = d.disp[(size_t)f * d.px + (size_t)v * W + u];
-            const bool m = v >= horizon && dv != 0 &&
-                           fabs((double)dv - d.fv[(size_t)f * H + v]) <= d.varpi;
-            n_mask += m;
-            if (m) {
-                const float* a = s_f + (r + 1) * FW + (c + 1);  // row v-1, col u-1
-                const float* b = a + FW;
-                const float* cc = b + FW;
-                const double gx = ((double)a[2] - a[0]) + 2 * ((double)b[2] - b[0]) +
-                                  ((double)cc[2] - cc[0]);
-                const double gy = ((double)cc[0] - a[0]) + 2 * ((double)cc[1] - a[1]) +
-                                  ((double)cc[2] - a[2]);
-                const double s = gx * gx + gy * gy;
-                const double ds = dg * (2 * fabs(gx) + dg) + dg * (2 * fabs(gy) + dg) + 1e-14;
-                cand = s + ds >= d.sobel_s_star;
+    {
+        float t[NF];
+#pragma unroll
+        for (int q = 0; q < NF; ++q) {
+            const int i = tid + q * 256;
+            t[q] = 0.f;
+            if (i < FH * FW) {
+                const int r = i / FW, c = i - r * FW;
+                t[q] = sf[(size_t)mirror(v0 - 1 + r, H) * W + mirror(u0 - 1 + c, W)];
             }
         }
-        s_cand[i] = cand;
+#pragma unroll
+        for (int q = 0; q < NF; ++q)
+            if (tid + q * 256 < FH * FW) s_f[tid + q * 256] = t[q];
+    }
+    if (tid < SB_TH) s_seg[tid] = 0;
+    if (tid < 2) s_tot[tid] = 0;
+    if (tid == 0) s_nneed = 0;
+    __syncthreads();
+    const float D = (float)(8.0 * kEpsSmooth + 1e-6);
+    int n_mask = 0, any_cand = 0;
+    unsigned cand_bits = 0;  // bit k: owned pixel k is a candidate
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int r = pr0 + 2 * k, v = v0 + r, u = u0 + pc;
+        const bool m = v < H && u < W && v >= horizon && dv[k] != 0 &&
+                       fabs((double)dv[k] - fvv[k]) <= d.varpi;  // road_mask, preprocess.hpp:14-25
+        n_mask += m;
+        bool cand = false;
+        if (m) {
+            const float* a = s_f + r * FW + pc;  // row v-1, col u-1
+            const float* b = a + FW;
+            const float* cc = b + FW;
+            const float gx = ((a[2] - a[0]) + 2.f * (b[2] - b[0])) + (cc[2] - cc[0]);
+            const float gy = ((cc[0] - a[0]) + 2.f * (cc[1] - a[1])) + (cc[2] - a[2]);
+            const float s = gx * gx + gy * gy;
+            const float ds = 1.001f * (D * (2.f * fabsf(gx) + D) + D * (2.f * fabsf(gy) + D)) +
+                             4e-7f * s + 1e-9f;
+            cand = s + ds >= d.sobel_s_star_lo;
+        }
+        cand_bits |= (unsigned)cand << k;
+        const unsigned bal = __ballot_sync(0xffffffffu, cand);
+        if (lane == 0) s_cw[r][pc >> 5] = bal;
         any_cand |= cand;
     }
     if (!__syncthreads_or(any_cand)) {  // no edge can exist in this tile (most tiles)
         for (int o = 16; o; o >>= 1) n_mask += __shfl_xor_sync(0xffffffffu, n_mask, o);
-        if ((threadIdx.x & 31) == 0 && n_mask)
-            atomicAdd(&d.aux[f].mask_px, (unsigned long long)n_mask);
-        if (threadIdx.x < SB_TH && v0 + threadIdx.x < H)
-            d.seg_cnt[((size_t)f * H + v0 + threadIdx.x) * d.n_seg + blockIdx.x] = 0;
+        if (lane == 0 && n_mask) atomicAdd(&d.aux[f].mask_px, (unsigned long long)n_mask);
+        if (tid < SB_TH && v0 + tid < H)
+            d.seg_cnt[((size_t)f * H + v0 + tid) * d.n_seg + blockIdx.x] = 0;
         return;
     }
-    for (int i = threadIdx.x; i < GH * GW; i += blockDim.x) {
-        const int r = i / GW, c = i - r * GW;
-        s_g[i] = grey[(size_t)s_rowg[r] + s_colg[c]];
+    {  // grey for the exact bilateral of the ring (loads first), k/255 table
+        uint8_t t[NG];
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+            const int i = tid + q * 256;
+            t[q] = 0;
+            if (i < GH * GW) {
+                const int r = i / GW, c = i - r * GW;
+                t[q] = grey[(size_t)mirror(v0 - 1 - RHO + r, H) * W + mirror(u0 - 1 - RHO + c, W)];
+            }
+        }
+        s_val[tid] = __ldg(d.val + tid);
+#pragma unroll
+        for (int q = 0; q < NG; ++q)
+            if (tid + q * 256 < GH * GW) s_g[tid + q * 256] = t[q];
     }
-    // pixels of tile + ring inside a candidate's 3x3 need the exact bilateral
-    for (int i = threadIdx.x; i < NH * NW; i += blockDim.x) {
-        const int r = i / NW, c = i - r * NW;  // ring coords: tile pixel (r-1, c-1)
-        bool need = false;
-        for (int y = r - 2; y <= r && !need; ++y)
-            for (int x = c - 2; x <= c; ++x)
-                if (y >= 0 && y < SB_TH && x >= 0 && x < SB_TW && s_cand[y * SB_TW + x]) {
-                    need = true;
-                    break;
-                }
-        if (need) s_need[atomicAdd(&s_nneed, 1)] = (short)i;
+    // pixels of tile + ring inside a candidate's 3x3 need the exact value:
+    // ring bit C of ring row R <-> tile (R - 1, C - 1); need = 3x3 dilation
+    if (tid < FH * NWORD) {
+        const int R = tid / NWORD, w = tid - R * NWORD;
+        auto tw = [&](int k) -> unsigned {  // OR of tile rows R-2..R, word k
+            unsigned x = 0;
+            if (k >= 0 && k < TWORD)
+#pragma unroll
+                for (int y = R - 2; y <= R; ++y)
+                    if (y >= 0 && y < SB_TH) x |= s_cw[y][k];
+            return x;
+        };
+        const unsigned t0 = tw(w), t1 = tw(w - 1);
+        // (T | T << 1 | T << 2) restricted to ring bits 32w .. 32w + 31
+        unsigned need = t0 | __funnelshift_l(t1, t0, 1) | __funnelshift_l(t1, t0, 2);
+        if (w == NWORD - 1) need &= (FW % 32) ? (1u << (FW % 32)) - 1u : 0xffffffffu;
+        if (need) {
+            int o = atomicAdd(&s_nneed, __popc(need));
+            while (need) {
+                const int bit = __ffs(need) - 1;
+                need &= need - 1;
+                s_need[o++] = (short)(R * FW + 32 * w + bit);
+            }
+        }
     }
     __syncthreads();
     const int gx0 = u0 - 1 - RHO, gy0 = v0 - 1 - RHO;
-    for (int k = threadIdx.x; k < s_nneed; k += blockDim.x) {
+    for (int k = tid; k < s_nneed; k += blockDim.x) {
         const int i = s_need[k];
-        const int r = i / NW, c = i - r * NW;
+        const int r = i / FW, c = i - r * FW;
         // ring positions outside the image hold their mirror pixel (preprocess.hpp:71-72)
         const int v = mirror(v0 - 1 + r, H), u = mirror(u0 - 1 + c, W);
-        const double e = exact_bilateral<RHO>(d, ws, s_g, GW, gx0, gy0, u, v);
+        const double e = exact_bilateral<RHO>(d, ws, s_g, s_val, GW, gx0, gy0, u, v);
         s_ex[i] = e;
         d.smoothed[(size_t)f * d.px + (size_t)v * W + u] = e;  // read back by k_edge_emit
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31;
     int n_edge = 0;
 #pragma unroll
-    for (int k = 0; k < SB_TW * SB_TH / 256; ++k) {
-        const int i = threadIdx.x + k * 256;
-        const int r = i / SB_TW, c = i % SB_TW;
-        const int v = v0 + r;
+    for (int k = 0; k < 4; ++k) {
+        const int r = pr0 + 2 * k, v = v0 + r;
         bool edge = false;
-        if (s_cand[i]) {  // candidate => masked and in the image
-            const double* a = s_ex + r * NW + c;  // row v-1, col u-1
-            const double* b = a + NW;
-            const double* cc = b + NW;
+        if ((cand_bits >> k) & 1) {  // candidate => masked and in the image
+            const double* a = s_ex + r * FW + pc;  // row v-1, col u-1
+            const double* b = a + FW;
+            const double* cc = b + FW;
             const double gx = (a[2] - a[0]) + 2 * (b[2] - b[0]) + (cc[2] - cc[0]);
             const double gy = (cc[0] - a[0]) + 2 * (cc[1] - a[1]) + (cc[2] - a[2]);
             edge = gx * gx + gy * gy >= d.sobel_s_star;
@@ -301,7 +372,7 @@ __global__ void __launch_bounds__(256) k_sobel_refine(Dev d, WsParam ws) {
         }
         const unsigned bal = __ballot_sync(0xffffffffu, edge);
         if (lane == 0 && v < H) {
-            const int word = (u0 + c) >> 5;
+            const int word = (u0 + pc) >> 5;
             if (word < d.words_per_row) d.ebits[((size_t)f * H + v) * d.words_per_row + word] = bal;
             if (bal) atomicAdd(&s_seg[r], __popc(bal));
         }

@@ -31,18 +31,34 @@ __global__ void __launch_bounds__(256) k_vdisparity(Dev d, int32_t* vhistT) {
     const uint8_t* disp = d.disp + (size_t)f * d.px + (size_t)v0 * d.W;
     const int npx = rows * d.W;
     unsigned long long valid = 0, counted = 0;
+    // (row, col) of pixel base + tid, advanced incrementally (no division)
+    int row = threadIdx.x / d.W, col = threadIdx.x - row * d.W;
     for (int base = 0; base < npx; base += blockDim.x) {
         const int i = base + threadIdx.x;
         int key = -1;
         if (i < npx) {
             const int dv = disp[i];
             valid += dv != 0;
-            if (dv >= 1 && dv <= d.d_max) key = (i / d.W) * D1 + dv;
+            if (dv >= 1 && dv <= d.d_max) key = row * D1 + dv;
+        }
+        col += blockDim.x;
+        while (col >= d.W) {
+            col -= d.W;
+            ++row;
         }
         const unsigned active = __ballot_sync(0xffffffffu, key >= 0);
+        if (!active) continue;
+        // a road row has one disparity almost everywhere: one atomic per warp
+        // when every active lane holds the same key, else per distinct key
+        const int kmin = __reduce_min_sync(0xffffffffu, key >= 0 ? key : 0x7fffffff);
+        const int kmax = __reduce_max_sync(0xffffffffu, key);
         if (key >= 0) {
-            const unsigned grp = __match_any_sync(active, key);
-            if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&sh_hist[key], __popc(grp));
+            if (kmin == kmax) {
+                if ((threadIdx.x & 31) == __ffs(active) - 1) atomicAdd(&sh_hist[key], __popc(active));
+            } else {
+                const unsigned grp = __match_any_sync(active, key);
+                if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&sh_hist[key], __popc(grp));
+            }
             counted += 1;
         }
     }
@@ -1468,23 +1484,44 @@ __global__ void __launch_bounds__(256) k_p99_select(Dev d) {
 // m1 sum run together from the bottom row upward.
 // =====================================================================
 __global__ void __launch_bounds__(128) k_energy(Dev d) {
+    extern __shared__ double sh_e[];  // per row v: vpx[v+1], vpy[v+1], denom, 1/denom
     const int f = blockIdx.y;
     if (frame_failed(d, f)) return;
-    const int ci = blockIdx.x * blockDim.x + threadIdx.x;
-    if (ci >= d.ext_cols) return;
     const int W = d.W, H = d.H;
     const int v_top = (int)d.rep[f].horizon, v_max = H - 1;
     const double* vpx = d.vpx + (size_t)f * H;
     const double* vpy = d.vpy + (size_t)f * H;
+    double* s_px = sh_e;
+    double* s_py = s_px + H;
+    double* s_den = s_py + H;
+    double* s_rcp = s_den + H;
+    // Every column divides by the same denom at row v, so 1/denom is
+    // computed once per row; each quotient is then q0 = RN(a y), r = a - q0 b
+    // (exact, FMA), q = RN(q0 + r y), which is the correctly rounded a / b
+    // (Markstein; checked against IEEE division on 3e10 cases by
+    // tools/markstein_check.cu). Zero, non-finite or extreme operands take the
+    // IEEE division.
+    for (int v = v_top + threadIdx.x; v < v_max; v += blockDim.x) {
+        const double py = vpy[v + 1];
+        const double den = (double)(v + 1) - py;
+        s_px[v] = vpx[v + 1];
+        s_py[v] = py;
+        s_den[v] = den;
+        s_rcp[v] = 1.0 / den;
+    }
+    __syncthreads();
+    const int ci = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ci >= d.ext_cols) return;
     const double* m1 = d.m1 + (size_t)f * d.px;
     const uint8_t* nz = d.m1_nz + (size_t)f * d.m_nty * d.m_ntx;  // unwritten tiles are zero
     const double lg = d.lambda_g;
+    const double w_hi = (double)W - 0.5;
     double u = (double)(d.ext_lo + ci);
     bool alive = true;
     double e = 0.0;
-    // Chunks of EC rows: the track recursion (a pure division chain) yields EC
-    // gather indices, the EC m1 loads are then all in flight together, and the
-    // decayed sum consumes them in row order (same arithmetic, same order).
+    // Chunks of EC rows: the track recursion (lane_track, lanes.hpp:83-96)
+    // yields EC gather indices, the EC m1 loads are then all in flight
+    // together, and the decayed sum consumes them in row order.
     constexpr int EC = 8;
     for (int vc = v_max; vc >= v_top; vc -= EC) {
         int idx[EC];
@@ -1494,19 +1531,27 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
             idx[k] = -1;
             if (v < v_top) continue;
             if (v < v_max && alive) {
-                const double py = vpy[v + 1];
-                const double denom = (double)(v + 1) - py;
-                if (fabs(denom) < 0.5) {
+                const double py = s_py[v], den = s_den[v];
+                if (fabs(den) < 0.5) {
                     alive = false;
                 } else {
-                    u = (vpx[v + 1] + v * u - py * u) / denom;
+                    const double a = s_px[v] + v * u - py * u;
+                    const double aa = fabs(a);
+                    if (aa >= 0x1p-500 && aa <= 0x1p500 && fabs(den) <= 0x1p500) {
+                        const double y = s_rcp[v];
+                        const double q0 = __dmul_rn(a, y);
+                        u = __fma_rn(__fma_rn(-q0, den, a), y, q0);
+                    } else {
+                        u = a / den;
+                    }
                 }
             }
-            if (alive && !isnan(u)) {
-                const long long r = llround_ref(u);
-                if (r >= 0 && r < W && v >= 0 && v < H &&
-                    nz[(v >> d.m_tile_shift) * d.m_ntx + ((int)r >> 7)])
-                    idx[k] = v * W + (int)r;  // < W*H <= 2^31
+            // llround(u) in [0, W)  <=>  -0.5 < u < W - 0.5 (NaN fails); then
+            // llround = trunc + (frac >= 0.5), exact for these magnitudes
+            if (alive && u > -0.5 && u < w_hi) {
+                const int t = (int)u;
+                const int r = t + (u - (double)t >= 0.5);
+                if (nz[(v >> d.m_tile_shift) * d.m_ntx + (r >> 7)]) idx[k] = v * W + r;  // < 2^31
             }
         }
         double c[EC];
@@ -1736,7 +1781,7 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
         k_p99_collect<<<dim3(lp.collect_blocks, n), 256, 0, s>>>(d);
         k_p99_select<<<n, 256, 0, s>>>(d);
     }
-    k_energy<<<dim3((d.ext_cols + 127) / 128, n), 128, 0, s>>>(d);
+    k_energy<<<dim3((d.ext_cols + 127) / 128, n), 128, (size_t)4 * d.H * 8, s>>>(d);
     k_select<<<n, 256, lp.select_smem, s>>>(d, lp.sort_cap);
     k_finish<<<(n + 127) / 128, 128, 0, s>>>(d, n);
     mark(12);
