@@ -288,9 +288,10 @@ def run_ours(args):
     bytes_per_frame = px * 2  # u8 grey + u8 disparity
     tf = L.lk_timed_frames(h) or B  # frames the stage events covered (branch 0 of the graph)
     achieved = bytes_per_frame * tf / (dom_ms * 1e-3) / 1e9
-    fp64 = C.c_double(0)
-    L.lk_measure_fp64(local, C.byref(fp64))
-    bf_ops = 4 * (2 * ((cfg.bf_window - 1) // 2) + 1) ** 2 * px * tf  # 2 DMUL + 2 DADD per tap
+    win = 2 * ((cfg.bf_window - 1) // 2) + 1
+    taps = win * win * px * tf  # nominal range-weight evaluations of one launch
+    sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+    xu_ex2_peak = 16 * torch.cuda.get_device_properties(local).multi_processor_count * sm_mhz * 1e6
     pipe_fps_hbm = fps / world / (hbm_peak * 1e9 / bytes_per_frame)
 
     line = {
@@ -316,20 +317,24 @@ def run_ours(args):
             "algorithmic_bytes": f"{bytes_per_frame} B/frame (u8 grey + u8 disparity) x {tf}",
             "frames_per_launch": tf,
             "pipeline_frac_of_hbm_roofline": pipe_fps_hbm,
-            "fp64": {"achieved_tops": bf_ops / (dom_ms * 1e-3) / 1e12 if dom == 9 else None,
-                     "peak_tops_measured": fp64.value / 1e12,
-                     "frac": (bf_ops / (dom_ms * 1e-3)) / fp64.value if dom == 9 else None,
-                     "note": "bilateral: 121 taps x (2 DMUL + 2 DADD) per pixel, exact FP64"},
+            "compute": {
+                "kernel": "k_bilateral_fast (certified FP32 approximation, DESIGN.md §3)",
+                "taps_per_s": taps / (dom_ms * 1e-3) if dom == 9 else None,
+                "mufu_ex2_only_ceiling_per_s": xu_ex2_peak,
+                "note": "range weights split between MUFU ex2 (1 of 5 tap pairs + the last "
+                        "tap) and a shared-memory table (4 of 5 pairs); the kernel is issue-"
+                        "bound (profiles/r01_bilateral_fast_ncu.txt). taps are nominal: "
+                        "tiles with no road-mask pixel within one pixel are skipped"},
         },
         "notes": f"paper: {PAPER_FPS} fps on GTX 970M + i7 (different hardware, context only)",
     }
     traffic = ROOT / "profiles" / "traffic.json"
     if traffic.exists():
         try:
-            t = json.loads(traffic.read_text()).get(args.config, {}).get(str(dom))
-            if t:
-                line["roofline"]["traffic"] = t * (B / json.loads(traffic.read_text())
-                                                  [args.config]["frames"])
+            tj = json.loads(traffic.read_text()).get(args.config, {})
+            t = tj.get(str(dom))
+            if t:  # per launch, scaled to the frames this run's launch covers
+                line["roofline"]["traffic"] = t * tf / tj["frames"]
         except Exception:
             pass
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

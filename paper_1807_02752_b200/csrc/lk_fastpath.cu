@@ -42,7 +42,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // range factor as the limiter. Tap pairs in the mask TB take it from a
 // 511-entry shared-memory table instead of MUFU ex2, so the XU and the LSU
 // pipes share the work. The table index comes from the float difference
-// itself: dr*1020 is within 1e-4 of the integer 4(k_q - k_p), so one FFMA with
+// itself: dr*1020*RC is within 3e-3 of the integer 4 RC (k_q - k_p), so one FFMA with
 // 1.5*2^23 rounds it into the low mantissa bits (no integer keys staged).
 // w = S_t * R[dr] rounds three times in FP32 (~2e-7 relative), inside the
 // ex2.approx error the bound in DESIGN.md already budgets.
@@ -52,12 +52,17 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // border stays within that pixel). Tiles whose one-pixel ring holds no masked
 // pixel are skipped; the test is the exact mask of k_sobel_refine
 // (road_mask, preprocess.hpp:14-25). all = 1 computes every tile (lk_fast_path_error).
+//
+// The table is replicated RC times, entry-major (word i * RC + copy), and lane
+// L reads copy L % RC: lanes with different entries then collide in a bank
+// at most 32 / RC ways (RC = 16: 2-way) instead of up to 16-way.
 template <int RHO, int TB>
 __global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p, int all) {
     constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
     constexpr int NPX = TWh * THh;
+    constexpr int RC = BF_TABLE_COPIES;
     static_assert(WIN == 11, "packed tap pairs assume an 11-wide window");
-    __shared__ float s_v[NPX], s_vf[256], s_R[512];
+    __shared__ float s_v[NPX], s_vf[256], s_R[TB ? 512 * RC : 1];
     __shared__ int s_row[THh], s_col[TWh];
     const int f = blockIdx.z;
     if (frame_failed(d, f)) return;
@@ -81,8 +86,13 @@ __global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p,
     const uint8_t* g = d.grey + (size_t)f * d.px;
     s_vf[threadIdx.x] = __ldg(d.fast_tab + threadIdx.x);
     if (TB) {
-        s_R[threadIdx.x] = __ldg(d.fast_tab + 256 + threadIdx.x);
-        s_R[threadIdx.x + 256] = __ldg(d.fast_tab + 512 + threadIdx.x);
+        const float r0 = __ldg(d.fast_tab + 256 + threadIdx.x);
+        const float r1 = __ldg(d.fast_tab + 512 + threadIdx.x);
+#pragma unroll
+        for (int k = 0; k < RC; ++k) {
+            s_R[threadIdx.x * RC + k] = r0;
+            s_R[(threadIdx.x + 256) * RC + k] = r1;
+        }
     }
     if (threadIdx.x < THh) s_row[threadIdx.x] = mirror(v0 + (int)threadIdx.x - RHO, d.H) * d.W;
     if (threadIdx.x < TWh) s_col[threadIdx.x] = mirror(u0 + (int)threadIdx.x - RHO, d.W);
@@ -104,11 +114,13 @@ __global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p,
     }
     const float2 c2 = make_float2(p.c2, p.c2);
     constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float + kMagic rounds to an integer
-    // t = dr*1020 + kMagic + 1020: its bit pattern is __float_as_int(kMagic) + the
-    // BYTE offset 4*(k_q - k_p + 255) of the table entry, so the LDS needs no
-    // address arithmetic beyond one add of a uniform base
-    const float2 k1020 = make_float2(1020.f, 1020.f), mg = make_float2(kMagic + 1020.f, kMagic + 1020.f);
-    const char* Rb = reinterpret_cast<const char*>(s_R) - __float_as_int(kMagic);
+    // t = dr*S + kMagic + S, S = 4 * 255 * RC: its bit pattern is
+    // __float_as_int(kMagic) + the BYTE offset 4 * RC * (k_q - k_p + 255) of the
+    // entry, so the LDS needs one add of the thread's base (its copy) only
+    constexpr float kS = 1020.f * RC;
+    const float2 kscale = make_float2(kS, kS), mg = make_float2(kMagic + kS, kMagic + kS);
+    const char* Rb = reinterpret_cast<const char*>(s_R) + 4 * (threadIdx.x % RC) -
+                     __float_as_int(kMagic);
 #pragma unroll
     for (int jj = 0; jj < BT_R + 2 * RHO; ++jj) {
         const int prow = (r0 + jj) * TWh + tx;
@@ -127,7 +139,7 @@ __global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p,
                 const float2 dr = __fadd2_rn(vp[q], nva[r]);
                 float2 w;
                 if ((TB >> q) & 1) {
-                    const float2 t = __ffma2_rn(dr, k1020, mg);
+                    const float2 t = __ffma2_rn(dr, kscale, mg);
                     w = __fmul2_rn(p.sp[dj][q],
                                    make_float2(*reinterpret_cast<const float*>(Rb + __float_as_int(t.x)),
                                                *reinterpret_cast<const float*>(Rb + __float_as_int(t.y))));

@@ -11,6 +11,11 @@ constexpr int K1_ROWS = 8;              // rows per v-disparity CTA
 constexpr int BF_TW = 32, BF_TH = 8;    // bilateral tile (generic window)
 constexpr int BT_W = 64, BT_H = 16, BT_R = 4;  // bilateral tile (11x11), outputs per thread
 constexpr int BT_TRI_N = 128;           // max distinct values per tile for the smem sub-table
+#ifndef BF_TABLE_COPIES
+#define BF_TABLE_COPIES 1               // fast-bilateral range table replicas: 1 is fastest
+                                        // (neighbouring lanes mostly read the same entry and
+                                        // get broadcast; 16 copies measured 1.5x slower)
+#endif
 constexpr int K4_THREADS = 512;         // V_px CTA (2 per SM)
 constexpr int K4_VOTE_CAP = 8192;       // edges whose vote columns are staged in smem
 constexpr int BT_CHUNK = 32;            // u-path backtrack: stages per window
