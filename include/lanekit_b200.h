@@ -244,7 +244,7 @@ lk_status lk_get_stage(lk_ctx* ctx, int frame, int stage, void* dst, size_t capa
  * from CUDA events recorded on the context stream around each stage's kernels
  * (event-record nodes inside the CUDA graph); ms[0] is the whole batch.
  * Stage 8 (road mask) is fused into stage 10's Sobel pass and reads ~0.
- * A captured batch runs as up to LK_BRANCHES (env, default 2) concurrent
+ * A captured batch runs as up to LK_BRANCHES (env, default 4) concurrent
  * frame ranges; the events time the first range (lk_timed_frames frames)
  * while the others overlap it. ms[0] is then that range's span. */
 lk_status lk_stage_times(lk_ctx* ctx, float ms[13]);

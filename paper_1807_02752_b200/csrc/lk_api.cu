@@ -12,6 +12,7 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <tuple>
 #include <random>
 #include <string>
 #include <vector>
@@ -78,9 +79,11 @@ const char* config_problem(const lk_config& c) {
 }
 
 constexpr int kMaxIter = 200;  // pipeline.hpp:198, 244
-constexpr int kMaxBranches = 4;       // concurrent frame ranges in a captured batch
+constexpr int kMaxBranches = 8;       // concurrent frame ranges (streams) per batch
 constexpr int kMinBranchFrames = 16;  // smallest range worth a branch
-constexpr int kFastTableDefault = 27;  // tap pairs of the fast bilateral served by the range table
+constexpr int kH2dChunksDefault = 8;  // host-fed batches: copy/compute pipeline depth
+constexpr int kBranchesDefault = 4;   // device-resident batches: concurrent frame ranges
+constexpr int kFastTableDefault = 21;  // tap pairs of the fast bilateral served by the range table
 
 }  // namespace
 
@@ -96,6 +99,9 @@ struct lk_ctx {
     int branches = 1;
     cudaStream_t side[kMaxBranches - 1] = {};
     cudaEvent_t fork = nullptr, join[kMaxBranches - 1] = {};
+    cudaEvent_t copied[kMaxBranches] = {};   // host-fed pipeline: chunk k's inputs are resident
+    int h2d_chunks = kMaxBranches;           // host-fed batches: copy/compute pipeline depth
+    std::map<std::tuple<long, int, int>, cudaGraphExec_t> range_graphs;  // (f0, n, timed)
     int timed_frames = 0;
     bool timed = false;
     std::vector<void*> allocs;
@@ -491,15 +497,23 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     for (int i = 0; i < 13 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     {
         const char* b = std::getenv("LK_BRANCHES");
-        c->branches = b ? std::atoi(b) : 2;
+        c->branches = b ? std::atoi(b) : kBranchesDefault;
         if (c->branches < 1) c->branches = 1;
         if (c->branches > kMaxBranches) c->branches = kMaxBranches;
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
-    for (int i = 0; i < c->branches - 1 && e == cudaSuccess; ++i) {
+    {
+        const char* k = std::getenv("LK_H2D_CHUNKS");
+        c->h2d_chunks = k ? std::atoi(k) : kH2dChunksDefault;
+        if (c->h2d_chunks < 1) c->h2d_chunks = 1;
+        if (c->h2d_chunks > kMaxBranches) c->h2d_chunks = kMaxBranches;
+    }
+    for (int i = 0; i < kMaxBranches - 1 && e == cudaSuccess; ++i) {
         e = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join[i], cudaEventDisableTiming);
     }
+    for (int i = 0; i < kMaxBranches && e == cudaSuccess; ++i)
+        e = cudaEventCreateWithFlags(&c->copied[i], cudaEventDisableTiming);
     if (e != cudaSuccess) {
         lk_destroy(c);
         return fail(LK_ERR_CUDA, std::string("context setup: ") + cudaGetErrorString(e));
@@ -513,6 +527,9 @@ lk_status lk_destroy(lk_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : c->range_graphs) cudaGraphExecDestroy(kv.second);
+    for (cudaEvent_t e : c->copied)
+        if (e) cudaEventDestroy(e);
     if (c->d.wr_tex) cudaDestroyTextureObject((cudaTextureObject_t)c->d.wr_tex);
     for (cudaEvent_t e : c->ev)
         if (e) cudaEventDestroy(e);
@@ -652,6 +669,64 @@ static lk_status enqueue_direct(lk_ctx* c, int n, bool timed) {
     return LK_OK;
 }
 
+// Replays (capturing on first use) the graph of frames [f0, f0 + n) on st.
+static lk_status launch_range_graph(lk_ctx* c, size_t f0, int n, cudaStream_t st, bool timed) {
+    const auto key = std::make_tuple((long)f0, n, timed ? 1 : 0);
+    auto it = c->range_graphs.find(key);
+    if (it == c->range_graphs.end()) {
+        cudaGraph_t g;
+        CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        lk_status s = enqueue_range(c, f0, n, st, timed ? c->ev : nullptr);
+        cudaError_t e = cudaStreamEndCapture(st, &g);
+        if (s != LK_OK) return s;
+        if (e != cudaSuccess) return fail(LK_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        cudaGraphExec_t ex;
+        e = cudaGraphInstantiate(&ex, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(LK_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        it = c->range_graphs.emplace(key, ex).first;
+    }
+    CU(cudaGraphLaunch(it->second, st));
+    return LK_OK;
+}
+
+// Host-fed batch: the frames are split into up to h2d_chunks ranges on the
+// context's streams. Range k's host->device copy starts when range k-1's
+// copy is done (the copies share the link), and range k's graph starts as
+// soon as its own inputs are resident, so copies overlap the compute of the
+// ranges before them instead of preceding the whole batch.
+static lk_status run_host_pipelined(lk_ctx* c, const uint8_t* grey, const uint8_t* disp, int n) {
+    int nk = c->h2d_chunks;
+    while (nk > 1 && n / nk < kMinBranchFrames) --nk;
+    const size_t px = c->d.px;
+    c->last_n = n;
+    c->timed = true;
+    CU(cudaEventRecord(c->fork, c->stream));
+    size_t f0 = 0;
+    for (int k = 0; k < nk; ++k) {
+        const int nf = n / nk + (k < n % nk);
+        cudaStream_t st = k == 0 ? c->stream : c->side[k - 1];
+        if (k) CU(cudaStreamWaitEvent(st, c->copied[k - 1], 0));
+        CU(cudaMemcpyAsync(c->in_grey + f0 * px, grey + f0 * px, (size_t)nf * px,
+                           cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(c->in_disp + f0 * px, disp + f0 * px, (size_t)nf * px,
+                           cudaMemcpyHostToDevice, st));
+        CU(cudaEventRecord(c->copied[k], st));
+        if (k == 0) c->timed_frames = nf;
+        if (c->flags & LK_FLAG_NO_GRAPH) {
+            if (lk_status s = enqueue_range(c, f0, nf, st, k == 0 ? c->ev : nullptr)) return s;
+        } else if (lk_status s = launch_range_graph(c, f0, nf, st, k == 0)) {
+            return s;
+        }
+        f0 += nf;
+    }
+    for (int k = 1; k < nk; ++k) {
+        CU(cudaEventRecord(c->join[k - 1], c->side[k - 1]));
+        CU(cudaStreamWaitEvent(c->stream, c->join[k - 1], 0));
+    }
+    return LK_OK;
+}
+
 lk_status lk_enqueue(lk_ctx* c, int n) {
     if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
     if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
@@ -706,10 +781,15 @@ lk_status lk_run_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* disparity,
     if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
     CU(cudaSetDevice(c->device));
     const size_t bytes = (size_t)n * c->d.px;
-    const cudaMemcpyKind k = where == LK_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (grey != c->in_grey) CU(cudaMemcpyAsync(c->in_grey, grey, bytes, k, c->stream));
-    if (disparity != c->in_disp) CU(cudaMemcpyAsync(c->in_disp, disparity, bytes, k, c->stream));
-    if (lk_status s = lk_enqueue(c, n)) return s;
+    if (where == LK_MEM_HOST) {
+        if (lk_status s = run_host_pipelined(c, grey, disparity, n)) return s;
+    } else {
+        if (grey != c->in_grey)
+            CU(cudaMemcpyAsync(c->in_grey, grey, bytes, cudaMemcpyDeviceToDevice, c->stream));
+        if (disparity != c->in_disp)
+            CU(cudaMemcpyAsync(c->in_disp, disparity, bytes, cudaMemcpyDeviceToDevice, c->stream));
+        if (lk_status s = lk_enqueue(c, n)) return s;
+    }
     if (reports) return lk_fetch_reports(c, reports, n);
     CU(cudaStreamSynchronize(c->stream));
     return LK_OK;
