@@ -178,7 +178,13 @@ typedef enum lk_stage {
     LK_STAGE_ENERGY = 19,
     LK_STAGE_LANES = 20,
     LK_STAGE_POLYLINES = 21,
-    LK_STAGE_COUNT = 22
+    /* stereo contexts (LK_FLAG_STEREO): PipelineResult members of stages 1-4 */
+    LK_STAGE_STATS_MU = 22,    /* f64 [H][W] stats_left.mu (0 on the border)      */
+    LK_STAGE_STATS_SIGMA = 23, /* f64 [H][W] stats_left.sigma                     */
+    LK_STAGE_DISP_LEFT = 24,   /* u8 [H][W] match_srp, left reference             */
+    LK_STAGE_DISP_RIGHT = 25,  /* u8 [H][W] match_srp, right reference            */
+    LK_STAGE_DISPARITY = 26,   /* u8 [H][W] lrc_check result (input of stage 5)   */
+    LK_STAGE_COUNT = 27
 } lk_stage;
 
 typedef struct lk_edge {   /* lanekit::EdgePixel (preprocess.hpp:92-95) */
@@ -199,6 +205,9 @@ typedef struct lk_lane {   /* lanekit::Lane (lanes.hpp:131-135) minus the polyli
 /* Context flags. */
 #define LK_FLAG_HOOKS 1u   /* also materialise mask, gx/gy/mag/theta, accumulator, m0 */
 #define LK_FLAG_NO_GRAPH 2u /* launch kernels directly instead of replaying a CUDA graph */
+#define LK_FLAG_STEREO 8u  /* also run stages 1-4 (stereo.hpp): stereo pair in, the whole
+                              * run_pipeline (pipeline.hpp:118-270); needs d_max <= 255 and
+                              * a block radius rho of 1..5 */
 #define LK_FLAG_EXACT 4u    /* exact bilateral on every pixel even without hooks (the
                                default throughput path computes it exactly only around
                                edge candidates; outputs are identical either way) */
@@ -251,6 +260,20 @@ lk_status lk_stage_times(lk_ctx* ctx, float ms[13]);
 
 /* Frames of the last batch covered by lk_stage_times. */
 int lk_timed_frames(lk_ctx* ctx);
+
+/* ---- stereo pair in (LK_FLAG_STEREO contexts): run_pipeline itself.
+ * lanekit::run_pipeline(left, right, cfg)      pipeline.hpp:118-270 -> lk_run_stereo_batch
+ *   stage 1 precompute_stats                   stereo.hpp:39-60     (both images)
+ *   stages 2/3 match_srp, left / right ref     stereo.hpp:157-196
+ *   stage 4 lrc_check                          stereo.hpp:263-276   -> the stage-5 disparity
+ * left/right: u8 [n][H][W] (k means k/255.0, image_io.hpp:147). Reports as lk_run_batch;
+ * lk_stage_times then also fills ms[1..4] (the two SRP views run as one launch: ms[3] ~ 0). */
+lk_status lk_run_stereo_batch(lk_ctx* ctx, const uint8_t* left, const uint8_t* right, int n,
+                              lk_mem where, lk_frame_report* reports);
+/* Device buffers [max_batch][H][W] for the left / right grey of lk_enqueue_stereo. */
+lk_status lk_stereo_inputs(lk_ctx* ctx, uint8_t** left, uint8_t** right);
+/* Enqueues stages 1-12 on frames already in the stereo input buffers (asynchronous). */
+lk_status lk_enqueue_stereo(lk_ctx* ctx, int n);
 
 /* Measured FP64 add+mul issue rate of this device (ops/s), for rooflines. */
 lk_status lk_measure_fp64(int device, double* ops_per_s);
@@ -305,6 +328,9 @@ lk_status lk_synth_scene(const lk_scene_params* p, uint8_t* grey_l, uint8_t* gre
 /* n scenes in parallel on host threads: params[i] -> frame i. */
 lk_status lk_synth_batch(const lk_scene_params* params, int n, uint8_t* grey, uint8_t* disparity,
                          int threads);
+/* Same, with the right view too (any output may be NULL). */
+lk_status lk_synth_stereo_batch(const lk_scene_params* params, int n, uint8_t* left,
+                                uint8_t* right, uint8_t* disparity, int threads);
 
 #ifdef __cplusplus
 }

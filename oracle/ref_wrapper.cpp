@@ -17,6 +17,7 @@
 #include "lanekit/lanes.hpp"
 #include "lanekit/preprocess.hpp"
 #include "lanekit/road_profile.hpp"
+#include "lanekit/stereo.hpp"
 #include "lanekit/synth.hpp"
 #include "lanekit/vanish.hpp"
 #include "lk_oracle.hpp"
@@ -289,6 +290,44 @@ int lkref_gen_scene(const lk_scene_params* p, uint8_t* left, uint8_t* right, uin
             std::strncpy(msg, e.what(), msglen - 1);
             msg[msglen - 1] = 0;
         }
+        return 1;
+    }
+}
+
+// Stages 1-4 exactly as run_pipeline composes them (pipeline.hpp:161-182):
+// precompute_stats on both images, match_srp for the left and the right
+// reference, lrc_check. Same outputs as orc_stereo.
+int lkref_stereo(const uint8_t* left, const uint8_t* right, int W, int H, int rho, int d_max,
+                 int tau, int tr_lrc, double sigma_floor, double* mu_l, double* sig_l,
+                 uint8_t* disp_l, uint8_t* disp_r, uint8_t* disparity) {
+    try {
+        GrayImage L(W, H, 0), R(W, H, 0);
+        for (size_t i = 0; i < L.data.size(); ++i) {
+            L.data[i] = left[i] / 255.0;  // image_io.hpp:147
+            R.data[i] = right[i] / 255.0;
+        }
+        StereoConfig sc;
+        sc.rho = rho;
+        sc.d_min = 0;
+        sc.d_max = d_max;
+        sc.tau = tau;
+        sc.tr_lrc = tr_lrc;
+        sc.sigma_floor = sigma_floor;
+        sc.threads = 1;
+        const BlockStats ls = precompute_stats(L, rho);
+        const BlockStats rs = precompute_stats(R, rho);
+        const DisparityMap dl = match_srp(L, R, ls, rs, RefView::left, sc);
+        const DisparityMap dr = match_srp(R, L, rs, ls, RefView::right, sc);
+        const DisparityMap out = lrc_check(dl, dr, tr_lrc);
+        for (size_t i = 0; i < L.data.size(); ++i) {
+            if (mu_l) mu_l[i] = ls.mu.data[i];
+            if (sig_l) sig_l[i] = ls.sigma.data[i];
+            if (disp_l) disp_l[i] = static_cast<uint8_t>(dl.data[i]);
+            if (disp_r) disp_r[i] = static_cast<uint8_t>(dr.data[i]);
+            if (disparity) disparity[i] = static_cast<uint8_t>(out.data[i]);
+        }
+        return 0;
+    } catch (const Error&) {
         return 1;
     }
 }

@@ -20,6 +20,7 @@ LK_ERR_UNAVAILABLE = 6
 LK_FLAG_HOOKS = 1
 LK_FLAG_NO_GRAPH = 2
 LK_FLAG_EXACT = 4
+LK_FLAG_STEREO = 8
 
 LK_MEM_HOST = 0
 LK_MEM_DEVICE = 1
@@ -29,6 +30,8 @@ STAGES = [
     "VDISPARITY", "VPATH", "BETA_INLIERS", "VPY", "VPY_SINGULAR", "MASK", "SMOOTHED",
     "GX", "GY", "MAG", "THETA", "EDGES", "VOTES", "VPX_ACC", "UPATH", "GAMMA_INLIERS",
     "VPX", "M0", "M1", "ENERGY", "LANES", "POLYLINES",
+    # stereo batches (LK_FLAG_STEREO): stats_left, SRP maps, the LRC disparity
+    "STATS_MU", "STATS_SIGMA", "DISP_LEFT", "DISP_RIGHT", "DISPARITY",
 ]
 STAGE = {name: i for i, name in enumerate(STAGES)}
 
@@ -231,4 +234,8 @@ def decode_stage(stage: int, raw: bytes, width: int, height: int, d_max: int,
         return np.frombuffer(raw, _LANE_DT)
     if name == "POLYLINES":
         return np.frombuffer(raw, "<f8").reshape(-1, rows)
+    if name in ("STATS_MU", "STATS_SIGMA"):
+        return np.frombuffer(raw, "<f8").reshape(H, W)
+    if name in ("DISP_LEFT", "DISP_RIGHT", "DISPARITY"):
+        return np.frombuffer(raw, "u1").reshape(H, W)
     raise ValueError(name)

@@ -17,7 +17,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "liblanekit_b200.so"
-SOURCES = ["lk_api.cu", "lk_kernels.cu", "lk_fastpath.cu", "synth.cpp"]
+SOURCES = ["lk_api.cu", "lk_kernels.cu", "lk_fastpath.cu", "lk_stereo.cu", "synth.cpp"]
 HEADERS = ["lk_device.cuh", "lk_fit.cuh", "lk_kernels.h", "../../include/lanekit_b200.h"]
 
 NVCC_FLAGS = [

@@ -101,13 +101,16 @@ struct lk_ctx {
     cudaEvent_t fork = nullptr, join[kMaxBranches - 1] = {};
     cudaEvent_t copied[kMaxBranches] = {};   // host-fed pipeline: chunk k's inputs are resident
     int h2d_chunks = kMaxBranches;           // host-fed batches: copy/compute pipeline depth
-    std::map<std::tuple<long, int, int>, cudaGraphExec_t> range_graphs;  // (f0, n, timed)
+    std::map<std::tuple<long, int, int>, cudaGraphExec_t> range_graphs;  // (f0, n, timed|stereo)
     int timed_frames = 0;
     bool timed = false;
     std::vector<void*> allocs;
     std::map<int, cudaGraphExec_t> graphs;
-    uint8_t* in_grey = nullptr;
-    uint8_t* in_disp = nullptr;
+    uint8_t* in_grey = nullptr;  // the (left) grey
+    uint8_t* in_disp = nullptr;  // the disparity (stereo: written by stage 4)
+    uint8_t* in_right = nullptr; // stereo contexts: the right grey
+    bool run_stereo = false;     // the batch being enqueued runs stages 1-4 first
+    bool last_stereo = false;
     int last_n = 0;
 
     template <typename T>
@@ -268,6 +271,24 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         delete c;
         return fail(LK_ERR_CONFIG, "extended column axis is empty");
     }
+    if (flags & LK_FLAG_STEREO) {  // run_pipeline's stage-1 checks (pipeline.hpp:121-126)
+        const char* why = nullptr;
+        if (W <= 2 * cfg->rho || H <= 2 * cfg->rho)
+            why = "stage 1 (block statistics): image smaller than the matching block";
+        else if (cfg->rho < 1 || cfg->rho > 5)
+            why = "stereo: block radius rho must be 1..5 on the GPU";
+        else if (cfg->d_max > 255)
+            why = "stereo: d_max must be <= 255 (u8 disparity maps)";
+        if (why) {
+            delete c;
+            return fail(LK_ERR_INVALID_ARGUMENT, why);
+        }
+        d.stereo = 1;
+        d.srho = cfg->rho;
+        d.tau = cfg->tau;
+        d.tr_lrc = cfg->tr_lrc;
+        d.sigma_floor = cfg->sigma_floor;
+    }
     const int C = d.ext_cols, D1 = d.D1;
 
     // ---- exact host tables (glibc exp, as the reference evaluates them)
@@ -330,6 +351,16 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     A(&d_rng, rng.size());
     A(&c->in_grey, (size_t)B * d.px);
     A(&c->in_disp, (size_t)B * d.px);
+    if (d.stereo) {
+        A(&c->in_right, (size_t)B * d.px);
+        A(&d.sat, (size_t)B * 4 * d.px);
+        A(&d.mu_l, (size_t)B * d.px);
+        A(&d.sig_l, (size_t)B * d.px);
+        A(&d.mu_r, (size_t)B * d.px);
+        A(&d.sig_r, (size_t)B * d.px);
+        A(&d.disp_l, (size_t)B * d.px);
+        A(&d.disp_r, (size_t)B * d.px);
+    }
     A(&d.rep, (size_t)B);
     A(&d.aux, (size_t)B);
     A(&d.vhist, (size_t)B * H * D1);
@@ -384,6 +415,8 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     d.rng = d_rng;
     d.grey = c->in_grey;
     d.disp = c->in_disp;
+    d.right = c->in_right;
+    d.disp_out = d.stereo ? c->in_disp : nullptr;
     if (!d.hooks) d.vchoice = nullptr;
 
     // ---- shared-memory plan
@@ -475,6 +508,13 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         return s;
     }
     cudaError_t e = lkg::configure_kernels(lp);
+    if (e == cudaSuccess && d.stereo) {
+        if (lkg::stereo_smem(d) > smem_cap) {
+            lk_destroy(c);
+            return fail(LK_ERR_CONFIG, "stereo: frame width exceeds the shared-memory row window");
+        }
+        e = lkg::configure_stereo(d);
+    }
     if (e == cudaSuccess) {  // texture view of the exact weight table (TEX-pipe gathers)
         cudaResourceDesc rd{};
         rd.resType = cudaResourceTypeLinear;
@@ -552,7 +592,8 @@ void* lk_stream(lk_ctx* c) { return c ? (void*)c->stream : nullptr; }
 static int branch_count(const lk_ctx* c, int n);
 
 int lk_launches_per_batch(lk_ctx* c) {
-    return c ? lkg::launches_per_batch(c->d) * branch_count(c, c->last_n ? c->last_n : c->max_batch)
+    return c ? (lkg::launches_per_batch(c->d) + (c->last_stereo ? lkg::stereo_launches() : 0)) *
+                   branch_count(c, c->last_n ? c->last_n : c->max_batch)
              : 0;
 }
 
@@ -577,6 +618,15 @@ static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     };
     sh(v.grey, px);
     sh(v.disp, px);
+    sh(v.right, px);
+    sh(v.sat, 4 * px);
+    sh(v.mu_l, px);
+    sh(v.sig_l, px);
+    sh(v.mu_r, px);
+    sh(v.sig_r, px);
+    sh(v.disp_l, px);
+    sh(v.disp_r, px);
+    sh(v.disp_out, px);
     sh(v.rep, 1);
     sh(v.aux, 1);
     sh(v.vhist, H * D1);
@@ -630,7 +680,8 @@ static lk_status enqueue_range(lk_ctx* c, size_t f0, int n, cudaStream_t st, cud
         CU(cudaMemsetAsync(d.p99hist, 0, (size_t)n * 2048 * sizeof(unsigned), st));
         CU(cudaMemsetAsync(d.p99hist2, 0, (size_t)n * 4096 * sizeof(unsigned), st));
     }
-    CU(lkg::launch_pipeline(d, lp, n, st, ev));
+    if (c->run_stereo) CU(lkg::launch_stereo(d, n, st, ev));
+    CU(lkg::launch_pipeline(d, lp, n, st, ev, !c->run_stereo));
     return LK_OK;
 }
 
@@ -671,7 +722,7 @@ static lk_status enqueue_direct(lk_ctx* c, int n, bool timed) {
 
 // Replays (capturing on first use) the graph of frames [f0, f0 + n) on st.
 static lk_status launch_range_graph(lk_ctx* c, size_t f0, int n, cudaStream_t st, bool timed) {
-    const auto key = std::make_tuple((long)f0, n, timed ? 1 : 0);
+    const auto key = std::make_tuple((long)f0, n, (timed ? 1 : 0) | (c->run_stereo ? 2 : 0));
     auto it = c->range_graphs.find(key);
     if (it == c->range_graphs.end()) {
         cudaGraph_t g;
@@ -696,11 +747,13 @@ static lk_status launch_range_graph(lk_ctx* c, size_t f0, int n, cudaStream_t st
 // soon as its own inputs are resident, so copies overlap the compute of the
 // ranges before them instead of preceding the whole batch.
 static lk_status run_host_pipelined(lk_ctx* c, const uint8_t* grey, const uint8_t* disp, int n) {
+    uint8_t* second = c->run_stereo ? c->in_right : c->in_disp;  // right grey or disparity
     int nk = c->h2d_chunks;
     while (nk > 1 && n / nk < kMinBranchFrames) --nk;
     const size_t px = c->d.px;
     c->last_n = n;
     c->timed = true;
+    c->last_stereo = c->run_stereo;
     CU(cudaEventRecord(c->fork, c->stream));
     size_t f0 = 0;
     for (int k = 0; k < nk; ++k) {
@@ -709,7 +762,7 @@ static lk_status run_host_pipelined(lk_ctx* c, const uint8_t* grey, const uint8_
         if (k) CU(cudaStreamWaitEvent(st, c->copied[k - 1], 0));
         CU(cudaMemcpyAsync(c->in_grey + f0 * px, grey + f0 * px, (size_t)nf * px,
                            cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(c->in_disp + f0 * px, disp + f0 * px, (size_t)nf * px,
+        CU(cudaMemcpyAsync(second + f0 * px, disp + f0 * px, (size_t)nf * px,
                            cudaMemcpyHostToDevice, st));
         CU(cudaEventRecord(c->copied[k], st));
         if (k == 0) c->timed_frames = nf;
@@ -727,17 +780,17 @@ static lk_status run_host_pipelined(lk_ctx* c, const uint8_t* grey, const uint8_
     return LK_OK;
 }
 
-lk_status lk_enqueue(lk_ctx* c, int n) {
-    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
-    if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
+static lk_status enqueue_mode(lk_ctx* c, int n) {
     CU(cudaSetDevice(c->device));
     c->last_n = n;
+    c->last_stereo = c->run_stereo;
     if (c->flags & LK_FLAG_NO_GRAPH) {
         c->timed = true;
         return enqueue_direct(c, n, true);
     }
     c->timed = true;
-    auto it = c->graphs.find(n);
+    const int key = 2 * n + (c->run_stereo ? 1 : 0);
+    auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
         cudaGraph_t g;
         CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -749,9 +802,32 @@ lk_status lk_enqueue(lk_ctx* c, int n) {
         e = cudaGraphInstantiate(&ex, g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) return fail(LK_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-        it = c->graphs.emplace(n, ex).first;
+        it = c->graphs.emplace(key, ex).first;
     }
     CU(cudaGraphLaunch(it->second, c->stream));
+    return LK_OK;
+}
+
+lk_status lk_enqueue(lk_ctx* c, int n) {
+    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
+    if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
+    c->run_stereo = false;
+    return enqueue_mode(c, n);
+}
+
+lk_status lk_enqueue_stereo(lk_ctx* c, int n) {
+    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
+    if (!c->d.stereo) return fail(LK_ERR_INVALID_ARGUMENT, "context was created without LK_FLAG_STEREO");
+    if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
+    c->run_stereo = true;
+    return enqueue_mode(c, n);
+}
+
+lk_status lk_stereo_inputs(lk_ctx* c, uint8_t** left, uint8_t** right) {
+    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
+    if (!c->d.stereo) return fail(LK_ERR_INVALID_ARGUMENT, "context was created without LK_FLAG_STEREO");
+    if (left) *left = c->in_grey;
+    if (right) *right = c->in_right;
     return LK_OK;
 }
 
@@ -781,6 +857,7 @@ lk_status lk_run_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* disparity,
     if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
     CU(cudaSetDevice(c->device));
     const size_t bytes = (size_t)n * c->d.px;
+    c->run_stereo = false;
     if (where == LK_MEM_HOST) {
         if (lk_status s = run_host_pipelined(c, grey, disparity, n)) return s;
     } else {
@@ -795,13 +872,35 @@ lk_status lk_run_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* disparity,
     return LK_OK;
 }
 
+lk_status lk_run_stereo_batch(lk_ctx* c, const uint8_t* left, const uint8_t* right, int n,
+                              lk_mem where, lk_frame_report* reports) {
+    if (!c || !left || !right) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    if (!c->d.stereo) return fail(LK_ERR_INVALID_ARGUMENT, "context was created without LK_FLAG_STEREO");
+    if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
+    CU(cudaSetDevice(c->device));
+    const size_t bytes = (size_t)n * c->d.px;
+    c->run_stereo = true;
+    if (where == LK_MEM_HOST) {
+        if (lk_status s = run_host_pipelined(c, left, right, n)) return s;
+    } else {
+        if (left != c->in_grey)
+            CU(cudaMemcpyAsync(c->in_grey, left, bytes, cudaMemcpyDeviceToDevice, c->stream));
+        if (right != c->in_right)
+            CU(cudaMemcpyAsync(c->in_right, right, bytes, cudaMemcpyDeviceToDevice, c->stream));
+        if (lk_status s = enqueue_mode(c, n)) return s;
+    }
+    if (reports) return lk_fetch_reports(c, reports, n);
+    CU(cudaStreamSynchronize(c->stream));
+    return LK_OK;
+}
+
 lk_status lk_stage_times(lk_ctx* c, float ms[13]) {
     if (!c || !ms) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
     for (int i = 0; i < 13; ++i) ms[i] = 0.f;
     if (!c->timed) return fail(LK_ERR_UNAVAILABLE, "no batch has run yet");
     CU(cudaStreamSynchronize(c->stream));
     int prev = 0;
-    for (int st : {5, 6, 7, 8, 9, 10, 11, 12}) {
+    for (int st = c->last_stereo ? 1 : 5; st <= 12; ++st) {  // [st] = end of stage st
         CU(cudaEventElapsedTime(&ms[st], c->ev[prev], c->ev[st]));
         prev = st;
     }
@@ -819,8 +918,11 @@ lk_status lk_get_stage(lk_ctx* c, int frame, int stage, void* dst, size_t capaci
     const Dev& d = c->d;
     lk_frame_report rep;
     CU(cudaMemcpy(&rep, d.rep + frame, sizeof rep, cudaMemcpyDeviceToHost));
-    static const int produced_by[LK_STAGE_COUNT] = {5, 6, 7, 7, 7, 8, 9, 10, 10, 10, 10,
-                                                    10, 11, 11, 11, 11, 11, 12, 12, 12, 12, 12};
+    static const int produced_by[LK_STAGE_COUNT] = {5,  6,  7,  7,  7,  8,  9,  10, 10,
+                                                    10, 10, 10, 11, 11, 11, 11, 11, 12,
+                                                    12, 12, 12, 12, 1,  1,  2,  3,  4};
+    if (stage >= LK_STAGE_STATS_MU && !c->last_stereo)
+        return fail(LK_ERR_UNAVAILABLE, "stage 1-4 hooks need a stereo batch (lk_run_stereo_batch)");
     if (rep.status != 0 && rep.failed_stage <= produced_by[stage])
         return fail(LK_ERR_UNAVAILABLE, "stage not reached: the frame failed earlier");
     const bool hook_only = stage == LK_STAGE_MASK || stage == LK_STAGE_GX || stage == LK_STAGE_GY ||
@@ -844,6 +946,11 @@ lk_status lk_get_stage(lk_ctx* c, int frame, int stage, void* dst, size_t capaci
     };
     lk_status s = LK_OK;
     switch (stage) {
+        case LK_STAGE_STATS_MU: s = grab(d.mu_l + f * px, px * 8); break;
+        case LK_STAGE_STATS_SIGMA: s = grab(d.sig_l + f * px, px * 8); break;
+        case LK_STAGE_DISP_LEFT: s = grab(d.disp_l + f * px, px); break;
+        case LK_STAGE_DISP_RIGHT: s = grab(d.disp_r + f * px, px); break;
+        case LK_STAGE_DISPARITY: s = grab(d.disp_out + f * px, px); break;
         case LK_STAGE_VDISPARITY: s = grab(d.vhist + f * H * D1, H * D1 * 4); break;
         case LK_STAGE_VPATH: s = grab(d.vpath + f * D1 * 2, D1 * 8); break;
         case LK_STAGE_BETA_INLIERS:
@@ -891,13 +998,14 @@ lk_status lk_get_stage(lk_ctx* c, int frame, int stage, void* dst, size_t capaci
         case LK_STAGE_M1: {
             s = grab(d.m1 + f * px, px * 8);
             if (s != LK_OK || d.hooks) break;
-            // without hooks only the non-zero tiles on road rows are written
+            // without hooks only the non-zero tiles on rows >= horizon - varsigma - 1 are written
             std::vector<uint8_t> nz((size_t)d.m_nty * d.m_ntx);
             CU(cudaMemcpy(nz.data(), d.m1_nz + f * nz.size(), nz.size(), cudaMemcpyDeviceToHost));
             double* m = (double*)buf.data();
             for (int v = 0; v < d.H; ++v)
                 for (int u = 0; u < d.W; ++u)
-                    if (v < rep.horizon || !nz[(v >> d.m_tile_shift) * d.m_ntx + (u / lkg::M_TW)])
+                    if (v < (int)rep.horizon - d.varsigma - 1 ||
+                        !nz[(v >> d.m_tile_shift) * d.m_ntx + (u / lkg::M_TW)])
                         m[(size_t)v * d.W + u] = 0.0;
             break;
         }

@@ -51,8 +51,21 @@ struct Dev {
     double sobel_s_star;  // smallest s with !(sqrt(s) < threshold): exact sqrt-free test
     float sobel_s_star_lo;  // largest float <= sobel_s_star (FP32 candidate screen)
     // inputs
-    const uint8_t* grey;
+    const uint8_t* grey;    // left grey (stereo) or the only grey
     const uint8_t* disp;
+    // stereo front end, stages 1-4 (LK_FLAG_STEREO; stereo.hpp)
+    int stereo;
+    int srho, tau, tr_lrc;  // block radius, search propagation bound, LRC tolerance
+    double sigma_floor;
+    const uint8_t* right;   // [B][H][W] right grey
+    double* sat;            // [B][4][H][W] integral images: left, left^2, right, right^2
+    double* mu_l;           // [B][H][W] block statistics (0 on the border)
+    double* sig_l;
+    double* mu_r;
+    double* sig_r;
+    uint8_t* disp_l;        // [B][H][W] SRP disparity, left / right reference
+    uint8_t* disp_r;
+    uint8_t* disp_out;      // the LRC result = the disparity input of stages 5-12
     // tables built on the host with the reference's libm
     const double* ws;       // [win*win] exp(-ds*inv_s2)
     const double* wr;       // [256][256] exp(-dr*dr*inv_r2)

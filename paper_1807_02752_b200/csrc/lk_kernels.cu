@@ -1173,9 +1173,9 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
     const int W = d.W, H = d.H, nu = d.nu, vs = d.varsigma;
     const int u0 = blockIdx.x * M_TW, v0 = blockIdx.y * tile_h;
     const int v_top = (int)d.rep[f].horizon, v_max = H - 1;
-    // w_g is zero above v_top, so m1 vanishes on rows < v_top - vs - 1. Without
-    // hooks only rows >= v_top are ever read (energy, threshold): skip the rest.
-    const int first_row = d.hooks ? 0 : v_top;
+    // w_g is zero above v_top, so m0 vanishes on rows < v_top - vs and m1 on
+    // rows < v_top - vs - 1: without hooks those rows are skipped (zero).
+    const int first_row = d.hooks ? 0 : max(0, v_top - vs - 1);
     if (v0 + tile_h <= first_row) return;
     if (d.hooks && v0 + tile_h <= v_top - vs - 1) {
         for (int i = threadIdx.x; i < tile_h * M_TW; i += blockDim.x) {
@@ -1704,7 +1704,7 @@ __global__ void k_finish(Dev d, int n) {
 namespace lkg {
 
 cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s,
-                            cudaEvent_t* stage_ev) {
+                            cudaEvent_t* stage_ev, bool mark_start) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cap);
     auto mark = [&](int stage) {  // event-record nodes when captured into the graph
@@ -1714,7 +1714,7 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
         else
             cudaEventRecord(stage_ev[stage], s);
     };
-    mark(0);
+    if (mark_start) mark(0);
     k_vdisparity<<<dim3((d.H + K1_ROWS - 1) / K1_ROWS, n), 256, K1_ROWS * d.D1 * 4, s>>>(
         d, lp.vhistT);
     mark(5);

@@ -64,7 +64,12 @@ struct LaunchPlan {
 // Enqueues stages 5-12 for n frames on stream s. stage_ev (13 events, may
 // be null) are recorded at the stage boundaries: [0] start, [k] end of stage k.
 cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s,
-                            cudaEvent_t* stage_ev);
+                            cudaEvent_t* stage_ev, bool mark_start = true);
+// Stages 1-4 (lk_stereo.cu): events [0] start, [1] stats, [2]/[3] both SRP views, [4] LRC.
+cudaError_t launch_stereo(const Dev& d, int n, cudaStream_t s, cudaEvent_t* stage_ev);
+cudaError_t configure_stereo(const Dev& d);
+size_t stereo_smem(const Dev& d);
+int stereo_launches();
 cudaError_t configure_kernels(const LaunchPlan& lp);
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all = 0);
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);

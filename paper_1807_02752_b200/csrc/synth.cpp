@@ -251,8 +251,8 @@ lk_status lk_synth_scene(const lk_scene_params* p, uint8_t* gl, uint8_t* gr, uin
     return synth_one(*p, gl, gr, dm, horizon);
 }
 
-lk_status lk_synth_batch(const lk_scene_params* params, int n, uint8_t* grey, uint8_t* disp,
-                         int threads) {
+lk_status lk_synth_stereo_batch(const lk_scene_params* params, int n, uint8_t* left,
+                                uint8_t* right, uint8_t* disp, int threads) {
     if (!params || n < 0) return LK_ERR_INVALID_ARGUMENT;
     if (threads < 1) threads = 1;
     std::atomic<int> next{0};
@@ -263,13 +263,18 @@ lk_status lk_synth_batch(const lk_scene_params* params, int n, uint8_t* grey, ui
             for (int i = next++; i < n; i = next++) {
                 const size_t off = static_cast<size_t>(i) * params[0].width * params[0].height;
                 if (params[i].width != params[0].width || params[i].height != params[0].height ||
-                    synth_one(params[i], grey ? grey + off : nullptr, nullptr,
+                    synth_one(params[i], left ? left + off : nullptr, right ? right + off : nullptr,
                               disp ? disp + off : nullptr, nullptr) != LK_OK)
                     bad = 1;
             }
         });
     for (auto& t : pool) t.join();
     return bad ? LK_ERR_INVALID_ARGUMENT : LK_OK;
+}
+
+lk_status lk_synth_batch(const lk_scene_params* params, int n, uint8_t* grey, uint8_t* disp,
+                         int threads) {
+    return lk_synth_stereo_batch(params, n, grey, nullptr, disp, threads);
 }
 
 }  // extern "C"

@@ -60,6 +60,10 @@ def library() -> C.CDLL:
     L.lk_fast_path_error.argtypes = [P, C.POINTER(C.c_double)]
     L.lk_synth_scene.argtypes = [C.POINTER(abi.LkSceneParams), P, P, P, C.POINTER(C.c_int32)]
     L.lk_synth_batch.argtypes = [C.POINTER(abi.LkSceneParams), I, P, P, I]
+    L.lk_synth_stereo_batch.argtypes = [C.POINTER(abi.LkSceneParams), I, P, P, P, I]
+    L.lk_run_stereo_batch.argtypes = [P, P, P, I, I, repp]
+    L.lk_stereo_inputs.argtypes = [P, C.POINTER(P), C.POINTER(P)]
+    L.lk_enqueue_stereo.argtypes = [P, I]
     L.lk_synth_last_error.restype = C.c_char_p
     L.lk_stage_name.restype = C.c_char_p
     _lib = L
@@ -101,12 +105,12 @@ class GpuPipeline:
 
     def __init__(self, width: int, height: int, config: abi.LkConfig | None = None,
                  max_batch: int = 1, device: int = 0, hooks: bool = False,
-                 graph: bool = True, exact: bool = False):
+                 graph: bool = True, exact: bool = False, stereo: bool = False):
         L = library()
         self.cfg = config if config is not None else default_config()
         self.width, self.height, self.max_batch = width, height, max_batch
         flags = (abi.LK_FLAG_HOOKS if hooks else 0) | (0 if graph else abi.LK_FLAG_NO_GRAPH) | \
-            (abi.LK_FLAG_EXACT if exact else 0)
+            (abi.LK_FLAG_EXACT if exact else 0) | (abi.LK_FLAG_STEREO if stereo else 0)
         h = C.c_void_p()
         _check(L.lk_create(C.byref(h), device, C.byref(self.cfg), width, height, max_batch,
                            flags))
@@ -148,6 +152,24 @@ class GpuPipeline:
         reps = (abi.LkFrameReport * n)()
         st = library().lk_run_batch(self._h, grey.ctypes.data, disparity.ctypes.data, n,
                                     abi.LK_MEM_HOST, reps)
+        if st not in (abi.LK_OK, abi.LK_ERR_FRAME):
+            _check(st)
+        self.reports = list(reps)
+        return self.reports
+
+    def run_stereo(self, left: np.ndarray, right: np.ndarray) -> list[abi.LkFrameReport]:
+        """Stages 1-12 (run_pipeline, pipeline.hpp:118-270) on u8 stereo pairs [n, H, W]."""
+        left = np.ascontiguousarray(left, np.uint8)
+        right = np.ascontiguousarray(right, np.uint8)
+        if left.ndim == 2:
+            left, right = left[None], right[None]
+        if left.shape != right.shape or left.shape[1:] != (self.height, self.width):
+            raise LanekitError(abi.LK_ERR_INVALID_ARGUMENT,
+                               "stage 1 (block statistics): stereo pair dimensions differ")
+        n = left.shape[0]
+        reps = (abi.LkFrameReport * n)()
+        st = library().lk_run_stereo_batch(self._h, left.ctypes.data, right.ctypes.data, n,
+                                           abi.LK_MEM_HOST, reps)
         if st not in (abi.LK_OK, abi.LK_ERR_FRAME):
             _check(st)
         self.reports = list(reps)
@@ -217,6 +239,43 @@ def run_pipeline_from_disparity(grey: np.ndarray, disparity: np.ndarray,
     if rep.status:
         raise stage_error(rep)
     return PipelineResult(pipe, 0)
+
+
+def run_pipeline(left: np.ndarray, right: np.ndarray, config: abi.LkConfig | None = None,
+                 device: int = 0, hooks: bool = True) -> PipelineResult:
+    """run_pipeline(left, right, cfg) (pipeline.hpp:118-270) on one u8 stereo pair;
+    raises StageError like the reference."""
+    cfg = config if config is not None else default_config()
+    validate_config(cfg)
+    if left.size == 0 or right.size == 0:
+        raise StageError(1, abi.STAGE_NAMES[0], "stage 1 (block statistics): empty input image")
+    if left.shape != right.shape:
+        raise StageError(1, abi.STAGE_NAMES[0],
+                         "stage 1 (block statistics): stereo pair dimensions differ")
+    H, W = left.shape
+    if W <= 2 * cfg.rho or H <= 2 * cfg.rho:
+        raise StageError(1, abi.STAGE_NAMES[0],
+                         "stage 1 (block statistics): image smaller than the matching block")
+    pipe = GpuPipeline(W, H, cfg, 1, device, hooks=hooks, stereo=True)
+    rep = pipe.run_stereo(left, right)[0]
+    if rep.status:
+        raise stage_error(rep)
+    return PipelineResult(pipe, 0)
+
+
+def synth_stereo_batch(params: Sequence[abi.LkSceneParams], threads: int = 8):
+    """Stereo pairs for a list of scenes: (left, right, true disparity) u8 [n, H, W]."""
+    L = library()
+    n = len(params)
+    H, W = params[0].height, params[0].width
+    left = np.zeros((n, H, W), np.uint8)
+    right = np.zeros_like(left)
+    disp = np.zeros_like(left)
+    arr = (abi.LkSceneParams * n)(*params)
+    if L.lk_synth_stereo_batch(arr, n, left.ctypes.data, right.ctypes.data, disp.ctypes.data,
+                               threads):
+        raise ValueError(L.lk_synth_last_error().decode())
+    return left, right, disp
 
 
 def synth_scene(p: abi.LkSceneParams):

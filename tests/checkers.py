@@ -1,6 +1,7 @@
 """TEST INFRASTRUCTURE: ctypes loaders for the CPU checkers under oracle/.
 
-- `Checker("oracle")` — oracle/liblk_oracle.so, the restatement of stages 5-12;
+- `Checker("oracle")` — oracle/liblk_oracle.so, the restatement of stages 1-4
+  (stereo) and 5-12;
 - `Checker("ref")`    — oracle/_ref/liblk_ref.so, the unmodified reference
   headers compiled against the Eigen stand-in (built only where
   /root/reference exists; prebuilt copies travel to the GPU box).
@@ -47,6 +48,8 @@ class Checker:
         f("run_batch").argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int,
                                    C.POINTER(abi.LkConfig), C.c_int,
                                    C.POINTER(abi.LkFrameReport)]
+        f("stereo").argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                C.c_int, C.c_double, _f64p, _f64p, _u8p, _u8p, _u8p]
         if kind == "ref":
             self.lib.lkref_gen_scene.argtypes = [
                 C.POINTER(abi.LkSceneParams), C.c_void_p, C.c_void_p, C.c_void_p,
@@ -70,6 +73,22 @@ class Checker:
 
     def _f(self, name):
         return getattr(self.lib, self.p + name)
+
+    def stereo(self, left: np.ndarray, right: np.ndarray, cfg: abi.LkConfig) -> dict:
+        """Stages 1-4 (pipeline.hpp:161-182) on one u8 pair: the PipelineResult
+        members stats_left (mu, sigma), disp_left, disp_right, disparity."""
+        H, W = left.shape
+        out = {"STATS_MU": np.zeros((H, W)), "STATS_SIGMA": np.zeros((H, W)),
+               "DISP_LEFT": np.zeros((H, W), np.uint8), "DISP_RIGHT": np.zeros((H, W), np.uint8),
+               "DISPARITY": np.zeros((H, W), np.uint8)}
+        rc = self._f("stereo")(np.ascontiguousarray(left, np.uint8),
+                               np.ascontiguousarray(right, np.uint8), W, H, cfg.rho, cfg.d_max,
+                               cfg.tau, cfg.tr_lrc, cfg.sigma_floor, out["STATS_MU"],
+                               out["STATS_SIGMA"], out["DISP_LEFT"], out["DISP_RIGHT"],
+                               out["DISPARITY"])
+        if rc:
+            raise ValueError("stereo: image smaller than the matching block")
+        return out
 
     def run(self, grey: np.ndarray, disp: np.ndarray, cfg: abi.LkConfig) -> "CheckerResult":
         H, W = grey.shape

@@ -1,0 +1,112 @@
+"""Stages 1-4 on the GPU (stereo pair in: the reference's run_pipeline) vs the
+compiled reference and the restatement, through the C-ABI. Every stage 1-4
+output is bit-exact (block statistics, both SRP maps, the LRC disparity), and
+stages 5-12 on top of it match the reference run on the reference's own
+disparity."""
+import numpy as np
+import pytest
+
+from paper_1807_02752_b200 import abi, lanekit, scenes
+from parity import compare_frame, compare_reports
+from test_stereo import _cfg, _small_pair
+
+pytestmark = pytest.mark.gpu
+
+STEREO_HOOKS = ["STATS_MU", "STATS_SIGMA", "DISP_LEFT", "DISP_RIGHT", "DISPARITY"]
+
+
+def _checker(oracle):
+    from checkers import Checker, ref_available
+
+    return Checker("ref") if ref_available() else oracle
+
+
+def _run(pipe_kw, left, right, cfg):
+    n, H, W = left.shape
+    pipe = lanekit.GpuPipeline(W, H, cfg, max_batch=n, stereo=True, **pipe_kw)
+    reps = pipe.run_stereo(left, right)
+    return pipe, reps
+
+
+def _compare(pipe, reps, left, right, cfg, chk, hooks):
+    problems = []
+    for i in range(left.shape[0]):
+        o = chk.stereo(left[i], right[i], cfg)
+        for k in STEREO_HOOKS:
+            g = pipe.stage(i, k)
+            if g.tobytes() != o[k].tobytes():
+                problems.append(f"frame {i}: {k} not bit-exact "
+                                f"({int((g != o[k]).sum())} of {g.size} differ)")
+        r = chk.run(left[i], o["DISPARITY"], cfg)
+        problems += [f"frame {i}: {x}" for x in compare_reports(reps[i], r.report)]
+        problems += [f"frame {i}: {x}" for x in
+                     compare_frame(lambda name: pipe.stage(i, name), r, hooks=hooks)]
+    return problems
+
+
+def test_stereo_small_frames(oracle):
+    pairs = [_small_pair(s) for s in (1, 2, 3, 4)]
+    left = np.stack([p[0] for p in pairs])
+    right = np.stack([p[1] for p in pairs])
+    cfg = _cfg(d_max=32)
+    pipe, reps = _run({}, left, right, cfg)
+    assert not (problems := _compare(pipe, reps, left, right, cfg, _checker(oracle), False)), \
+        "\n".join(problems)
+
+
+def test_stereo_kitti_size_with_hooks(oracle):
+    params = [scenes.probe_scene(5), scenes.batch_scene(3)]
+    left, right, _ = lanekit.synth_stereo_batch(params)
+    cfg = abi.default_config()
+    pipe, reps = _run({"hooks": True}, left, right, cfg)
+    assert not (problems := _compare(pipe, reps, left, right, cfg, _checker(oracle), True)), \
+        "\n".join(problems)
+    assert reps[0].status == 0 and reps[0].lane_count >= 1
+
+
+@pytest.mark.parametrize("kw", [dict(tau=0), dict(tau=3), dict(tr_lrc=0), dict(rho=2),
+                                dict(rho=5), dict(sigma_floor=0.05)])
+def test_stereo_config_variants(oracle, kw):
+    pairs = [_small_pair(s) for s in (4, 6)]
+    left = np.stack([p[0] for p in pairs])
+    right = np.stack([p[1] for p in pairs])
+    cfg = _cfg(d_max=32, **kw)
+    pipe, reps = _run({}, left, right, cfg)
+    assert not (problems := _compare(pipe, reps, left, right, cfg, _checker(oracle), False)), \
+        "\n".join(problems)
+
+
+def test_stereo_batch_pipelined_and_device_paths_agree(oracle):
+    """64 KITTI pairs: the host-fed pipelined path (8 ranges) and the
+    device-resident graph (4 branches) give identical reports and disparities,
+    and they match the reference on a sample."""
+    params = [scenes.batch_scene(i) for i in range(64)]
+    left, right, _ = lanekit.synth_stereo_batch(params)
+    cfg = abi.default_config()
+    pipe, reps = _run({}, left, right, cfg)
+    d_host = [pipe.stage(i, "DISPARITY").copy() for i in range(64)]
+    L = lanekit.library()
+    import ctypes as C
+    dl, dr = C.c_void_p(), C.c_void_p()
+    assert L.lk_stereo_inputs(pipe._h, C.byref(dl), C.byref(dr)) == 0
+    assert L.lk_enqueue_stereo(pipe._h, 64) == 0
+    reps2 = (abi.LkFrameReport * 64)()
+    L.lk_fetch_reports(pipe._h, reps2, 64)
+    for i in range(64):
+        assert bytes(reps[i]) == bytes(reps2[i]), i
+        assert np.array_equal(pipe.stage(i, "DISPARITY"), d_host[i]), i
+    chk = _checker(oracle)
+    for i in (0, 17, 63):
+        o = chk.stereo(left[i], right[i], cfg)
+        assert o["DISPARITY"].tobytes() == d_host[i].tobytes(), i
+
+
+def test_stereo_run_pipeline_api():
+    p = scenes.probe_scene(5)
+    left, right, _, _ = lanekit.synth_scene(p)
+    res = lanekit.run_pipeline(left, right, abi.default_config())
+    assert res.report.status == 0
+    assert res.stage("DISPARITY").shape == left.shape
+    with pytest.raises(lanekit.StageError) as e:
+        lanekit.run_pipeline(left[:5, :5], right[:5, :5], abi.default_config())
+    assert "image smaller than the matching block" in str(e.value)
