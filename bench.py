@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--config", default="kitti", choices=["kitti", "hires"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stereo", action="store_true",
+                    help="stereo pairs in: stages 1-12 (the reference's run_pipeline) instead "
+                         "of the north-star path (stages 5-12 on a given disparity)")
     return ap.parse_args()
 
 
@@ -68,11 +71,15 @@ def workload(cfg_name: str, batch: int):
             f"disparity, 2-4 curved lanes, non-flat road), stages 5-12 in one CUDA graph")
 
 
-def make_frames(scene_fn, n_pool: int, batch: int, seed0: int):
+def make_frames(scene_fn, n_pool: int, batch: int, seed0: int, stereo: bool = False):
+    """(grey, disparity) [batch, H, W], or (left, right) for stereo runs."""
     from paper_1807_02752_b200 import lanekit
 
     params = [scene_fn(seed0 + i) for i in range(n_pool)]
-    grey, disp = lanekit.synth_batch(params, threads=os.cpu_count() or 8)
+    if stereo:
+        grey, disp, _ = lanekit.synth_stereo_batch(params, threads=os.cpu_count() or 8)
+    else:
+        grey, disp = lanekit.synth_batch(params, threads=os.cpu_count() or 8)
     if n_pool < batch:
         reps = math.ceil(batch / n_pool)
         grey = np.concatenate([grey] * reps)[:batch]
@@ -140,7 +147,8 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def cpu_baseline(grey, disp, cfg, frames: int, impl_kind: str | None = None):
+def cpu_baseline(grey, disp, cfg, frames: int, impl_kind: str | None = None,
+                 stereo: bool = False):
     """Reference CPU pipeline on this host's cores, frame-parallel (one frame per
     worker thread, each frame single-threaded as cfg.threads=1 runs it)."""
     sys.path.insert(0, str(ROOT / "tests"))
@@ -151,8 +159,19 @@ def cpu_baseline(grey, disp, cfg, frames: int, impl_kind: str | None = None):
     cores = os.cpu_count() or 1
     n = min(frames, grey.shape[0])
     t0 = time.perf_counter()
-    reps = chk.run_batch(np.ascontiguousarray(grey[:n]), np.ascontiguousarray(disp[:n]), cfg,
-                         threads=cores)
+    if stereo and kind == "reference":  # run_pipeline on the pairs (stages 1-12)
+        from paper_1807_02752_b200 import abi
+
+        reps = (abi.LkFrameReport * n)()
+        chk.lib.lkref_run_stereo_batch.argtypes = [
+            C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(abi.LkConfig), C.c_int,
+            C.POINTER(abi.LkFrameReport)]
+        chk.lib.lkref_run_stereo_batch(np.ascontiguousarray(grey[:n]).ctypes.data,
+                                       np.ascontiguousarray(disp[:n]).ctypes.data, n,
+                                       grey.shape[2], grey.shape[1], C.byref(cfg), cores, reps)
+    else:
+        reps = chk.run_batch(np.ascontiguousarray(grey[:n]), np.ascontiguousarray(disp[:n]),
+                             cfg, threads=cores)
     dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{n} frames of the same workload, frame-parallel on {cores} host threads "
@@ -215,11 +234,17 @@ def run_ours(args):
     torch.cuda.set_device(local)
     scene_fn, cfg, W, H, B, desc = workload(args.config, args.batch)
     pool = args.pool or B
-    grey, disp = make_frames(scene_fn, pool, B, 1 + rank * pool)
+    stereo = args.stereo
+    if stereo:
+        desc = desc.replace("(grey + dense disparity", "(stereo pairs").replace(
+            "stages 5-12", "stages 1-12")
+    grey, disp = make_frames(scene_fn, pool, B, 1 + rank * pool, stereo)
     px = W * H
 
-    pipe = lanekit.GpuPipeline(W, H, cfg, max_batch=B, device=local)
+    pipe = lanekit.GpuPipeline(W, H, cfg, max_batch=B, device=local, stereo=stereo)
     L = lanekit.library()
+    run_fn = L.lk_run_stereo_batch if stereo else L.lk_run_batch
+    enq_fn = L.lk_enqueue_stereo if stereo else L.lk_enqueue
     h = pipe._h
     stream = torch.cuda.ExternalStream(L.lk_stream(h), device=local)
     dg, dd = C.c_void_p(), C.c_void_p()
@@ -232,14 +257,14 @@ def run_ours(args):
     C.memmove(hg, grey.ctypes.data, B * px)
     C.memmove(hd, disp.ctypes.data, B * px)
     reps = (abi.LkFrameReport * B)()
-    st = L.lk_run_batch(h, hg, hd, B, abi.LK_MEM_HOST, reps)
+    st = run_fn(h, hg, hd, B, abi.LK_MEM_HOST, reps)
     if st not in (abi.LK_OK, abi.LK_ERR_FRAME):
         raise RuntimeError(L.lk_last_error().decode())
     failed = sum(1 for r in reps if r.status)
 
     launches = pipe.launches_per_batch
     for _ in range(args.warmup):
-        L.lk_enqueue(h, B)
+        enq_fn(h, B)
     L.lk_synchronize(h)
     if world > 1:
         torch.distributed.barrier()
@@ -253,7 +278,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            L.lk_enqueue(h, B)
+            enq_fn(h, B)
             L.lk_stage_times(h, ms13)  # waits for this step; per-kernel events of this replay
             stage_acc += np.frombuffer(ms13, np.float32)
         e1.record(stream)
@@ -262,14 +287,14 @@ def run_ours(args):
     tf = L.lk_timed_frames(h) or B  # frames the stage events covered (range 0 of the graph)
     # ---- end to end through the public API: pinned host buffers in, reports out
     for _ in range(2):
-        L.lk_run_batch(h, hg, hd, B, abi.LK_MEM_HOST, reps)
+        run_fn(h, hg, hd, B, abi.LK_MEM_HOST, reps)
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
     e2_steps = max(3, args.steps // 4)
     torch.cuda.synchronize()
     e2.record(stream)
     for _ in range(e2_steps):
-        L.lk_run_batch(h, hg, hd, B, abi.LK_MEM_HOST, reps)
+        run_fn(h, hg, hd, B, abi.LK_MEM_HOST, reps)
     e3.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)
@@ -283,10 +308,11 @@ def run_ours(args):
     e2e_fps = world * B * e2_steps / (e2e_ms * 1e-3)
     stage_ms = stage_acc / args.steps
     # dominant kernel: the bilateral (stage 9 is exactly one launch)
-    dom = int(np.argmax(stage_ms[5:13])) + 5
+    first = 1 if stereo else 5
+    dom = int(np.argmax(stage_ms[first:13])) + first
     dom_ms = float(stage_ms[dom])
     hbm_peak, peak_src = measured_peaks()
-    bytes_per_frame = px * 2  # u8 grey + u8 disparity
+    bytes_per_frame = px * 2  # u8 grey + u8 disparity, or u8 left + right
     achieved = bytes_per_frame * tf / (dom_ms * 1e-3) / 1e9
     win = 2 * ((cfg.bf_window - 1) // 2) + 1
     taps = win * win * px * tf  # nominal range-weight evaluations of one launch
@@ -306,7 +332,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "gpu_launches": launches * args.steps,
         "failed_frames": failed,
-        "stage_ms": {str(k): round(float(stage_ms[k]), 4) for k in (5, 6, 7, 8, 9, 10, 11, 12)},
+        "stage_ms": {str(k): round(float(stage_ms[k]), 4) for k in range(first, 13)},
         "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": 2 * B * px,
                 "d2h_bytes_per_step": B * C.sizeof(abi.LkFrameReport),
                 "api": "lk_run_batch(pinned host grey+disparity, LK_MEM_HOST) -> reports"},
@@ -314,11 +340,13 @@ def run_ours(args):
             "bound": "hbm", "kernel": f"stage {dom} ({abi.STAGE_NAMES[dom - 1]})",
             "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
             "traffic": None, "peak_source": peak_src,
-            "algorithmic_bytes": f"{bytes_per_frame} B/frame (u8 grey + u8 disparity) x {tf}",
+            "algorithmic_bytes": f"{bytes_per_frame} B/frame (u8 "
+                                 f"{'left + right' if stereo else 'grey + disparity'}) x {tf}",
             "frames_per_launch": tf,
             "pipeline_frac_of_hbm_roofline": pipe_fps_hbm,
             "compute": {
-                "kernel": "k_bilateral_fast (certified FP32 approximation, DESIGN.md §3)",
+                "kernel": "k_bilateral_fast (certified FP32 approximation, DESIGN.md §3)"
+                          if dom == 9 else f"stage {dom} kernels (see stage_ms)",
                 "taps_per_s": taps / (dom_ms * 1e-3) if dom == 9 else None,
                 "mufu_ex2_only_ceiling_per_s": xu_ex2_peak,
                 "note": "range weights split between MUFU ex2 (1 of 5 tap pairs + the last "
@@ -338,7 +366,7 @@ def run_ours(args):
         except Exception:
             pass
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb, _ = cpu_baseline(grey, disp, cfg, frames=2 * (os.cpu_count() or 8))
+        cb, _ = cpu_baseline(grey, disp, cfg, frames=2 * (os.cpu_count() or 8), stereo=stereo)
         line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line), flush=True)

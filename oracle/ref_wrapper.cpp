@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lanekit/config.hpp"
@@ -330,6 +331,33 @@ int lkref_stereo(const uint8_t* left, const uint8_t* right, int W, int H, int rh
     } catch (const Error&) {
         return 1;
     }
+}
+
+// run_pipeline on stereo pairs (stages 1-4 then 5-12, pipeline.hpp:118-270),
+// frame-parallel on `threads` host threads: the CPU baseline of the stereo bench.
+int lkref_run_stereo_batch(const uint8_t* left, const uint8_t* right, int n, int W, int H,
+                           const lk_config* cfg, int threads, lk_frame_report* reps) {
+    if (threads < 1) threads = 1;
+    const size_t frame = static_cast<size_t>(W) * H;
+    std::vector<std::thread> pool;
+    std::atomic<int> next{0};
+    auto worker = [&] {
+        orc::Result r;
+        std::vector<uint8_t> disp(frame);
+        for (int i = next++; i < n; i = next++) {
+            lkref_stereo(left + frame * i, right + frame * i, W, H, cfg->rho, cfg->d_max, cfg->tau,
+                         cfg->tr_lrc, cfg->sigma_floor, nullptr, nullptr, nullptr, nullptr,
+                         disp.data());
+            compute_frame(left + frame * i, disp.data(), W, H, *cfg, r);
+            if (reps) reps[i] = r.rep;
+        }
+    };
+    for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    int failed = 0;
+    if (reps)
+        for (int i = 0; i < n; ++i) failed += reps[i].status != 0;
+    return failed;
 }
 
 }  // extern "C"

@@ -22,6 +22,7 @@ namespace lkg {
 // the previous group's last row. The recurrence and its rounding are the
 // reference's, element for element.
 __global__ void __launch_bounds__(128) k_integral(Dev d) {
+    extern __shared__ double sh_int[];  // [4 warps][W] last row of the previous group
     __shared__ double s_val[256];
     const int f = blockIdx.x;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) s_val[i] = d.val[i];
@@ -31,29 +32,40 @@ __global__ void __launch_bounds__(128) k_integral(Dev d) {
     const bool sq = warp & 1;  // stats of x^2 (stereo.hpp:45)
     const uint8_t* img = (warp >= 2 ? d.right : d.grey) + (size_t)f * d.px;
     double* out = d.sat + ((size_t)f * 4 + warp) * d.px;
+    double* last = sh_int + (size_t)warp * W;  // row 32g - 1, kept on chip for lane 0
     for (int g = 0; g * 32 < H; ++g) {
-        __syncwarp();  // the previous group's rows are visible to lane 0
+        __syncwarp();  // lane 31's writes of the previous group are visible to lane 0
         const int v = g * 32 + lane;
         const bool row_ok = v < H;
-        const double* above = out + (size_t)(v - 1) * W;  // lane 0 only
+        const uint8_t* irow = img + (size_t)(row_ok ? v : 0) * W;
         double mine1 = 0.0, mine2 = 0.0;  // my results of the last two steps
+        int k_next = (row_ok && lane == 0) ? irow[0] : 0;  // pixel of the next step
+        // lane 0: last[u] prefetched one step ahead; last[u-1] is the previous step's
+        double above_u = (v > 0 && lane == 0) ? last[0] : 0.0, above_prev = 0.0;
         for (int t = 0; t < W + 31; ++t) {
             const int u = t - lane;
+            const bool act = row_ok && u >= 0 && u < W;
+            const int k = k_next;
+            if (row_ok && u + 1 >= 0 && u + 1 < W) k_next = irow[u + 1];  // prefetch
             double up = __shfl_up_sync(0xffffffffu, mine1, 1);    // in(u, v-1)
             double diag = __shfl_up_sync(0xffffffffu, mine2, 1);  // in(u-1, v-1)
-            if (lane == 0) {
-                up = (v > 0 && u >= 0 && u < W) ? above[u] : 0.0;
-                diag = (v > 0 && u >= 1 && u <= W) ? above[u - 1] : 0.0;
+            if (lane == 0) {  // the row above comes from the previous group (u = t >= 0)
+                diag = above_prev;                                  // last[u-1] (0 at u = 0)
+                up = (v > 0 && u < W) ? above_u : 0.0;              // last[u]
+                above_prev = up;
+                above_u = (v > 0 && u + 1 < W) ? last[u + 1] : 0.0;
             }
             double val = 0.0;
-            if (row_ok && u >= 0 && u < W) {
-                double x = s_val[img[(size_t)v * W + u]];
+            if (act) {
+                double x = s_val[k];
                 if (sq) x = x * x;
                 val = ((up + mine1) - diag) + x;  // mine1 = in(u-1, v)
                 out[(size_t)v * W + u] = val;
             }
             mine2 = mine1;
             mine1 = val;
+            // lane 31 hands its row to the next group's lane 0 (read after __syncwarp)
+            if (lane == 31 && act) last[u] = val;
         }
     }
 }
@@ -235,7 +247,8 @@ __global__ void __launch_bounds__(256) k_lrc(Dev d) {
 size_t stereo_smem(const Dev& d) { return (size_t)(2 * d.srho + 1) * d.W * 8 + 2 * (size_t)d.W; }
 
 cudaError_t configure_stereo(const Dev& d) {
-    cudaError_t e = cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_integral, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)((size_t)4 * d.W * 8));
     for (auto fn : {k_srp<1>, k_srp<2>, k_srp<3>, k_srp<4>, k_srp<5>})
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -256,7 +269,7 @@ cudaError_t launch_stereo(const Dev& d, int n, cudaStream_t s, cudaEvent_t* ev) 
             cudaEventRecord(ev[k], s);
     };
     mark(0);
-    k_integral<<<n, 128, 0, s>>>(d);
+    k_integral<<<n, 128, (size_t)4 * d.W * 8, s>>>(d);
     k_block_stats<<<dim3((d.W + 255) / 256, d.H, n), 256, 0, s>>>(d);
     mark(1);
     const dim3 g(n, 2);  // both reference views concurrently
