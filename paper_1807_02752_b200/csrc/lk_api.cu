@@ -79,9 +79,9 @@ const char* config_problem(const lk_config& c) {
 }
 
 constexpr int kMaxIter = 200;  // pipeline.hpp:198, 244
-constexpr int kMaxBranches = 8;       // concurrent frame ranges (streams) per batch
+constexpr int kMaxBranches = 16;      // concurrent frame ranges (streams) per batch
 constexpr int kMinBranchFrames = 16;  // smallest range worth a branch
-constexpr int kH2dChunksDefault = 8;  // host-fed batches: copy/compute pipeline depth
+constexpr int kH2dChunksDefault = 12; // host-fed batches: copy/compute pipeline depth
 constexpr int kBranchesDefault = 4;   // device-resident batches: concurrent frame ranges
 constexpr int kFastTableDefault = 21;  // tap pairs of the fast bilateral served by the range table
 
