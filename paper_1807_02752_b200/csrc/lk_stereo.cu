@@ -106,55 +106,136 @@ __global__ void __launch_bounds__(256) k_block_stats(Dev d) {
 // ---- stages 2/3: match_srp (stereo.hpp:157-196) for one (frame, view)
 //
 // Rows run bottom to top inside one CTA (each row's search ranges come from
-// the row below). The 2*rho+1 rows of the OTHER image that the current row's
-// blocks touch live in shared memory as doubles (a ring indexed by row mod
-// 2*rho+1); the reference block of a pixel is loaded once into registers and
-// every candidate's 49-term dot product accumulates y-major / x-minor in the
-// reference's order. Cost: (dot - n*mu_l*mu_r) / (n*sl*sr) with the LEFT
-// block's statistics first (ncc_cost, stereo.hpp:67-84); the best is the
-// highest cost, smallest d on ties (ascending candidates, strict '>').
+// the row below). Shared memory holds the 2*rho+1 grey rows of BOTH images
+// that the current row's blocks touch (u8 rings indexed by row mod 2*rho+1)
+// and the row's block statistics.
+//
+// Certified integer correlation. The reference's dot product is a sequential
+// FP64 sum of 49 rounded products of rounded k/255 values; the exact integer
+// K = sum k_l * k_r (DP4A on packed bytes) gives dot ~ x = K / 65025 with
+// |dot_ref - x| <= 49 * 3u + 48 * 49u + 2u < 2700u (u = 2^-53, every term
+// <= 1; x carries two roundings). A = n mu_l mu_r and B = n sl sr are
+// evaluated exactly as the reference does, and c~ = (x - A) * fl(1/B) is
+// within a few u|c| of fl(fl(x - A) / B), so
+//   |c_ref - c~| <= (2700u + 2u |x - A|) / B + 6u (|c~| + 1) =: E
+// (covered with slack below). The candidate with the best c~ (smallest d on
+// ties) is certified when every other candidate's c~ + E lies below its
+// c~ - E: those cannot reach the reference's best cost, not even tie it.
+// Otherwise every candidate is re-evaluated with the reference's FP64 dot in
+// its exact order and compared with its exact rule (ascending d, '>').
+template <int RHO>
+__device__ __forceinline__ double exact_dot(const uint8_t* rr, const uint8_t* ro, int W, int v,
+                                            int ucol_ref, int ucol_oth, bool ref_is_left,
+                                            const double* val) {
+    constexpr int B = 2 * RHO + 1, RB = B + 1;
+    double dot = 0.0;
+    for (int y = 0; y < B; ++y) {
+        const int slot = ((v + y - RHO) % RB) * W;
+        for (int x = 0; x < B; ++x) {
+            const double a = __ldg(val + rr[slot + ucol_ref - RHO + x]);
+            const double b = __ldg(val + ro[slot + ucol_oth - RHO + x]);
+            dot += ref_is_left ? a * b : b * a;  // pl[x] * pr[x] (stereo.hpp:77-81)
+        }
+    }
+    return dot;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// 4 bytes of a u8 row starting at byte offset o (any alignment), little endian
+__device__ __forceinline__ unsigned bytes4(const uint8_t* row, int o) {
+    const unsigned* w = reinterpret_cast<const unsigned*>(row + (o & ~3));
+    return __funnelshift_r(w[0], w[1], (o & 3) * 8);
+}
+
 template <int RHO>
 __global__ void __launch_bounds__(256) k_srp(Dev d) {
     constexpr int B = 2 * RHO + 1;
+    constexpr int RB = B + 1;        // ring slots: the block rows + the prefetched row
+    constexpr int NW = (B + 3) / 4;  // packed words per block row
+    static_assert(B <= 12, "block rows are packed into at most 3 words");
     extern __shared__ double sh_srp[];
     const int f = blockIdx.x, view = blockIdx.y;  // 0: left reference, 1: right
     const int W = d.W, H = d.H;
-    double* ring = sh_srp;                              // [B][W]
-    uint8_t* drow = (uint8_t*)(ring + (size_t)B * W);   // [2][W] disparity of rows v+1, v
+    const int WP = (W + 16 + 3) & ~3;         // padded u8 row pitch (word reads past the end)
+    double* sbuf = sh_srp;                    // [2][4][W] statistics of rows v (and v-1, prefetched)
+    uint8_t* rr = (uint8_t*)(sbuf + (size_t)8 * W);  // [RB][WP] reference-image rows
+    uint8_t* ro = rr + (size_t)RB * WP;       // [RB][WP] other-image rows
+    uint8_t* drow = ro + (size_t)RB * WP;     // [2][W] disparity of rows v+1, v
     const size_t fo = (size_t)f * d.px;
     const uint8_t* ref = (view ? d.right : d.grey) + fo;
     const uint8_t* oth = (view ? d.grey : d.right) + fo;
-    const double* ref_sig = (view ? d.sig_r : d.sig_l) + fo;
-    const double* oth_sig = (view ? d.sig_l : d.sig_r) + fo;
-    const double* mu_l = d.mu_l + fo;
-    const double* mu_r = d.mu_r + fo;
-    const double* sg_l = d.sig_l + fo;
-    const double* sg_r = d.sig_r + fo;
     uint8_t* out = (view ? d.disp_r : d.disp_l) + fo;
     const double* val = d.val;
     const double n = (double)B * (double)B;
     const double floor_ = d.sigma_floor;
     const int d_min = 0, d_max = d.d_max, tau = d.tau;
     const int v_bottom = H - 1 - RHO;
-    // rows never matched stay 0 (DisparityMap disp(w, h, 0))
+    constexpr double kU = 1.1102230246251565e-16;  // 2^-53
     for (size_t i = threadIdx.x; i < (size_t)W * RHO; i += blockDim.x) {
-        out[i] = 0;
+        out[i] = 0;  // rows never matched stay 0 (DisparityMap disp(w, h, 0))
         out[(size_t)(H - RHO) * W + i] = 0;
     }
-    auto load_row = [&](int y) {  // other-image row y into its ring slot
-        double* dst = ring + (size_t)(y % B) * W;
-        const uint8_t* src = oth + (size_t)y * W;
-        for (int u = threadIdx.x; u < W; u += blockDim.x) dst[u] = __ldg(val + src[u]);
+    for (int i = threadIdx.x; i < 2 * RB * WP; i += blockDim.x) rr[i] = 0;  // pads read as 0
+    __syncthreads();
+    auto load_rows = [&](int y) {  // grey row y of both images into its ring slot
+        uint8_t* a = rr + (size_t)(y % RB) * WP;
+        uint8_t* b = ro + (size_t)(y % RB) * WP;
+        const uint8_t* sa = ref + (size_t)y * W;
+        const uint8_t* sb = oth + (size_t)y * W;
+        for (int u = threadIdx.x; u < W; u += blockDim.x) {
+            a[u] = sa[u];
+            b[u] = sb[u];
+        }
     };
-    for (int y = v_bottom - RHO; y <= v_bottom + RHO; ++y) load_row(y);
+    auto fetch_stats = [&](int v) {  // row v's four statistics, asynchronously
+        double* dst = sbuf + (size_t)(v & 1) * 4 * W;
+        const size_t i0 = fo + (size_t)v * W;
+        for (int u = threadIdx.x; u < W; u += blockDim.x) {
+            cp_async8(dst + u, d.mu_l + i0 + u);
+            cp_async8(dst + W + u, d.mu_r + i0 + u);
+            cp_async8(dst + 2 * W + u, d.sig_l + i0 + u);
+            cp_async8(dst + 3 * W + u, d.sig_r + i0 + u);
+        }
+    };
+    for (int y = v_bottom - RHO; y <= v_bottom + RHO; ++y) load_rows(y);
+    fetch_stats(v_bottom);
+    cp_async_wait_all();
+    __syncthreads();
+    constexpr int PF = 8;  // prefetched grey bytes per thread
+    const bool reg_pf = W <= PF * (int)blockDim.x;  // wider rows load at the end of the row
     for (int v = v_bottom; v >= RHO; --v) {
-        if (v < v_bottom) load_row(v - RHO);
-        __syncthreads();
+        // prefetch row v-1's statistics (async) and grey row v-1-RHO (registers)
+        const bool more = v - 1 >= RHO;
+        uint8_t pa[PF], pb[PF];
+        if (more) fetch_stats(v - 1);
+        if (more && reg_pf) {
+            const uint8_t* sa = ref + (size_t)(v - 1 - RHO) * W;
+            const uint8_t* sb = oth + (size_t)(v - 1 - RHO) * W;
+#pragma unroll
+            for (int k = 0; k < PF; ++k) {
+                const int u = threadIdx.x + k * blockDim.x;
+                pa[k] = u < W ? sa[u] : 0;
+                pb[k] = u < W ? sb[u] : 0;
+            }
+        }
+        const double* s_mul = sbuf + (size_t)(v & 1) * 4 * W;
+        const double* s_mur = s_mul + W;
+        const double* s_sgl = s_mur + W;
+        const double* s_sgr = s_sgl + W;
+        const double* ref_sg = view ? s_sgr : s_sgl;
+        const double* oth_sg = view ? s_sgl : s_sgr;
         uint8_t* cur = drow + (size_t)(v & 1) * W;
         const uint8_t* below = drow + (size_t)((v + 1) & 1) * W;
         for (int u = threadIdx.x; u < W; u += blockDim.x) {
             int res = 0;
-            if (u >= RHO && u < W - RHO && !(ref_sig[(size_t)v * W + u] < floor_)) {
+            if (u >= RHO && u < W - RHO && !(ref_sg[u] < floor_)) {
                 // search ranges (SearchRanges, stereo.hpp:89-112): up to three
                 // clamped intervals, iterated ascending without repeats
                 int lo[3], hi[3], cnt = 0;
@@ -176,8 +257,7 @@ __global__ void __launch_bounds__(256) k_srp(Dev d) {
                     }
                     if (cnt == 0) add(d_min, d_max);  // every interval clamped away
                 }
-                // std::sort of (lo, hi) pairs
-                for (int a = 1; a < cnt; ++a)
+                for (int a = 1; a < cnt; ++a)  // std::sort of (lo, hi) pairs
                     for (int b = a; b > 0 && (lo[b] < lo[b - 1] ||
                                               (lo[b] == lo[b - 1] && hi[b] < hi[b - 1]));
                          --b) {
@@ -187,42 +267,110 @@ __global__ void __launch_bounds__(256) k_srp(Dev d) {
                         lo[b - 1] = tl;
                         hi[b - 1] = th;
                     }
-                double rb[B][B];  // the reference block
+                // the reference block, packed (bytes past the block are zero)
+                unsigned rw[B][NW];
 #pragma unroll
-                for (int y = 0; y < B; ++y)
+                for (int y = 0; y < B; ++y) {
+                    const uint8_t* row = rr + (size_t)((v + y - RHO) % RB) * WP;
 #pragma unroll
-                    for (int x = 0; x < B; ++x)
-                        rb[y][x] = __ldg(val + ref[(size_t)(v + y - RHO) * W + u - RHO + x]);
-                double best_cost = 0.0;
+                    for (int k = 0; k < NW; ++k) {
+                        unsigned w = bytes4(row, u - RHO + 4 * k);
+                        const int keep = B - 4 * k;  // bytes of this word inside the block
+                        if (keep < 4) w &= (1u << (8 * keep)) - 1u;
+                        rw[y][k] = w;
+                    }
+                }
+                // approximate costs: the best (smallest d on ties) and M, the
+                // largest c~ + E over every other candidate (including bests it
+                // displaced). Certified iff M < best_c - best_e.
+                double best_c = 0.0, best_e = 0.0, M = -1e300;
                 int best_d = -1;
                 int next = INT_MIN;
+                const double mu_ref = view ? s_mur[u] : s_mul[u];
+                const double sg_ref = view ? s_sgr[u] : s_sgl[u];
                 for (int iv = 0; iv < cnt; ++iv) {
                     for (int dd = max(lo[iv], next); dd <= hi[iv]; ++dd) {
                         const int uo = view ? u + dd : u - dd;
                         if (uo < RHO || uo >= W - RHO) continue;
-                        if (oth_sig[(size_t)v * W + uo] < floor_) continue;
-                        double dot = 0.0;
+                        if (oth_sg[uo] < floor_) continue;
+                        unsigned K = 0;
 #pragma unroll
                         for (int y = 0; y < B; ++y) {
-                            const double* o = ring + (size_t)((v + y - RHO) % B) * W + uo - RHO;
+                            const uint8_t* row = ro + (size_t)((v + y - RHO) % RB) * WP;
+                            const int o = uo - RHO;
+                            const unsigned* w = reinterpret_cast<const unsigned*>(row + (o & ~3));
+                            const int sh = (o & 3) * 8;
+                            unsigned wd[NW + 1];
 #pragma unroll
-                            for (int x = 0; x < B; ++x) dot += rb[y][x] * o[x];
+                            for (int k = 0; k <= NW; ++k) wd[k] = w[k];
+#pragma unroll
+                            for (int k = 0; k < NW; ++k)
+                                K = __dp4a(rw[y][k], __funnelshift_r(wd[k], wd[k + 1], sh), K);
                         }
-                        const int ul = view ? uo : u, ur = view ? u : uo;
-                        const size_t il = (size_t)v * W + ul, ir = (size_t)v * W + ur;
-                        const double c = (dot - n * mu_l[il] * mu_r[ir]) / (n * sg_l[il] * sg_r[ir]);
-                        if (best_d < 0 || c > best_cost) {
-                            best_cost = c;
+                        // A and B in the reference's order: n * (left stats) * (right stats)
+                        const double mu_o = view ? s_mul[uo] : s_mur[uo];
+                        const double sg_o = view ? s_sgl[uo] : s_sgr[uo];
+                        const double A = view ? n * mu_o * mu_ref : n * mu_ref * mu_o;
+                        const double Bn = view ? n * sg_o * sg_ref : n * sg_ref * sg_o;
+                        const double ib = 1.0 / Bn;
+                        const double x = (double)K * (1.0 / 65025.0);
+                        const double num = x - A;
+                        const double c = num * ib;  // within 4u|c| of fl(fl(x - A) / B)
+                        const double e = 1.01 * ((2700.0 * kU + 2.0 * kU * fabs(num)) * ib +
+                                                 6.0 * kU * (fabs(c) + 1.0)) + 1e-300;
+                        if (best_d < 0 || c > best_c) {
+                            if (best_d >= 0) M = fmax(M, best_c + best_e);
+                            best_c = c;
+                            best_e = e;
                             best_d = dd;
+                        } else {
+                            M = fmax(M, c + e);
                         }
                     }
                     next = max(next, hi[iv] + 1);
+                }
+                if (best_d >= 0 && !(M < best_c - best_e)) {
+                    // ambiguous (rare): the reference's loop verbatim (stereo.hpp:124-144)
+                    double bc = 0.0;
+                    int bd = -1;
+                    next = INT_MIN;
+                    for (int iv = 0; iv < cnt; ++iv) {
+                        for (int dd = max(lo[iv], next); dd <= hi[iv]; ++dd) {
+                            const int uo = view ? u + dd : u - dd;
+                            if (uo < RHO || uo >= W - RHO) continue;
+                            if (oth_sg[uo] < floor_) continue;
+                            const double dot = exact_dot<RHO>(rr, ro, WP, v, u, uo, view == 0, val);
+                            const int ul = view ? uo : u, ur = view ? u : uo;
+                            const double c = (dot - n * s_mul[ul] * s_mur[ur]) /
+                                             (n * s_sgl[ul] * s_sgr[ur]);
+                            if (bd < 0 || c > bc) {
+                                bc = c;
+                                bd = dd;
+                            }
+                        }
+                        next = max(next, hi[iv] + 1);
+                    }
+                    best_d = bd;
                 }
                 res = best_d < 0 ? 0 : best_d;
             }
             cur[u] = (uint8_t)res;
             out[(size_t)v * W + u] = (uint8_t)res;
         }
+        if (more && !reg_pf) load_rows(v - 1 - RHO);
+        if (more && reg_pf) {
+            uint8_t* a = rr + (size_t)((v - 1 - RHO) % RB) * WP;
+            uint8_t* b = ro + (size_t)((v - 1 - RHO) % RB) * WP;
+#pragma unroll
+            for (int k = 0; k < PF; ++k) {
+                const int u = threadIdx.x + k * blockDim.x;
+                if (u < W) {
+                    a[u] = pa[k];
+                    b[u] = pb[k];
+                }
+            }
+        }
+        cp_async_wait_all();
         __syncthreads();
     }
 }
@@ -244,7 +392,10 @@ __global__ void __launch_bounds__(256) k_lrc(Dev d) {
     }
 }
 
-size_t stereo_smem(const Dev& d) { return (size_t)(2 * d.srho + 1) * d.W * 8 + 2 * (size_t)d.W; }
+size_t stereo_smem(const Dev& d) {
+    const size_t wp = (size_t)((d.W + 16 + 3) & ~3);
+    return (size_t)8 * d.W * 8 + 2 * (size_t)(2 * d.srho + 2) * wp + 2 * (size_t)d.W;
+}
 
 cudaError_t configure_stereo(const Dev& d) {
     cudaError_t e = cudaFuncSetAttribute(k_integral, cudaFuncAttributeMaxDynamicSharedMemorySize,
