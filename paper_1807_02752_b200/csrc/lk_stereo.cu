@@ -39,33 +39,48 @@ __global__ void __launch_bounds__(128) k_integral(Dev d) {
         const bool row_ok = v < H;
         const uint8_t* irow = img + (size_t)(row_ok ? v : 0) * W;
         double mine1 = 0.0, mine2 = 0.0;  // my results of the last two steps
-        int k_next = (row_ok && lane == 0) ? irow[0] : 0;  // pixel of the next step
         // lane 0: last[u] prefetched one step ahead; last[u-1] is the previous step's
         double above_u = (v > 0 && lane == 0) ? last[0] : 0.0, above_prev = 0.0;
-        for (int t = 0; t < W + 31; ++t) {
-            const int u = t - lane;
-            const bool act = row_ok && u >= 0 && u < W;
-            const int k = k_next;
-            if (row_ok && u + 1 >= 0 && u + 1 < W) k_next = irow[u + 1];  // prefetch
-            double up = __shfl_up_sync(0xffffffffu, mine1, 1);    // in(u, v-1)
-            double diag = __shfl_up_sync(0xffffffffu, mine2, 1);  // in(u-1, v-1)
-            if (lane == 0) {  // the row above comes from the previous group (u = t >= 0)
-                diag = above_prev;                                  // last[u-1] (0 at u = 0)
-                up = (v > 0 && u < W) ? above_u : 0.0;              // last[u]
-                above_prev = up;
-                above_u = (v > 0 && u + 1 < W) ? last[u + 1] : 0.0;
+        // input bytes in blocks of PB steps, loaded one block ahead (L2 latency)
+        constexpr int PB = 8;
+        auto load_block = [&](int t0, int (&kb)[PB]) {
+#pragma unroll
+            for (int j = 0; j < PB; ++j) {
+                const int u = t0 + j - lane;
+                kb[j] = (row_ok && u >= 0 && u < W) ? irow[u] : 0;
             }
-            double val = 0.0;
-            if (act) {
-                double x = s_val[k];
-                if (sq) x = x * x;
-                val = ((up + mine1) - diag) + x;  // mine1 = in(u-1, v)
-                out[(size_t)v * W + u] = val;
+        };
+        int kb_cur[PB], kb_nxt[PB];
+        load_block(0, kb_cur);
+        for (int t0 = 0; t0 < W + 31; t0 += PB) {
+            load_block(t0 + PB, kb_nxt);
+#pragma unroll
+            for (int j = 0; j < PB; ++j) {
+                const int t = t0 + j;
+                const int u = t - lane;
+                double up = __shfl_up_sync(0xffffffffu, mine1, 1);    // in(u, v-1)
+                double diag = __shfl_up_sync(0xffffffffu, mine2, 1);  // in(u-1, v-1)
+                if (lane == 0) {  // the row above comes from the previous group (u = t >= 0)
+                    diag = above_prev;                                  // last[u-1] (0 at u = 0)
+                    up = (v > 0 && u < W) ? above_u : 0.0;              // last[u]
+                    above_prev = up;
+                    above_u = (v > 0 && u + 1 < W) ? last[u + 1] : 0.0;
+                }
+                double val = 0.0;
+                const bool act = row_ok && u >= 0 && u < W;
+                if (act) {
+                    double x = s_val[kb_cur[j]];
+                    if (sq) x = x * x;
+                    val = ((up + mine1) - diag) + x;  // mine1 = in(u-1, v)
+                    out[(size_t)v * W + u] = val;
+                }
+                mine2 = mine1;
+                mine1 = val;
+                // lane 31 hands its row to the next group's lane 0 (read after __syncwarp)
+                if (lane == 31 && act) last[u] = val;
             }
-            mine2 = mine1;
-            mine1 = val;
-            // lane 31 hands its row to the next group's lane 0 (read after __syncwarp)
-            if (lane == 31 && act) last[u] = val;
+#pragma unroll
+            for (int j = 0; j < PB; ++j) kb_cur[j] = kb_nxt[j];
         }
     }
 }
@@ -392,6 +407,8 @@ __global__ void __launch_bounds__(256) k_lrc(Dev d) {
     }
 }
 
+size_t integral_smem(const Dev& d) { return (size_t)4 * d.W * 8; }
+
 size_t stereo_smem(const Dev& d) {
     const size_t wp = (size_t)((d.W + 16 + 3) & ~3);
     return (size_t)8 * d.W * 8 + 2 * (size_t)(2 * d.srho + 2) * wp + 2 * (size_t)d.W;
@@ -399,7 +416,7 @@ size_t stereo_smem(const Dev& d) {
 
 cudaError_t configure_stereo(const Dev& d) {
     cudaError_t e = cudaFuncSetAttribute(k_integral, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)((size_t)4 * d.W * 8));
+                                         (int)integral_smem(d));
     for (auto fn : {k_srp<1>, k_srp<2>, k_srp<3>, k_srp<4>, k_srp<5>})
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -420,7 +437,7 @@ cudaError_t launch_stereo(const Dev& d, int n, cudaStream_t s, cudaEvent_t* ev) 
             cudaEventRecord(ev[k], s);
     };
     mark(0);
-    k_integral<<<n, 128, (size_t)4 * d.W * 8, s>>>(d);
+    k_integral<<<n, 128, integral_smem(d), s>>>(d);
     k_block_stats<<<dim3((d.W + 255) / 256, d.H, n), 256, 0, s>>>(d);
     mark(1);
     const dim3 g(n, 2);  // both reference views concurrently
