@@ -110,3 +110,24 @@ def test_stereo_run_pipeline_api():
     with pytest.raises(lanekit.StageError) as e:
         lanekit.run_pipeline(left[:5, :5], right[:5, :5], abi.default_config())
     assert "image smaller than the matching block" in str(e.value)
+
+
+def test_stereo_exact_ties_take_the_fp64_path(oracle):
+    """Identical pairs (NCC = +1 at d = 0 and wherever blocks repeat) and a
+    horizontally periodic texture (exact ties every period) cannot be
+    certified by the integer costs: the exact FP64 fallback must reproduce the
+    reference's tie rule (smallest d)."""
+    left, _, _ = _small_pair(3)
+    rng = np.random.default_rng(7)
+    period = np.tile(rng.integers(0, 256, (120, 8), dtype=np.uint8), (1, 40))  # 120 x 320
+    shifted = np.roll(period, -5, axis=1)
+    L = np.stack([left, period])
+    R = np.stack([left, shifted])
+    cfg = _cfg(d_max=32)
+    pipe, reps = _run({}, L, R, cfg)
+    chk = _checker(oracle)
+    for i in range(2):
+        o = chk.stereo(L[i], R[i], cfg)
+        for k in STEREO_HOOKS:
+            assert pipe.stage(i, k).tobytes() == o[k].tobytes(), (i, k)
+    assert not pipe.stage(0, "DISP_LEFT").any()  # identical pair: d = 0 everywhere
