@@ -44,13 +44,30 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
-        return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, *[str(CSRC / s) for s in SOURCES], "-o", str(LIB)]
+    if force or stale():
+        cmd = [nvcc(), *NVCC_FLAGS, *[str(CSRC / s) for s in SOURCES], "-o", str(LIB)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True, cwd=str(CSRC))
+    build_cli(force, verbose)
+    return LIB
+
+
+CLI = PKG / "lanedet_gpu"
+
+
+def build_cli(force: bool = False, verbose: bool = False) -> Path:
+    """lanedet_gpu: the reference's lanedet CLI over the C-ABI (host C++ + zlib)."""
+    src = CSRC / "lanedet_gpu.cpp"
+    if not force and CLI.exists() and CLI.stat().st_mtime >= max(
+            src.stat().st_mtime, LIB.stat().st_mtime):
+        return CLI
+    cmd = [os.environ.get("CXX", "g++"), "-std=c++17", "-O2", "-Wall", str(src),
+           f"-L{PKG}", "-llanekit_b200", "-lz", "-Wl,-rpath,$ORIGIN", "-o", str(CLI)]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=str(CSRC))
-    return LIB
+    return CLI
 
 
 if __name__ == "__main__":

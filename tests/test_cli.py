@@ -1,0 +1,118 @@
+"""lanedet_gpu (the reference's lanedet CLI over the C-ABI): file formats on
+CPU (synth needs no GPU), and detect's artifacts against the compiled
+reference on the GPU."""
+import json
+import subprocess
+import zlib
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1807_02752_b200 import abi, lanekit
+
+ROOT = Path(__file__).resolve().parents[1]
+CLI = ROOT / "paper_1807_02752_b200" / "lanedet_gpu"
+
+
+def read_png(path):
+    """Minimal decoder for the CLI's PNGs (8-bit grey or RGB, filter 0)."""
+    d = Path(path).read_bytes()
+    assert d[:8] == b"\x89PNG\r\n\x1a\n"
+    o, idat, w = 8, b"", 0
+    while o < len(d):
+        n = int.from_bytes(d[o:o + 4], "big")
+        t = d[o + 4:o + 8]
+        body = d[o + 8:o + 8 + n]
+        assert zlib.crc32(d[o + 4:o + 8 + n]) == int.from_bytes(d[o + 8 + n:o + 12 + n], "big")
+        if t == b"IHDR":
+            w, h, ch = int.from_bytes(body[:4], "big"), int.from_bytes(body[4:8], "big"), body[9]
+        elif t == b"IDAT":
+            idat += body
+        o += 12 + n
+    c = 3 if ch == 2 else 1
+    raw = np.frombuffer(zlib.decompress(idat), np.uint8).reshape(h, w * c + 1)
+    assert not raw[:, 0].any()
+    return raw[:, 1:].reshape(h, w, c).squeeze()
+
+
+def read_pgm(path):
+    d = Path(path).read_bytes()
+    parts = d.split(b"\n", 3)
+    assert parts[0] == b"P5"
+    w, h = map(int, parts[1].split())
+    maxval = int(parts[2])
+    dt = ">u2" if maxval > 255 else "u1"
+    return np.frombuffer(parts[3], dt).reshape(h, w), maxval
+
+
+def test_cli_synth_formats(tmp_path):
+    out = subprocess.run([str(CLI), "synth", "--out-dir", str(tmp_path), "--seed", "3",
+                          "--width", "320", "--height", "240"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    left = read_png(tmp_path / "left.png")
+    right = read_png(tmp_path / "right.png")
+    disp, maxval = read_pgm(tmp_path / "true_disparity.pgm")
+    assert left.shape == (240, 320) and right.shape == (240, 320) and maxval == 65535
+    import ctypes as C
+
+    q = abi.LkSceneParams()
+    lanekit.library().lk_scene_default(C.byref(q))
+    q.width, q.height, q.rng_seed, q.noise_sigma = 320, 240, 3, 0.02
+    l2, r2, d2, _ = lanekit.synth_scene(q)
+    assert np.array_equal(left, l2) and np.array_equal(right, r2)
+    assert np.array_equal(disp, d2.astype(np.uint16) * 256)
+
+
+def test_cli_rejects_bad_input(tmp_path):
+    (tmp_path / "a.pgm").write_bytes(b"P5\n4 4\n65535\n" + bytes(32))
+    out = subprocess.run([str(CLI), "detect", "--left", str(tmp_path / "a.pgm"), "--right",
+                          str(tmp_path / "a.pgm"), "--out-dir", str(tmp_path / "o")],
+                         capture_output=True, text=True)
+    assert out.returncode == 1 and "maxval 255" in out.stderr
+    out = subprocess.run([str(CLI), "detect", "--left", "x", "--right", "y", "--out-dir",
+                          str(tmp_path), "--set", "nope=1"], capture_output=True, text=True)
+    assert out.returncode == 1 and "config: unknown key 'nope'" in out.stderr
+
+
+@pytest.mark.gpu
+def test_cli_detect_artifacts_match_reference(tmp_path, oracle):
+    from checkers import Checker, ref_available
+
+    chk = Checker("ref") if ref_available() else oracle
+    out = subprocess.run([str(CLI), "synth", "--out-dir", str(tmp_path), "--seed", "5",
+                          "--width", "1242", "--height", "375"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    left, right = read_png(tmp_path / "left.png"), read_png(tmp_path / "right.png")
+    od = tmp_path / "out"
+    out = subprocess.run([str(CLI), "detect", "--left", str(tmp_path / "left.png"), "--right",
+                          str(tmp_path / "right.png"), "--out-dir", str(od), "--emit-all"],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    cfg = abi.default_config()
+    st = chk.stereo(left, right, cfg)
+    r = chk.run(left, st["DISPARITY"], cfg)
+    rep = r.report
+    disp, _ = read_pgm(od / "disparity.pgm")
+    assert np.array_equal(disp, st["DISPARITY"].astype(np.uint16) * 256)
+    dl, _ = read_pgm(od / "disparity_left.pgm")
+    assert np.array_equal(dl, st["DISP_LEFT"].astype(np.uint16) * 256)
+    j = json.loads((od / "report.json").read_text())
+    assert j["lanes"]["count"] == rep.lane_count and j["road"]["horizon"] == rep.horizon
+    assert j["edges"]["count"] == rep.edge_pixels
+    assert j["stereo"]["valid_disparities"] == rep.valid_disparities
+    assert j["road"]["beta"] == [rep.beta[0], rep.beta[1], rep.beta[2]]
+    lanes = r.get("LANES")
+    assert [d["bottom_col"] for d in j["lanes"]["detected"]] == list(lanes["bottom_col"])
+    csv = (od / "lanes.csv").read_text().splitlines()
+    assert csv[0] == "lane_id,v,u" and len(csv) > 1
+    edges = read_png(od / "edges.png")
+    e = r.get("EDGES")
+    ref_edges = np.zeros_like(edges)
+    ref_edges[e["v"], e["u"]] = 255
+    assert np.array_equal(edges, ref_edges)
+    vd, _ = read_pgm(od / "vdisparity.pgm")
+    assert np.array_equal(vd, np.minimum(r.get("VDISPARITY"), 255).astype(np.uint8))
+    for f in ("overlay.png", "vpx_accumulator.pgm", "road_fit.csv", "smoothed.png", "m1.png",
+              "energy_histogram.csv", "upath.csv", "vpath.csv", "block_sigma.png"):
+        assert (od / f).exists(), f
