@@ -1484,74 +1484,69 @@ __global__ void __launch_bounds__(256) k_p99_select(Dev d) {
 // m1 sum run together from the bottom row upward.
 // =====================================================================
 __global__ void __launch_bounds__(128) k_energy(Dev d) {
-    extern __shared__ double sh_e[];  // per row v: vpx[v+1], vpy[v+1], denom, 1/denom
+    extern __shared__ double4 sh_e4[];  // per row v: (vpx[v+1], vpy[v+1], denom, 1/denom)
+    __shared__ int s_dead;
     const int f = blockIdx.y;
     if (frame_failed(d, f)) return;
     const int W = d.W, H = d.H;
     const int v_top = (int)d.rep[f].horizon, v_max = H - 1;
     const double* vpx = d.vpx + (size_t)f * H;
     const double* vpy = d.vpy + (size_t)f * H;
-    double* s_px = sh_e;
-    double* s_py = s_px + H;
-    double* s_den = s_py + H;
-    double* s_rcp = s_den + H;
+    uint8_t* s_nz = (uint8_t*)(sh_e4 + H);  // the frame's m1 tile flags
     // Every column divides by the same denom at row v, so 1/denom is
     // computed once per row; each quotient is then q0 = RN(a y), r = a - q0 b
     // (exact, FMA), q = RN(q0 + r y), which is the correctly rounded a / b
     // (Markstein; checked against IEEE division on 3e10 cases by
     // tools/markstein_check.cu). Zero, non-finite or extreme operands take the
-    // IEEE division.
+    // IEEE division. The track of EVERY column stops at the same row: the
+    // first v (going up) with |denom| < 0.5 (lanes.hpp:91), found once here.
+    if (threadIdx.x == 0) s_dead = -1;
+    __syncthreads();
     for (int v = v_top + threadIdx.x; v < v_max; v += blockDim.x) {
         const double py = vpy[v + 1];
         const double den = (double)(v + 1) - py;
-        s_px[v] = vpx[v + 1];
-        s_py[v] = py;
-        s_den[v] = den;
-        s_rcp[v] = 1.0 / den;
+        sh_e4[v] = make_double4(vpx[v + 1], py, den, 1.0 / den);
+        if (fabs(den) < 0.5) atomicMax(&s_dead, v);
     }
+    for (int i = threadIdx.x; i < d.m_nty * d.m_ntx; i += blockDim.x)
+        s_nz[i] = d.m1_nz[(size_t)f * d.m_nty * d.m_ntx + i];
     __syncthreads();
     const int ci = blockIdx.x * blockDim.x + threadIdx.x;
     if (ci >= d.ext_cols) return;
     const double* m1 = d.m1 + (size_t)f * d.px;
-    const uint8_t* nz = d.m1_nz + (size_t)f * d.m_nty * d.m_ntx;  // unwritten tiles are zero
     const double lg = d.lambda_g;
     const double w_hi = (double)W - 0.5;
+    const int v_alive = max(v_top, s_dead + 1);  // rows v_alive..v_max carry the track
     double u = (double)(d.ext_lo + ci);
-    bool alive = true;
     double e = 0.0;
     // Chunks of EC rows: the track recursion (lane_track, lanes.hpp:83-96)
     // yields EC gather indices, the EC m1 loads are then all in flight
     // together, and the decayed sum consumes them in row order.
     constexpr int EC = 8;
-    for (int vc = v_max; vc >= v_top; vc -= EC) {
+    for (int vc = v_max; vc >= v_alive; vc -= EC) {
         int idx[EC];
 #pragma unroll
         for (int k = 0; k < EC; ++k) {
             const int v = vc - k;
             idx[k] = -1;
-            if (v < v_top) continue;
-            if (v < v_max && alive) {
-                const double py = s_py[v], den = s_den[v];
-                if (fabs(den) < 0.5) {
-                    alive = false;
+            if (v < v_alive) continue;
+            if (v < v_max) {
+                const double4 rw = sh_e4[v];
+                const double a = rw.x + (double)v * u - rw.y * u;
+                const double aa = fabs(a);
+                if (aa >= 0x1p-500 && aa <= 0x1p500 && fabs(rw.z) <= 0x1p500) {
+                    const double q0 = __dmul_rn(a, rw.w);
+                    u = __fma_rn(__fma_rn(-q0, rw.z, a), rw.w, q0);
                 } else {
-                    const double a = s_px[v] + v * u - py * u;
-                    const double aa = fabs(a);
-                    if (aa >= 0x1p-500 && aa <= 0x1p500 && fabs(den) <= 0x1p500) {
-                        const double y = s_rcp[v];
-                        const double q0 = __dmul_rn(a, y);
-                        u = __fma_rn(__fma_rn(-q0, den, a), y, q0);
-                    } else {
-                        u = a / den;
-                    }
+                    u = a / rw.z;
                 }
             }
             // llround(u) in [0, W)  <=>  -0.5 < u < W - 0.5 (NaN fails); then
             // llround = trunc + (frac >= 0.5), exact for these magnitudes
-            if (alive && u > -0.5 && u < w_hi) {
+            if (u > -0.5 && u < w_hi) {
                 const int t = (int)u;
                 const int r = t + (u - (double)t >= 0.5);
-                if (nz[(v >> d.m_tile_shift) * d.m_ntx + (r >> 7)]) idx[k] = v * W + r;  // < 2^31
+                if (s_nz[(v >> d.m_tile_shift) * d.m_ntx + (r >> 7)]) idx[k] = v * W + r;  // < 2^31
             }
         }
         double c[EC];
@@ -1559,8 +1554,10 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
         for (int k = 0; k < EC; ++k) c[k] = idx[k] >= 0 ? m1[idx[k]] : 0.0;
 #pragma unroll
         for (int k = 0; k < EC; ++k)
-            if (vc - k >= v_top) e = c[k] + lg * e;
+            if (vc - k >= v_alive) e = c[k] + lg * e;
     }
+    // rows after the track stops contribute +0.0 (kept: 0 + (-0.0) is +0.0)
+    for (int v = v_alive - 1; v >= v_top; --v) e = 0.0 + lg * e;
     d.energy[(size_t)f * d.ext_cols + ci] = e;
 }
 
@@ -1781,7 +1778,8 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
         k_p99_collect<<<dim3(lp.collect_blocks, n), 256, 0, s>>>(d);
         k_p99_select<<<n, 256, 0, s>>>(d);
     }
-    k_energy<<<dim3((d.ext_cols + 127) / 128, n), 128, (size_t)4 * d.H * 8, s>>>(d);
+    k_energy<<<dim3((d.ext_cols + 127) / 128, n), 128,
+               (size_t)d.H * sizeof(double4) + (size_t)d.m_nty * d.m_ntx, s>>>(d);
     k_select<<<n, 256, lp.select_smem, s>>>(d, lp.sort_cap);
     k_finish<<<(n + 127) / 128, 128, 0, s>>>(d, n);
     mark(12);
