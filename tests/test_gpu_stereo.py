@@ -131,3 +131,18 @@ def test_stereo_exact_ties_take_the_fp64_path(oracle):
         for k in STEREO_HOOKS:
             assert pipe.stage(i, k).tobytes() == o[k].tobytes(), (i, k)
     assert not pipe.stage(0, "DISP_LEFT").any()  # identical pair: d = 0 everywhere
+
+
+def test_stereo_hires_frame(oracle):
+    """2560x1024 with d_max 248 (config 4): rows wider than the register
+    prefetch, the largest shared-memory windows, u8 disparities near 255."""
+    p = scenes.hires_scene(3)
+    left, right, _ = lanekit.synth_stereo_batch([p])
+    cfg = scenes.hires_config()
+    pipe, reps = _run({}, left, right, cfg)
+    chk = _checker(oracle)
+    o = chk.stereo(left[0], right[0], cfg)
+    for k in STEREO_HOOKS:
+        assert pipe.stage(0, k).tobytes() == o[k].tobytes(), k
+    r = chk.run(left[0], o["DISPARITY"], cfg)
+    assert not compare_reports(reps[0], r.report)
