@@ -480,7 +480,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     if (lp.upath_sp == 7) lp.upath_sp = 8;
     if (lp.upath_nt == 1024 && lp.upath_sp < 5) lp.upath_sp = 5;
     if (lp.upath_sp > 8) lp.upath_sp = 0;
-    lp.gamma_smem = (size_t)20 * H * 4 + 8 + (size_t)6 * H * 8 + 16;  // px, pv, NW+2 lists, basis rows
+    lp.gamma_smem = (size_t)(GAMMA_NW + 4) * H * 4 + 8 + (size_t)6 * H * 8 + 16;  // px, pv, NW+2 lists, basis rows
     lp.m_tile_h = 16;
     auto m_bytes = [&](int th) {
         const size_t GH = th + 2 + 2 * cfg->varsigma, GW = lkg::M_TW + 2 + 2 * cfg->nu;

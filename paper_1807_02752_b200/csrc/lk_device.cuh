@@ -156,6 +156,20 @@ __device__ __forceinline__ double* align8(void* p) {
     return (double*)(c + ((8 - ((uintptr_t)c & 7)) & 7));
 }
 
+// a / b, correctly rounded, given y = RN(1 / b): q0 = RN(a y), r = a - q0 b
+// (exact, FMA), q = RN(q0 + r y) (Markstein's theorem; checked against IEEE
+// division on 3e10 cases by tools/markstein_check.cu). Zero, non-finite or
+// extreme operands fall back to the IEEE division, so the result is always
+// bit-identical to a / b. Lets several quotients share one reciprocal.
+__device__ __forceinline__ double div_rn(double a, double b, double y) {
+    const double aa = fabs(a), ab = fabs(b);
+    if (aa >= 0x1p-500 && aa <= 0x1p500 && ab >= 0x1p-500 && ab <= 0x1p500) {
+        const double q0 = __dmul_rn(a, y);
+        return __fma_rn(__fma_rn(-q0, b, a), y, q0);
+    }
+    return a / b;
+}
+
 // Ordered double -> u64 key (total order equal to '<' for non-NaN values).
 __device__ __forceinline__ unsigned long long order_key(double x) {
     unsigned long long b = (unsigned long long)__double_as_longlong(x);

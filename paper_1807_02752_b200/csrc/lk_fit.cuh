@@ -53,8 +53,11 @@ struct RansacState {  // lives in shared memory
     double best_model[5];
     double best_s;
     double w_s[RS_MAX_WARPS];
+    double w_frac[RS_MAX_WARPS];  // inlier fraction of warp w's iteration (ransac.hpp:76)
 #ifdef LK_GAMMA_PROF
     long long t_loop;
+    long long t_fit, t_cls, t_commit;
+    int rounds;
 #endif
 };
 
@@ -381,10 +384,16 @@ __device__ void block_ransac(const int* px, const int* pv, int n, double tol, do
         if (n < K) st.msg = LK_MSG_RANSAC_FEW_POINTS;  // ransac.hpp:41-42
     }
     __syncthreads();
+#ifdef LK_GAMMA_PROF
+    if (tid == 0) { st.t_fit = st.t_cls = st.t_commit = 0; st.rounds = 0; }
+#endif
     if (st.done) return;
     for (int i = tid; i < n; i += blockDim.x) bufs[0][i] = i;
     __syncthreads();
     while (!st.done) {
+#ifdef LK_GAMMA_PROF
+        const long long r0 = clock64();
+#endif
         const int it = st.it0 + warp;
         const int msz = st.msz;
         if (warp < NW && it < max_iter && msz >= K) {
@@ -421,15 +430,28 @@ __device__ void block_ransac(const int* px, const int* pv, int n, double tol, do
             }
             ok = __shfl_sync(0xffffffffu, ok, 0);
             __syncwarp();
+#ifdef LK_GAMMA_PROF
+            if (warp == 0 && lane == 0) st.t_fit += clock64() - r0;
+            const long long r1 = clock64();
+#endif
             if (ok) {
                 double mdl[5];
                 for (int k = 0; k < K; ++k) mdl[k] = st.w_model[warp][k];
                 const int cnt =
                     warp_classify<K>(px, pv, m, msz, mdl, tol, bufs[st.w_buf[warp]]);
-                if (lane == 0) st.w_cnt[warp] = cnt;
+                if (lane == 0) {  // the fraction is computed here, not in the serial commit
+                    st.w_cnt[warp] = cnt;
+                    st.w_frac[warp] = (double)cnt / (double)msz;
+                }
             }
+#ifdef LK_GAMMA_PROF
+            if (warp == 0 && lane == 0) st.t_cls += clock64() - r1;
+#endif
         }
         __syncthreads();
+#ifdef LK_GAMMA_PROF
+        const long long r2 = clock64();
+#endif
         if (tid == 0) {  // commit in iteration order (ransac.hpp:54-87)
             int next_it0 = st.it0 + NW;
             for (int w = 0; w < NW; ++w) {
@@ -445,7 +467,7 @@ __device__ void block_ransac(const int* px, const int* pv, int n, double tol, do
                 }
                 if (!st.w_ok[w]) continue;  // degenerate sample, iteration consumed
                 const int cnt = st.w_cnt[w];
-                const double fraction = (double)cnt / (double)st.msz;
+                const double fraction = st.w_frac[w];  // = cnt / st.msz (same msz this round)
                 if (fraction > st.best) {
                     st.best = fraction;
                     for (int k = 0; k < K; ++k) st.best_model[k] = st.w_model[w][k];
@@ -473,6 +495,9 @@ __device__ void block_ransac(const int* px, const int* pv, int n, double tol, do
             if (st.it0 >= max_iter) st.done = 1;
         }
         __syncthreads();
+#ifdef LK_GAMMA_PROF
+        if (tid == 0) { st.t_commit += clock64() - r2; ++st.rounds; }
+#endif
     }
 #ifdef LK_GAMMA_PROF
     if (tid == 0) st.t_loop = clock64();

@@ -1063,7 +1063,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
 // (:276-281), then the w_g edge weights of build_m0 (lanes.hpp:35-44).
 // One CTA per frame; warp 0 runs the RANSAC.
 // =====================================================================
-__global__ void __launch_bounds__(512, 2) k_gamma_fit(Dev d) {
+__global__ void __launch_bounds__(32 * GAMMA_NW, 2) k_gamma_fit(Dev d) {
     extern __shared__ int sh_g[];
     const int f = blockIdx.x;
     if (frame_failed(d, f)) return;
@@ -1071,7 +1071,7 @@ __global__ void __launch_bounds__(512, 2) k_gamma_fit(Dev d) {
     lk_frame_report& rep = d.rep[f];
     const int v_top = (int)rep.horizon, v_max = H - 1;
     const int nrows = v_max - v_top + 1;
-    constexpr int NW = 16;  // 512 threads: 16 speculative RANSAC iterations per round
+    constexpr int NW = GAMMA_NW;  // speculative RANSAC iterations per round, one warp each
     int* px = sh_g;
     int* pv = px + H;
     int* bufs[NW + 2];
@@ -1149,6 +1149,10 @@ __global__ void __launch_bounds__(512, 2) k_gamma_fit(Dev d) {
         rep.gamma_kappa = (double)(st.t_loop - t0);
         rep.gamma_v_normalizer = (double)(t1 - st.t_loop);
         rep.gamma_inlier_fraction = (double)(clock64() - t1);
+        rep.beta[0] = (double)st.t_fit;
+        rep.beta[1] = (double)st.t_cls;
+        rep.beta[2] = (double)st.t_commit;
+        rep.vpath_energy = (double)st.rounds;
     }
 #endif
 }
@@ -1766,7 +1770,7 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
         }
     }
 #undef LK_VANISH
-    k_gamma_fit<<<n, 512, lp.gamma_smem, s>>>(d);
+    k_gamma_fit<<<n, 32 * GAMMA_NW, lp.gamma_smem, s>>>(d);
     mark(11);
     const bool auto_tr = isnan(d.tr_lpv);
     k_m0_m1<<<dim3((d.W + M_TW - 1) / M_TW, (d.H + lp.m_tile_h - 1) / lp.m_tile_h, n), 256,

@@ -17,6 +17,9 @@ constexpr int BT_TRI_N = 128;           // max distinct values per tile for the 
                                         // get broadcast; 16 copies measured 1.5x slower)
 #endif
 constexpr int K4_THREADS = 512;         // V_px CTA (2 per SM)
+#ifndef GAMMA_NW
+#define GAMMA_NW 8                      // RANSAC-gamma warps = speculative iterations per round
+#endif
 constexpr int K4_VOTE_CAP = 8192;       // edges whose vote columns are staged in smem
 constexpr int BT_CHUNK = 32;            // u-path backtrack: stages per window
 constexpr int BT_SPAN = 5 * BT_CHUNK;   // max drift inside a window (|offset| <= 5)
