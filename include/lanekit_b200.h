@@ -240,6 +240,18 @@ lk_status lk_run_batch(lk_ctx* ctx, const uint8_t* grey, const uint8_t* disparit
  * until lk_fetch_reports. Asynchronous on the context stream. */
 lk_status lk_device_inputs(lk_ctx* ctx, uint8_t** grey, uint8_t** disparity);
 lk_status lk_enqueue(lk_ctx* ctx, int n);
+
+/* Streaming host-fed batches: batch k+1's host-to-device copy (a copy stream,
+ * two input slots) overlaps batch k's kernels. lk_submit_batch queues the copy
+ * of grey/disparity (u8 [n][H][W], pinned: lk_host_alloc), the pipeline and the
+ * read-back of the n reports into `reports` (pinned; may be NULL), and returns
+ * without waiting. Up to two batches are in flight: a third submit first waits
+ * for the oldest. lk_wait_batch waits for the oldest submitted batch and
+ * returns its status (LK_ERR_FRAME when one of its frames failed). The host
+ * buffers of a batch must stay untouched until it has been waited for. */
+lk_status lk_submit_batch(lk_ctx* ctx, const uint8_t* grey, const uint8_t* disparity, int n,
+                          lk_frame_report* reports);
+lk_status lk_wait_batch(lk_ctx* ctx);
 lk_status lk_fetch_reports(lk_ctx* ctx, lk_frame_report* reports, int n);
 lk_status lk_synchronize(lk_ctx* ctx);
 void* lk_stream(lk_ctx* ctx); /* cudaStream_t of the context */

@@ -110,6 +110,18 @@ struct lk_ctx {
     uint8_t* in_disp = nullptr;  // the disparity (stereo: written by stage 4)
     uint8_t* in_right = nullptr; // stereo contexts: the right grey
     bool run_stereo = false;     // the batch being enqueued runs stages 1-4 first
+    int slot = 0;                // input slot the captured graphs read (streaming API)
+    // streaming API (lk_submit_batch / lk_wait_batch): two input slots
+    uint8_t* slot_grey[2] = {};
+    uint8_t* slot_disp[2] = {};
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t slot_copied[2] = {}, slot_free[2] = {}, slot_done[2] = {};
+    struct Pending {
+        int slot, n;
+        lk_frame_report* reports;
+    };
+    Pending pending[2];
+    int n_pending = 0, next_slot = 0;
     bool last_stereo = false;
     int last_n = 0;
 
@@ -567,6 +579,13 @@ lk_status lk_destroy(lk_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamDestroy(c->copy_stream);
+    }
+    for (int k = 0; k < 2; ++k)
+        for (cudaEvent_t e : {c->slot_copied[k], c->slot_free[k], c->slot_done[k]})
+            if (e) cudaEventDestroy(e);
     for (auto& kv : c->range_graphs) cudaGraphExecDestroy(kv.second);
     for (cudaEvent_t e : c->copied)
         if (e) cudaEventDestroy(e);
@@ -789,7 +808,7 @@ static lk_status enqueue_mode(lk_ctx* c, int n) {
         return enqueue_direct(c, n, true);
     }
     c->timed = true;
-    const int key = 2 * n + (c->run_stereo ? 1 : 0);
+    const int key = 4 * n + 2 * c->slot + (c->run_stereo ? 1 : 0);
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
         cudaGraph_t g;
@@ -813,6 +832,77 @@ lk_status lk_enqueue(lk_ctx* c, int n) {
     if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
     c->run_stereo = false;
     return enqueue_mode(c, n);
+}
+
+// ---- streaming: batch k+1's host->device copy (copy stream) overlaps batch
+// k's kernels (context stream). Two input slots; the kernels of consecutive
+// batches stay ordered on the context stream (they share intermediates).
+lk_status lk_wait_batch(lk_ctx* c) {
+    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
+    if (c->n_pending == 0) return fail(LK_ERR_INVALID_ARGUMENT, "no submitted batch to wait for");
+    const lk_ctx::Pending p = c->pending[0];
+    c->pending[0] = c->pending[1];
+    --c->n_pending;
+    CU(cudaEventSynchronize(c->slot_done[p.slot]));
+    bool any = false;
+    if (p.reports)
+        for (int i = 0; i < p.n; ++i) {
+            p.reports[i].rng_seed = c->cfg.rng_seed;
+            any |= p.reports[i].status != 0;
+        }
+    return any ? LK_ERR_FRAME : LK_OK;
+}
+
+lk_status lk_submit_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* disparity, int n,
+                          lk_frame_report* reports) {
+    if (!c || !grey || !disparity) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
+    CU(cudaSetDevice(c->device));
+    if (!c->copy_stream) {  // first use: the second input slot and the copy stream
+        if (lk_status s = c->alloc(&c->slot_grey[1], (size_t)c->max_batch * c->d.px)) return s;
+        if (lk_status s = c->alloc(&c->slot_disp[1], (size_t)c->max_batch * c->d.px)) return s;
+        c->slot_grey[0] = c->in_grey;
+        c->slot_disp[0] = c->in_disp;
+        CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            CU(cudaEventCreateWithFlags(&c->slot_copied[k], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&c->slot_free[k], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&c->slot_done[k], cudaEventDisableTiming));
+            CU(cudaEventRecord(c->slot_free[k], c->stream));
+        }
+    }
+    if (c->n_pending == 2) {  // at most two batches in flight
+        const lk_status s = lk_wait_batch(c);
+        if (s != LK_OK && s != LK_ERR_FRAME) return s;
+    }
+    const int sl = c->next_slot;
+    c->next_slot ^= 1;
+    const size_t bytes = (size_t)n * c->d.px;
+    // inputs into the slot once the batch that last read it has finished
+    CU(cudaStreamWaitEvent(c->copy_stream, c->slot_free[sl], 0));
+    CU(cudaMemcpyAsync(c->slot_grey[sl], grey, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+    CU(cudaMemcpyAsync(c->slot_disp[sl], disparity, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+    CU(cudaEventRecord(c->slot_copied[sl], c->copy_stream));
+    // kernels on the slot (graphs are keyed by slot), then the reports
+    CU(cudaStreamWaitEvent(c->stream, c->slot_copied[sl], 0));
+    const uint8_t* g0 = c->d.grey;
+    const uint8_t* d0 = c->d.disp;
+    c->d.grey = c->slot_grey[sl];
+    c->d.disp = c->slot_disp[sl];
+    c->slot = sl;
+    c->run_stereo = false;
+    const lk_status s = enqueue_mode(c, n);
+    c->d.grey = g0;
+    c->d.disp = d0;
+    c->slot = 0;
+    if (s != LK_OK) return s;
+    CU(cudaEventRecord(c->slot_free[sl], c->stream));
+    if (reports)
+        CU(cudaMemcpyAsync(reports, c->d.rep, (size_t)n * sizeof(lk_frame_report),
+                           cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaEventRecord(c->slot_done[sl], c->stream));
+    c->pending[c->n_pending++] = {sl, n, reports};
+    return LK_OK;
 }
 
 lk_status lk_enqueue_stereo(lk_ctx* c, int n) {

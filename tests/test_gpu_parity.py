@@ -166,3 +166,29 @@ def test_direct_launch_matches_graph(oracle):
         b = [r.as_dict() for r in p2.run(grey, disp)]
     assert a == b
     assert t[0] > 0 and t[9] > 0
+
+
+def test_streaming_submit_wait_matches_run_batch():
+    """lk_submit_batch / lk_wait_batch (two input slots, copies overlapping the
+    previous batch's kernels): every batch's reports equal lk_run_batch's on
+    the same frames, across slot reuse and the auto-wait of a third submit."""
+    import ctypes as C
+
+    cfg = abi.default_config()
+    batches = []
+    for b in range(4):
+        params = [scenes.batch_scene(100 + 16 * b + i) for i in range(16)]
+        batches.append(lanekit.synth_batch(params, threads=8))
+    with lanekit.GpuPipeline(1242, 375, cfg, max_batch=16) as pipe:
+        want = [[bytes(r) for r in pipe.run(g, d)] for g, d in batches]
+        L = lanekit.library()
+        got = [(abi.LkFrameReport * 16)() for _ in batches]
+        keep = [(np.ascontiguousarray(g), np.ascontiguousarray(d)) for g, d in batches]
+        for b, (g, d) in enumerate(keep):  # the third submit waits for the first
+            st = L.lk_submit_batch(pipe._h, g.ctypes.data, d.ctypes.data, 16, got[b])
+            assert st == abi.LK_OK, L.lk_last_error()
+        assert L.lk_wait_batch(pipe._h) in (abi.LK_OK, abi.LK_ERR_FRAME)
+        assert L.lk_wait_batch(pipe._h) in (abi.LK_OK, abi.LK_ERR_FRAME)
+        assert L.lk_wait_batch(pipe._h) == abi.LK_ERR_INVALID_ARGUMENT  # nothing pending
+        for b in range(4):
+            assert [bytes(r) for r in got[b]] == want[b], b
