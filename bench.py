@@ -97,27 +97,39 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.lines = []
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            if ln.strip():
+                self.lines.append(ln)
 
     def __enter__(self):
+        import threading
+
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(self.device)],
+                 "-lms", "50", "-i", str(self.device)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+            t0 = time.time()  # the first sample marks nvidia-smi as running
+            while not self.lines and time.time() - t0 < 5:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.start = len(self.lines)  # samples taken inside the timed region only
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc:
+            time.sleep(0.06)  # one more sample interval covers the region's tail
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
-                out = ""
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        self.lines = self.lines[self.start:]
 
     def summary(self):
         sm, smax, reasons = [], [], set()
