@@ -1199,28 +1199,31 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
     double* gw = sh5;
     double* m0 = gw + GH * GW;
     unsigned int* hist = (unsigned int*)(m0 + MH * MW);
-    for (int i = threadIdx.x; i < GH * GW; i += blockDim.x) gw[i] = 0.0;
-    if (want_hist)
-        for (int i = threadIdx.x; i < 2048; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
     const int32_t* roff = d.row_off + (size_t)f * (H + 1);
     const size_t eb = (size_t)f * d.px;
     const int r_lo = max(max(gr0, 0), v_top), r_hi = min(gr0 + GH - 1, v_max);
+    // A tile without a non-zero w_g in reach has m0 = m1 = +0 everywhere: it
+    // is flagged instead of written (readers of m1 consult the flag). The test
+    // runs first, so such tiles (most of them) skip the staging entirely.
     int nonzero = 0;
-    if (r_lo <= r_hi) {
+    if (r_lo <= r_hi)
+        for (int e = roff[r_lo] + threadIdx.x; e < roff[r_hi + 1] && !nonzero; e += blockDim.x) {
+            const int u = d.e_uv[eb + e] & 0xffff;
+            nonzero = u >= gc0 && u < gc0 + GW && d.e_wg[eb + e] != 0.0;
+        }
+    nonzero = __syncthreads_or(nonzero);
+    if (nonzero) {
+        for (int i = threadIdx.x; i < GH * GW; i += blockDim.x) gw[i] = 0.0;
+        if (want_hist)
+            for (int i = threadIdx.x; i < 2048; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
         for (int e = roff[r_lo] + threadIdx.x; e < roff[r_hi + 1]; e += blockDim.x) {
             const int uv = d.e_uv[eb + e];
             const int u = uv & 0xffff, v = uv >> 16;
-            if (u >= gc0 && u < gc0 + GW) {
-                const double w = d.e_wg[eb + e];
-                gw[(v - gr0) * GW + (u - gc0)] = w;
-                nonzero |= w != 0.0;
-            }
+            if (u >= gc0 && u < gc0 + GW) gw[(v - gr0) * GW + (u - gc0)] = d.e_wg[eb + e];
         }
+        __syncthreads();
     }
-    // A tile without a non-zero w_g in reach has m0 = m1 = +0 everywhere: it
-    // is flagged instead of written (readers of m1 consult the flag).
-    nonzero = __syncthreads_or(nonzero);
     const int t_lo = max(0, v_top), t_hi = min(H - 1, v_max);
     if (threadIdx.x == 0)
         d.m1_nz[((size_t)f * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = (uint8_t)nonzero;
