@@ -83,7 +83,7 @@ constexpr int kMaxBranches = 16;      // concurrent frame ranges (streams) per b
 constexpr int kMinBranchFrames = 16;  // smallest range worth a branch
 constexpr int kH2dChunksDefault = 12; // host-fed batches: copy/compute pipeline depth
 constexpr int kBranchesDefault = 4;   // device-resident batches: concurrent frame ranges
-constexpr int kFastTableDefault = 21;  // tap pairs of the fast bilateral served by the range table
+constexpr int kFastTableDefault = 27;  // tap pairs of the fast bilateral served by the range table
 
 }  // namespace
 
@@ -464,22 +464,31 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         for (int dj = 0; dj < 11; ++dj)
             for (int q = 0; q < 5; ++q)
                 lp.fbf.cp[dj][q] = make_float2(lp.fbf.c[dj * 11 + 2 * q], lp.fbf.c[dj * 11 + 2 * q + 1]);
+        for (int k = 0; k < 12; ++k) {
+            auto c10 = [&](int dj) { return dj < 0 || dj > 10 ? -INFINITY : lp.fbf.c[dj * 11 + 10]; };
+            lp.fbf.c10[k] = make_float2(c10(k), c10(k - 1));
+        }
         lp.fbf.c2 = (float)(-inv_r2 * log2e);
-        for (int k = 0; k < 256; ++k) lp.fbf.vf[k] = (float)(k / 255.0);
         for (int dj = -5; dj <= 5; ++dj)
             for (int q = 0; q < 5; ++q) {
                 auto sf = [&](int di) { return (float)std::exp(-(double)(di * di + dj * dj) * inv_s2); };
                 lp.fbf.sp[dj + 5][q] = make_float2(sf(2 * q - 5), sf(2 * q - 4));
             }
         fast_tab.resize(256 + 512);
-        for (int k = 0; k < 256; ++k) fast_tab[k] = lp.fbf.vf[k];
+        for (int k = 0; k < 256; ++k) fast_tab[k] = (float)(k / 255.0);
         for (int i = 0; i < 512; ++i) {
             const double dr = (i - 255) / 255.0;
             fast_tab[256 + i] = i < 511 ? (float)std::exp(-dr * dr * inv_r2) : 0.f;
         }
         const char* m = std::getenv("LK_BF_TABLE");
         lp.fast_table = m ? std::atoi(m) & 31 : kFastTableDefault;
-        if (lp.fast_front) A(&d.smoothed_f, (size_t)B * d.px);
+        const char* tpc = std::getenv("LK_BF_TPC");  // tiles per CTA
+        lp.fast_tpc = tpc ? std::atoi(tpc) : 24;
+        d.bf_ntiles = ((W + lkg::BT_W - 1) / lkg::BT_W) * ((H + lkg::BT_H - 1) / lkg::BT_H);
+        if (lp.fast_front) {
+            A(&d.smoothed_f, (size_t)B * d.px);
+            A(&d.bf_flag, (size_t)B * d.bf_ntiles);
+        }
         A(&d_ft, fast_tab.size());
     }
     lp.vanish_smem = (size_t)(2 * C + 32) * 8 + (size_t)2 * C * 4 + (size_t)2 * H * 4 +
@@ -659,6 +668,7 @@ static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     sh(v.vpx, H);
     sh(v.smoothed, px);
     sh(v.smoothed_f, px);
+    sh(v.bf_flag, (size_t)d.bf_ntiles);
     sh(v.ebits, H * d.words_per_row);
     sh(v.seg_cnt, H * d.n_seg);
     sh(v.seg_off, H * d.n_seg);

@@ -85,6 +85,8 @@ struct Dev {
     double* vpx;            // [B][H]
     double* smoothed;       // [B][H][W] (fast path: exact only around edge candidates)
     float* smoothed_f;      // [B][H][W] certified approximation (fast path)
+    uint8_t* bf_flag;       // [B][bf_ntiles] fast-bilateral tiles the Sobel screen needs
+    int bf_ntiles;          // fast-bilateral tiles per frame
     const float* fast_tab;  // [256] k/255 as float, then [512] range factor of dr = (i-255)/255
     uint32_t* ebits;        // [B][H][words_per_row]
     int n_seg;              // edge-list segments per row (ceil(W / SB_TW))

@@ -23,6 +23,9 @@
 // path, so the SMOOTHED/GX/GY/MAG/THETA maps it exports are exact.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <climits>
+
 #include "lk_kernels.h"
 
 namespace lkg {
@@ -37,131 +40,236 @@ __device__ __forceinline__ float ex2_approx(float x) {
 
 // ---- 1. approximate bilateral: tile BT_W x BT_H, BT_R outputs per thread
 //
-// Taps (2q, 2q+1) of a window row are processed as one packed f32x2 lane pair
-// (FADD2 / FMUL2 / FFMA2), which halves the FP32 issue slots and leaves the
-// range factor as the limiter. Tap pairs in the mask TB take it from a
-// 511-entry shared-memory table instead of MUFU ex2, so the XU and the LSU
-// pipes share the work. The table index comes from the float difference
-// itself: dr*1020*RC is within 3e-3 of the integer 4 RC (k_q - k_p), so one FFMA with
-// 1.5*2^23 rounds it into the low mantissa bits (no integer keys staged).
-// w = S_t * R[dr] rounds three times in FP32 (~2e-7 relative), inside the
-// ex2.approx error the bound in DESIGN.md already budgets.
+// Issue-slot budget per (output, window row): 5 packed tap pairs + the 11th
+// column, where every instruction counts (the kernel is issue-, LSU- and
+// MUFU-bound at once):
+//  - window values come in as 8-byte pairs (LDS.64). The tile is staged twice,
+//    the second copy shifted by one pixel, so an odd column's pair is aligned too;
+//  - MUFU pairs: dr = v_q - v_p (FADD2), c2*dr^2 + c_t (FMUL2, FFMA2), 2x ex2;
+//  - table pairs: one FFMA2 turns v_q into the shared-memory byte ADDRESS of
+//    R[k_q - k_p]. The FMA lands in the subnormal range, where a float's bit
+//    pattern is the integer multiple of 2^-149, so RN(v_q*1020*2^-149 + C_p)
+//    has bits A_R + 4(k_q - k_p + 255) exactly (v_q*1020 is within 1e-4 of
+//    4 k_q; C_p = RN((A_R + 1020 - v_p*1020) * 2^-149) is an exact integer).
+//    The LDS takes that register as its address: no integer adds, no keys;
+//  - sums go straight into float2 accumulators (no per-row combine);
+//  - the 11th column of outputs r and r+1 runs as one packed pair (the window
+//    row offsets differ by one; a -inf exponent zeroes a row outside a window).
+// The FP32 error of the longer sum chains is budgeted in DESIGN.md §3.
 //
 // all = 0 (the pipeline): s~ is consumed only by the Sobel of road-mask pixels
 // (k_sobel_refine), i.e. within one pixel of a masked pixel (mirroring at the
 // border stays within that pixel). Tiles whose one-pixel ring holds no masked
 // pixel are skipped; the test is the exact mask of k_sobel_refine
 // (road_mask, preprocess.hpp:14-25). all = 1 computes every tile (lk_fast_path_error).
+__device__ __forceinline__ float lds_f32(unsigned addr) {
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
 //
-// The table is replicated RC times, entry-major (word i * RC + copy), and lane
-// L reads copy L % RC: lanes with different entries then collide in a bank
-// at most 32 / RC ways (RC = 16: 2-way) instead of up to 16-way.
+// Range table: R[|k_q - k_p|] (R is even: the reference's dr * dr), 256
+// entries replicated 32 times, entry-major (word 32 |delta| + lane): lane L
+// always reads bank L, so a warp's lookup is one wavefront whatever the
+// differences (a single copy averaged ~3.1 wavefronts per lookup). The index
+// FFMA2 takes |dr| (dr is already there for the MUFU pairs' exponent), so the
+// address constant is per lane, not per output. The 32 KB table is staged once
+// per CTA, which walks TPC consecutive tiles to amortise it.
+//
+// Staging is software-pipelined: the grey bytes of the CTA's next needed tile
+// are loaded into registers before the current tile's taps run, so their
+// global latency hides behind ~10^4 cycles of arithmetic (the old per-tile
+// load -> barrier -> compute sequence left ~30 % of the stall samples on the
+// staging loads). Which tiles are needed comes from k_bf_flags.
+constexpr int BF_PF = (BT_W + 10) * (BT_H + 10) / 256 + 1;  // prefetched bytes per thread
+
+template <int RHO>
+__device__ __forceinline__ void bf_issue(const Dev& d, int nbx, int nb, int t, uint32_t (&pb)[BF_PF]) {
+    constexpr int TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO, NPX = TWh * THh;
+    const int f = t / nb, tr = t - f * nb, by = tr / nbx, bx = tr - by * nbx;
+    const int u0 = bx * BT_W - RHO, v0 = by * BT_H - RHO;
+    const uint8_t* g = d.grey + (size_t)f * d.px;
+    const bool inner = u0 >= 0 && v0 >= 0 && u0 + TWh <= d.W && v0 + THh <= d.H;
+#pragma unroll
+    for (int k = 0; k < BF_PF; ++k) {
+        const int i = threadIdx.x + 256 * k;
+        if (i < NPX) {
+            const int ry = i / TWh, rx = i - ry * TWh;
+            int v = v0 + ry, u = u0 + rx;
+            if (!inner) {
+                v = mirror(v, d.H);
+                u = mirror(u, d.W);
+            }
+            pb[k] = __ldg(g + (size_t)v * d.W + u);
+        }
+    }
+}
+
 template <int RHO, int TB>
-__global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p, int all) {
+__global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p, int n, int tpc, int all) {
     constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
     constexpr int NPX = TWh * THh;
-    constexpr int RC = BF_TABLE_COPIES;
-    static_assert(WIN == 11, "packed tap pairs assume an 11-wide window");
-    __shared__ float s_v[NPX], s_vf[256], s_R[TB ? 512 * RC : 1];
-    __shared__ int s_row[THh], s_col[TWh];
-    const int f = blockIdx.z;
-    if (frame_failed(d, f)) return;
-    const int u0 = blockIdx.x * BT_W, v0 = blockIdx.y * BT_H;
-    if (!all) {
-        const int horizon = (int)d.rep[f].horizon;
-        if (v0 + BT_H < horizon) return;  // ring rows all above the horizon
-        const uint8_t* dp = d.disp + (size_t)f * d.px;
-        const double* fv = d.fv + (size_t)f * d.H;
-        int any = 0;
-        for (int i = threadIdx.x; i < (BT_H + 2) * (BT_W + 2) && !any; i += blockDim.x) {
-            const int r = i / (BT_W + 2), c = i - r * (BT_W + 2);
-            const int v = v0 - 1 + r, u = u0 - 1 + c;
-            if (v >= horizon && v >= 0 && v < d.H && u >= 0 && u < d.W) {
-                const int dv = dp[(size_t)v * d.W + u];
-                any = dv != 0 && fabs((double)dv - fv[v]) <= d.varpi;
-            }
-        }
-        if (!__syncthreads_or(any)) return;
+    static_assert(WIN == 11 && BT_R % 2 == 0 && TWh % 2 == 0, "packed pairs assume an 11-wide window");
+    __shared__ __align__(16) float s_v[2][NPX + 2];
+    __shared__ __align__(16) float s_R[TB ? 256 * 32 : 4];
+    const int nbx = (d.W + BT_W - 1) / BT_W, nb = nbx * ((d.H + BT_H - 1) / BT_H);
+    const int tile0 = blockIdx.x * tpc, tile1 = min(tile0 + tpc, n * nb);
+    // needed tiles of this chunk (tpc <= 32): one ballot, the same in every warp
+    unsigned need;
+    {
+        const int t = tile0 + (threadIdx.x & 31);
+        bool nd = false;
+        if (t < tile1) nd = all ? !frame_failed(d, t / nb) : d.bf_flag[t] != 0;
+        need = __ballot_sync(0xffffffffu, nd);
     }
-    const uint8_t* g = d.grey + (size_t)f * d.px;
-    s_vf[threadIdx.x] = __ldg(d.fast_tab + threadIdx.x);
-    if (TB) {
-        const float r0 = __ldg(d.fast_tab + 256 + threadIdx.x);
-        const float r1 = __ldg(d.fast_tab + 512 + threadIdx.x);
-#pragma unroll
-        for (int k = 0; k < RC; ++k) {
-            s_R[threadIdx.x * RC + k] = r0;
-            s_R[(threadIdx.x + 256) * RC + k] = r1;
-        }
-    }
-    if (threadIdx.x < THh) s_row[threadIdx.x] = mirror(v0 + (int)threadIdx.x - RHO, d.H) * d.W;
-    if (threadIdx.x < TWh) s_col[threadIdx.x] = mirror(u0 + (int)threadIdx.x - RHO, d.W);
-    __syncthreads();
-    for (int i = threadIdx.x; i < NPX; i += blockDim.x) {
-        const int ty = i / TWh, tx = i - ty * TWh;
-        s_v[i] = s_vf[g[(size_t)s_row[ty] + s_col[tx]]];
-    }
-    __syncthreads();
+    if (!need) return;
     const int tx = threadIdx.x % BT_W, ty = threadIdx.x / BT_W;
     const int r0 = ty * BT_R;
-    float va[BT_R], num[BT_R], den[BT_R];
-    float2 nva[BT_R];
+    // aligned base of this thread's window rows: element (row, tx + k) is
+    // base[row * TWh + k] in both cases (copy 1 holds element i at i + 1)
+    const float* base = (tx & 1) ? &s_v[1][tx + 1] : &s_v[0][tx];
+    const float kA = __int_as_float(128 * 255);  // |dr| * 32640 * 2^-149 = 128 |delta| (subnormal)
+    const float cb = __int_as_float((int)((unsigned)__cvta_generic_to_shared(s_R) + 4u * (threadIdx.x % 32)));
+    const float2 c2 = make_float2(p.c2, p.c2), kA2 = make_float2(kA, kA), cb2 = make_float2(cb, cb);
+    uint32_t pb[BF_PF];
+    int cur = tile0 + __ffs(need) - 1;
+    need &= need - 1;
+    bf_issue<RHO>(d, nbx, nb, cur, pb);
+    if (TB) {
+        const float r = __ldg(d.fast_tab + 256 + 255 + threadIdx.x);  // R[|delta| = tid]
 #pragma unroll
-    for (int r = 0; r < BT_R; ++r) {
-        va[r] = s_v[(r0 + r + RHO) * TWh + tx + RHO];
-        nva[r] = make_float2(-va[r], -va[r]);
-        num[r] = den[r] = 0.f;
+        for (int k = 0; k < 32; k += 4)
+            *reinterpret_cast<float4*>(&s_R[threadIdx.x * 32 + k]) = make_float4(r, r, r, r);
     }
-    const float2 c2 = make_float2(p.c2, p.c2);
-    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float + kMagic rounds to an integer
-    // t = dr*S + kMagic + S, S = 4 * 255 * RC: its bit pattern is
-    // __float_as_int(kMagic) + the BYTE offset 4 * RC * (k_q - k_p + 255) of the
-    // entry, so the LDS needs one add of the thread's base (its copy) only
-    constexpr float kS = 1020.f * RC;
-    const float2 kscale = make_float2(kS, kS), mg = make_float2(kMagic + kS, kMagic + kS);
-    const char* Rb = reinterpret_cast<const char*>(s_R) + 4 * (threadIdx.x % RC) -
-                     __float_as_int(kMagic);
+    while (true) {
+        __syncthreads();  // the previous tile's taps are done with s_v
 #pragma unroll
-    for (int jj = 0; jj < BT_R + 2 * RHO; ++jj) {
-        const int prow = (r0 + jj) * TWh + tx;
-        float2 vp[5];
-#pragma unroll
-        for (int q = 0; q < 5; ++q) vp[q] = make_float2(s_v[prow + 2 * q], s_v[prow + 2 * q + 1]);
-        const float vl = s_v[prow + 10];
+        for (int k = 0; k < BF_PF; ++k) {
+            const int i = threadIdx.x + 256 * k;
+            if (i < NPX) {
+                const float v = __ldg(d.fast_tab + pb[k]);  // (float)(k / 255.0), an L1 hit
+                s_v[0][i] = v;
+                s_v[1][i + 1] = v;  // copy 1 is shifted: s_v[1][i] = s_v[0][i - 1]
+            }
+        }
+        __syncthreads();
+        const int f = cur / nb, tr = cur - f * nb, by = tr / nbx, bx = tr - by * nbx;
+        const int u0 = bx * BT_W, v0 = by * BT_H;
+        const int nxt = need ? tile0 + __ffs(need) - 1 : -1;
+        need &= need - 1;
+        if (nxt >= 0) bf_issue<RHO>(d, nbx, nb, nxt, pb);  // in flight during the taps below
+        float va[BT_R];
+        float2 nva[BT_R], num[BT_R], den[BT_R];
 #pragma unroll
         for (int r = 0; r < BT_R; ++r) {
-            const int dj = jj - r;
-            if (dj < 0 || dj >= WIN) continue;
-            // row partial sums keep the FP32 error small (two interleaved chains)
-            float2 rn = make_float2(0.f, 0.f), rd = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int q = 0; q < 5; ++q) {
-                const float2 dr = __fadd2_rn(vp[q], nva[r]);
-                float2 w;
-                if ((TB >> q) & 1) {
-                    const float2 t = __ffma2_rn(dr, kscale, mg);
-                    w = __fmul2_rn(p.sp[dj][q],
-                                   make_float2(*reinterpret_cast<const float*>(Rb + __float_as_int(t.x)),
-                                               *reinterpret_cast<const float*>(Rb + __float_as_int(t.y))));
-                } else {
-                    const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.cp[dj][q]);
-                    w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-                }
-                rn = __ffma2_rn(w, vp[q], rn);
-                rd = __fadd2_rn(w, rd);
-            }
-            const float dr = vl - va[r];
-            const float w = ex2_approx(fmaf(p.c2, dr * dr, p.c[dj * WIN + 10]));
-            num[r] += fmaf(w, vl, rn.x + rn.y);
-            den[r] += (rd.x + rd.y) + w;
+            va[r] = base[(r0 + r + RHO) * TWh + RHO];
+            nva[r] = make_float2(-va[r], -va[r]);
+            num[r] = den[r] = make_float2(0.f, 0.f);
         }
-    }
-    const int u = u0 + tx;
+        float2 n11[BT_R / 2], d11[BT_R / 2], nv11[BT_R / 2];
 #pragma unroll
-    for (int r = 0; r < BT_R; ++r) {
-        const int v = v0 + r0 + r;
-        if (u < d.W && v < d.H)
-            d.smoothed_f[(size_t)f * d.px + (size_t)v * d.W + u] = __fdiv_rn(num[r], den[r]);
+        for (int m = 0; m < BT_R / 2; ++m) {
+            n11[m] = d11[m] = make_float2(0.f, 0.f);
+            nv11[m] = make_float2(-va[2 * m], -va[2 * m + 1]);
+        }
+#pragma unroll
+        for (int jj = 0; jj < BT_R + 2 * RHO; ++jj) {
+            const float* row = base + (r0 + jj) * TWh;
+            float2 vp[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) vp[q] = *reinterpret_cast<const float2*>(row + 2 * q);
+            const float vl = row[10];
+#pragma unroll
+            for (int r = 0; r < BT_R; ++r) {
+                const int dj = jj - r;
+                if (dj < 0 || dj >= WIN) continue;
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    const float2 dr = __fadd2_rn(vp[q], nva[r]);
+                    float2 w;
+                    if ((TB >> q) & 1) {
+                        const float2 t = __ffma2_rn(make_float2(fabsf(dr.x), fabsf(dr.y)), kA2, cb2);
+                        w = __fmul2_rn(p.sp[dj][q], make_float2(lds_f32(__float_as_uint(t.x)),
+                                                                lds_f32(__float_as_uint(t.y))));
+                    } else {
+                        const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.cp[dj][q]);
+                        w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                    }
+                    num[r] = __ffma2_rn(w, vp[q], num[r]);
+                    den[r] = __fadd2_rn(w, den[r]);
+                }
+            }
+            // 11th column: outputs (2m, 2m + 1) use window rows (jj - 2m, jj - 2m - 1)
+#pragma unroll
+            for (int m = 0; m < BT_R / 2; ++m) {
+                const int k = jj - 2 * m;
+                if (k < 0 || k > WIN) continue;
+                const float2 vl2 = make_float2(vl, vl);
+                const float2 dr = __fadd2_rn(vl2, nv11[m]);
+                const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.c10[k]);
+                const float2 w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                n11[m] = __ffma2_rn(w, vl2, n11[m]);
+                d11[m] = __fadd2_rn(w, d11[m]);
+            }
+        }
+        const int u = u0 + tx;
+#pragma unroll
+        for (int r = 0; r < BT_R; ++r) {
+            const int v = v0 + r0 + r;
+            const float a = (r & 1) ? n11[r / 2].y : n11[r / 2].x;
+            const float b = (r & 1) ? d11[r / 2].y : d11[r / 2].x;
+            if (u < d.W && v < d.H)
+                d.smoothed_f[(size_t)f * d.px + (size_t)v * d.W + u] =
+                    __fdiv_rn((num[r].x + num[r].y) + a, (den[r].x + den[r].y) + b);
+        }
+        if (nxt < 0) break;
+        cur = nxt;
+    }
+}
+
+// Which fast-bilateral tiles the pipeline needs: s~ is read only by the Sobel
+// of road-mask pixels (k_sobel_refine), i.e. within one pixel of a masked
+// pixel (mirroring at the border stays within that pixel). Flag = some pixel
+// of the tile's one-pixel ring is in road_mask (preprocess.hpp:14-25, the exact
+// test k_sobel_refine applies). One CTA per (tile row, frame); failed frames
+// and bands above the horizon get 0.
+__global__ void __launch_bounds__(256) k_bf_flags(Dev d) {
+    __shared__ unsigned s_bits[(65536 + 31) / 32];
+    const int f = blockIdx.y, by = blockIdx.x, v0 = by * BT_H;
+    const int nbx = (d.W + BT_W - 1) / BT_W;
+    uint8_t* out = d.bf_flag + (size_t)f * nbx * gridDim.x + (size_t)by * nbx;
+    const int horizon = frame_failed(d, f) ? INT_MAX : (int)d.rep[f].horizon;
+    if (v0 + BT_H < horizon) {
+        for (int bx = threadIdx.x; bx < nbx; bx += blockDim.x) out[bx] = 0;
+        return;
+    }
+    const uint8_t* dp = d.disp + (size_t)f * d.px;
+    const double* fv = d.fv + (size_t)f * d.H;
+    const int ra = max(max(v0 - 1, horizon), 0), rb = min(v0 + BT_H, d.H - 1);
+    const int nw = (d.W + 31) / 32;
+    for (int c0 = threadIdx.x & ~31; c0 < nw * 32; c0 += blockDim.x) {
+        const int c = c0 + (threadIdx.x & 31);
+        bool any = false;
+        if (c < d.W)
+            for (int r = ra; r <= rb && !any; ++r) {
+                const int dv = dp[(size_t)r * d.W + c];
+                any = dv != 0 && fabs((double)dv - fv[r]) <= d.varpi;
+            }
+        const unsigned b = __ballot_sync(0xffffffffu, any);
+        if ((threadIdx.x & 31) == 0) s_bits[c0 >> 5] = b;
+    }
+    __syncthreads();
+    for (int bx = threadIdx.x; bx < nbx; bx += blockDim.x) {
+        const int lo = max(bx * BT_W - 1, 0), hi = min(bx * BT_W + BT_W, d.W - 1);
+        bool any = false;
+        for (int w = lo >> 5; w <= (hi >> 5) && !any; ++w) {
+            unsigned m = s_bits[w];
+            if (w == (lo >> 5)) m &= ~0u << (lo & 31);
+            if (w == (hi >> 5)) m &= (hi & 31) == 31 ? ~0u : (1u << ((hi & 31) + 1)) - 1u;
+            any = m != 0;
+        }
+        out[bx] = any;
     }
 }
 
@@ -408,12 +516,16 @@ __global__ void __launch_bounds__(256, 3) k_sobel_refine(Dev d, WsParam ws) {
 
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all) {
     const dim3 g((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n);
+    const int tpc = std::min(32, std::max(1, lp.fast_tpc));
+    const int pg = (int)((g.x * g.y * g.z + tpc - 1) / tpc);
+    if (!all)
+        k_bf_flags<<<dim3((d.H + BT_H - 1) / BT_H, n), 256, 0, s>>>(d);
     switch (lp.fast_table) {
 #define LK_BF(M) \
-    case M: k_bilateral_fast<5, M><<<g, 256, 0, s>>>(d, lp.fbf, all); break;
-        LK_BF(0) LK_BF(2) LK_BF(10) LK_BF(14) LK_BF(21) LK_BF(27) LK_BF(31)
+    case M: k_bilateral_fast<5, M><<<pg, 256, 0, s>>>(d, lp.fbf, n, tpc, all); break;
+        LK_BF(0) LK_BF(10) LK_BF(14) LK_BF(21) LK_BF(27) LK_BF(31)
 #undef LK_BF
-        default: k_bilateral_fast<5, 10><<<g, 256, 0, s>>>(d, lp.fbf, all); break;
+        default: k_bilateral_fast<5, 21><<<pg, 256, 0, s>>>(d, lp.fbf, n, tpc, all); break;
     }
 }
 

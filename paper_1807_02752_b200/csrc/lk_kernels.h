@@ -11,11 +11,6 @@ constexpr int K1_ROWS = 8;              // rows per v-disparity CTA
 constexpr int BF_TW = 32, BF_TH = 8;    // bilateral tile (generic window)
 constexpr int BT_W = 64, BT_H = 16, BT_R = 4;  // bilateral tile (11x11), outputs per thread
 constexpr int BT_TRI_N = 128;           // max distinct values per tile for the smem sub-table
-#ifndef BF_TABLE_COPIES
-#define BF_TABLE_COPIES 1               // fast-bilateral range table replicas: 1 is fastest
-                                        // (neighbouring lanes mostly read the same entry and
-                                        // get broadcast; 16 copies measured 1.5x slower)
-#endif
 constexpr int K4_THREADS = 512;         // V_px CTA (2 per SM)
 #ifndef GAMMA_NW
 #define GAMMA_NW 8                      // RANSAC-gamma warps = speculative iterations per round
@@ -37,8 +32,8 @@ struct FastBfParam {
     float2 cp[11][5];  // c of taps (2q, 2q+1) of window row dj: packed f32x2 operands
     float2 sp[11][5];  // the same taps' spatial factors 2^c (range-table taps)
     float c[121];  // -ds * inv_s2 * log2(e) per tap
+    float2 c10[12];  // 11th-column pair (c[k][10], c[k-1][10]), -inf outside the window
     float c2;      // -inv_r2 * log2(e)
-    float vf[256]; // k / 255
 };
 
 struct LaunchPlan {
@@ -46,6 +41,7 @@ struct LaunchPlan {
     FastBfParam fbf;
     int fast_front;           // certified fast bilateral + exact refinement (lk_fastpath.cu)
     int fast_table;           // mask of tap pairs whose range factor comes from the smem table
+    int fast_tpc;             // fast-bilateral tiles per CTA (LK_BF_TPC)
     int32_t* vhistT;          // [B][D1][H] transposed v-disparity for the v-path DP
     size_t vpath_smem;
     int vpath_choice_smem;    // choices of the v-path DP kept in shared memory
