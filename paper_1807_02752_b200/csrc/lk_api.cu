@@ -361,7 +361,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     A(&d_wr, wr.size());
     A(&d_val, val.size());
     A(&d_rng, rng.size());
-    A(&c->in_grey, (size_t)B * d.px);
+    A(&c->in_grey, (size_t)B * d.px + 16);  // +16: k_refine_exact reads rows as whole words
     A(&c->in_disp, (size_t)B * d.px);
     if (d.stereo) {
         A(&c->in_right, (size_t)B * d.px);
@@ -485,9 +485,17 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         const char* tpc = std::getenv("LK_BF_TPC");  // tiles per CTA
         lp.fast_tpc = tpc ? std::atoi(tpc) : 24;
         d.bf_ntiles = ((W + lkg::BT_W - 1) / lkg::BT_W) * ((H + lkg::BT_H - 1) / lkg::BT_H);
+        d.n_stile = ((W + lkg::SB_TW - 1) / lkg::SB_TW) * ((H + lkg::SB_TH - 1) / lkg::SB_TH);
+        d.need_cap = d.n_stile * (lkg::SB_TW + 2) * (lkg::SB_TH + 2);  // every ring pixel of every tile
+        lp.refine_ctas = 8;
+        lp.decide_ctas = 32;
         if (lp.fast_front) {
             A(&d.smoothed_f, (size_t)B * d.px);
             A(&d.bf_flag, (size_t)B * d.bf_ntiles);
+            A(&d.need, (size_t)B * d.need_cap);
+            A(&d.need_cnt, (size_t)B);
+            A(&d.ctile, (size_t)B * d.n_stile);
+            A(&d.ctile_cnt, (size_t)B);
         }
         A(&d_ft, fast_tab.size());
     }
@@ -669,6 +677,10 @@ static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     sh(v.smoothed, px);
     sh(v.smoothed_f, px);
     sh(v.bf_flag, (size_t)d.bf_ntiles);
+    sh(v.need, (size_t)d.need_cap);
+    sh(v.need_cnt, 1);
+    sh(v.ctile, (size_t)d.n_stile);
+    sh(v.ctile_cnt, 1);
     sh(v.ebits, H * d.words_per_row);
     sh(v.seg_cnt, H * d.n_seg);
     sh(v.seg_off, H * d.n_seg);
@@ -869,7 +881,7 @@ lk_status lk_submit_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* dispari
     if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
     CU(cudaSetDevice(c->device));
     if (!c->copy_stream) {  // first use: the second input slot and the copy stream
-        if (lk_status s = c->alloc(&c->slot_grey[1], (size_t)c->max_batch * c->d.px)) return s;
+        if (lk_status s = c->alloc(&c->slot_grey[1], (size_t)c->max_batch * c->d.px + 16)) return s;
         if (lk_status s = c->alloc(&c->slot_disp[1], (size_t)c->max_batch * c->d.px)) return s;
         c->slot_grey[0] = c->in_grey;
         c->slot_disp[0] = c->in_disp;

@@ -87,6 +87,12 @@ struct Dev {
     float* smoothed_f;      // [B][H][W] certified approximation (fast path)
     uint8_t* bf_flag;       // [B][bf_ntiles] fast-bilateral tiles the Sobel screen needs
     int bf_ntiles;          // fast-bilateral tiles per frame
+    uint32_t* need;         // [B][need_cap] pixels (v << 16 | u) whose exact smoothed value the
+                            // fast path needs (3x3 neighbourhoods of Sobel candidates)
+    uint32_t* need_cnt;     // [B]
+    uint32_t* ctile;        // [B][n_stile] Sobel tiles holding candidates
+    uint32_t* ctile_cnt;    // [B]
+    int need_cap, n_stile;
     const float* fast_tab;  // [256] k/255 as float, then [512] range factor of dr = (i-255)/255
     uint32_t* ebits;        // [B][H][words_per_row]
     int n_seg;              // edge-list segments per row (ceil(W / SB_TW))

@@ -239,6 +239,10 @@ __global__ void __launch_bounds__(256) k_bf_flags(Dev d) {
     const int f = blockIdx.y, by = blockIdx.x, v0 = by * BT_H;
     const int nbx = (d.W + BT_W - 1) / BT_W;
     uint8_t* out = d.bf_flag + (size_t)f * nbx * gridDim.x + (size_t)by * nbx;
+    if (by == 0 && threadIdx.x == 0) {  // the Sobel screen appends to these lists
+        d.need_cnt[f] = 0;
+        d.ctile_cnt[f] = 0;
+    }
     const int horizon = frame_failed(d, f) ? INT_MAX : (int)d.rep[f].horizon;
     if (v0 + BT_H < horizon) {
         for (int bx = threadIdx.x; bx < nbx; bx += blockDim.x) out[bx] = 0;
@@ -315,9 +319,17 @@ __device__ __forceinline__ double exact_bilateral(const Dev& d, const WsParam& w
 
 // ---- 2. Sobel on s~ with the propagated bound, exact refinement, edge bits
 //
-// Tile SB_TW x SB_TH, 256 threads; thread t owns pixels (row (t>>7) + 2k,
-// col t & 127), k < 4, so each warp covers 32 consecutive pixels of a row
-// and its ballot is a candidate / edge word directly.
+// Three kernels, so that the exact FP64 refinement (a 121-tap dependent
+// chain per pixel, ~1.6 % of the pixels) runs at full occupancy instead of
+// leaving most of a tile's threads waiting at a barrier:
+//   k_sobel_screen  (tile 128 x 8): FP32 Sobel of s~ with the certified bound
+//                   below; candidate bits -> ebits, need pixels (the 3x3
+//                   neighbourhoods of candidates) -> the frame's need list,
+//                   candidate tiles -> the frame's tile list;
+//   k_refine_exact  one thread per need pixel: the exact LUT bilateral
+//                   (preprocess.hpp:38-56) -> smoothed;
+//   k_sobel_decide  per candidate tile: the exact Sobel of the candidates ->
+//                   edge bits, segment counts, edge count.
 //
 // Candidate screening runs in FP32 on s~ (values in [0, 1]). Its rounding
 // error is folded into the certified bound: each FP32 Sobel component is
@@ -328,21 +340,20 @@ __device__ __forceinline__ double exact_bilateral(const Dev& d, const WsParam& w
 // s_f = fl32(gx_f^2 + gy_f^2). ds below over-covers this (x1.001, +4e-7 s_f,
 // +1e-9) and the test uses s*_lo = the largest float <= s*, so every pixel
 // with s >= s* is a candidate.
-template <int RHO>
-__global__ void __launch_bounds__(256, 3) k_sobel_refine(Dev d, WsParam ws) {
-    constexpr int FW = SB_TW + 2, FH = SB_TH + 2;               // tile + 1-px ring
-    constexpr int GW = SB_TW + 2 + 2 * RHO, GH = SB_TH + 2 + 2 * RHO;  // grey for the ring
-    constexpr int NWORD = (FW + 31) / 32;                       // ring row bitmap words
-    constexpr int TWORD = SB_TW / 32;                           // tile row bitmap words
-    constexpr int NF = (FH * FW + 255) / 256, NG = (GH * GW + 255) / 256;
+//
+// Thread t of a tile owns pixels (row (t>>7) + 2k, col t & 127), k < 4, so
+// each warp covers 32 consecutive pixels of a row and its ballot is a
+// candidate / edge word directly.
+__global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
+    constexpr int FW = SB_TW + 2, FH = SB_TH + 2;  // tile + 1-px ring
+    constexpr int NWORD = (FW + 31) / 32;          // ring row bitmap words
+    constexpr int TWORD = SB_TW / 32;              // tile row bitmap words
+    constexpr int NF = (FH * FW + 255) / 256;
     static_assert(SB_TW == 128 && SB_TH == 8, "pixel ownership assumes a 128 x 8 tile");
     __shared__ float s_f[FH * FW];
-    __shared__ uint8_t s_g[GH * GW];
-    __shared__ double s_ex[FH * FW];
-    __shared__ double s_val[256];
-    __shared__ short s_need[FH * FW];
     __shared__ unsigned s_cw[SB_TH][TWORD];
-    __shared__ int s_nneed, s_seg[SB_TH], s_tot[2];
+    __shared__ unsigned s_need[FH][NWORD];
+    __shared__ int s_nneed, s_base;
     const int f = blockIdx.z;
     if (frame_failed(d, f)) return;
     if (d.W < 3 || d.H < 3) {  // preprocess.hpp:68-69
@@ -359,7 +370,6 @@ __global__ void __launch_bounds__(256, 3) k_sobel_refine(Dev d, WsParam ws) {
         return;
     }
     const float* sf = d.smoothed_f + (size_t)f * d.px;
-    const uint8_t* grey = d.grey + (size_t)f * d.px;
     const int pc = tid & (SB_TW - 1), pr0 = tid >> 7;  // owned pixels: (pr0 + 2k, pc)
     // independent loads first: disparity and profile of the owned pixels, s~ tile
     int dv[4];
@@ -372,6 +382,7 @@ __global__ void __launch_bounds__(256, 3) k_sobel_refine(Dev d, WsParam ws) {
         fvv[k] = in ? d.fv[(size_t)f * H + v] : 0.0;
     }
     {
+        const bool inner = u0 >= 1 && v0 >= 1 && u0 + FW - 1 <= W && v0 + FH - 1 <= H;
         float t[NF];
 #pragma unroll
         for (int q = 0; q < NF; ++q) {
@@ -379,20 +390,19 @@ __global__ void __launch_bounds__(256, 3) k_sobel_refine(Dev d, WsParam ws) {
             t[q] = 0.f;
             if (i < FH * FW) {
                 const int r = i / FW, c = i - r * FW;
-                t[q] = sf[(size_t)mirror(v0 - 1 + r, H) * W + mirror(u0 - 1 + c, W)];
+                const int v = inner ? v0 - 1 + r : mirror(v0 - 1 + r, H);
+                const int u = inner ? u0 - 1 + c : mirror(u0 - 1 + c, W);
+                t[q] = sf[(size_t)v * W + u];
             }
         }
 #pragma unroll
         for (int q = 0; q < NF; ++q)
             if (tid + q * 256 < FH * FW) s_f[tid + q * 256] = t[q];
     }
-    if (tid < SB_TH) s_seg[tid] = 0;
-    if (tid < 2) s_tot[tid] = 0;
     if (tid == 0) s_nneed = 0;
     __syncthreads();
     const float D = (float)(8.0 * kEpsSmooth + 1e-6);
     int n_mask = 0, any_cand = 0;
-    unsigned cand_bits = 0;  // bit k: owned pixel k is a candidate
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int r = pr0 + 2 * k, v = v0 + r, u = u0 + pc;
@@ -411,36 +421,26 @@ __global__ void __launch_bounds__(256, 3) k_sobel_refine(Dev d, WsParam ws) {
                              4e-7f * s + 1e-9f;
             cand = s + ds >= d.sobel_s_star_lo;
         }
-        cand_bits |= (unsigned)cand << k;
         const unsigned bal = __ballot_sync(0xffffffffu, cand);
         if (lane == 0) s_cw[r][pc >> 5] = bal;
         any_cand |= cand;
     }
+    for (int o = 16; o; o >>= 1) n_mask += __shfl_xor_sync(0xffffffffu, n_mask, o);
+    if (lane == 0 && n_mask) atomicAdd(&d.aux[f].mask_px, (unsigned long long)n_mask);
     if (!__syncthreads_or(any_cand)) {  // no edge can exist in this tile (most tiles)
-        for (int o = 16; o; o >>= 1) n_mask += __shfl_xor_sync(0xffffffffu, n_mask, o);
-        if (lane == 0 && n_mask) atomicAdd(&d.aux[f].mask_px, (unsigned long long)n_mask);
         if (tid < SB_TH && v0 + tid < H)
             d.seg_cnt[((size_t)f * H + v0 + tid) * d.n_seg + blockIdx.x] = 0;
         return;
     }
-    {  // grey for the exact bilateral of the ring (loads first), k/255 table
-        uint8_t t[NG];
-#pragma unroll
-        for (int q = 0; q < NG; ++q) {
-            const int i = tid + q * 256;
-            t[q] = 0;
-            if (i < GH * GW) {
-                const int r = i / GW, c = i - r * GW;
-                t[q] = grey[(size_t)mirror(v0 - 1 - RHO + r, H) * W + mirror(u0 - 1 - RHO + c, W)];
-            }
-        }
-        s_val[tid] = __ldg(d.val + tid);
-#pragma unroll
-        for (int q = 0; q < NG; ++q)
-            if (tid + q * 256 < GH * GW) s_g[tid + q * 256] = t[q];
+    // candidate words -> ebits (k_sobel_decide keeps the edges among them)
+    if (tid < SB_TH * TWORD) {
+        const int r = tid / TWORD, w = tid - r * TWORD, word = (u0 >> 5) + w;
+        if (v0 + r < H && word < d.words_per_row)
+            d.ebits[((size_t)f * H + v0 + r) * d.words_per_row + word] = s_cw[r][w];
     }
     // pixels of tile + ring inside a candidate's 3x3 need the exact value:
     // ring bit C of ring row R <-> tile (R - 1, C - 1); need = 3x3 dilation
+    unsigned need = 0;
     if (tid < FH * NWORD) {
         const int R = tid / NWORD, w = tid - R * NWORD;
         auto tw = [&](int k) -> unsigned {  // OR of tile rows R-2..R, word k
@@ -453,64 +453,191 @@ __global__ void __launch_bounds__(256, 3) k_sobel_refine(Dev d, WsParam ws) {
         };
         const unsigned t0 = tw(w), t1 = tw(w - 1);
         // (T | T << 1 | T << 2) restricted to ring bits 32w .. 32w + 31
-        unsigned need = t0 | __funnelshift_l(t1, t0, 1) | __funnelshift_l(t1, t0, 2);
+        need = t0 | __funnelshift_l(t1, t0, 1) | __funnelshift_l(t1, t0, 2);
         if (w == NWORD - 1) need &= (FW % 32) ? (1u << (FW % 32)) - 1u : 0xffffffffu;
-        if (need) {
-            int o = atomicAdd(&s_nneed, __popc(need));
-            while (need) {
-                const int bit = __ffs(need) - 1;
-                need &= need - 1;
-                s_need[o++] = (short)(R * FW + 32 * w + bit);
+        s_need[R][w] = need;
+        if (need) atomicAdd(&s_nneed, __popc(need));
+    }
+    __syncthreads();
+    if (tid == 0) {
+        s_base = (int)atomicAdd(&d.need_cnt[f], (unsigned)s_nneed);
+        const unsigned ct = atomicAdd(&d.ctile_cnt[f], 1u);
+        d.ctile[(size_t)f * d.n_stile + ct] = blockIdx.y * gridDim.x + blockIdx.x;
+    }
+    __syncthreads();
+    if (tid < FH * NWORD && need) {
+        const int R = tid / NWORD, w = tid - R * NWORD;
+        int o = s_base;  // this word's slot: the need bits of the words before it
+        for (int j = 0; j < R * NWORD + w; ++j) o += __popc(s_need[j / NWORD][j % NWORD]);
+        uint32_t* out = d.need + (size_t)f * d.need_cap;
+        // ring positions outside the image hold their mirror pixel (preprocess.hpp:71-72)
+        const int v = mirror(v0 - 1 + R, H);
+        while (need) {
+            const int bit = __ffs(need) - 1;
+            need &= need - 1;
+            const int u = mirror(u0 - 1 + 32 * w + bit, W);
+            out[o++] = ((uint32_t)v << 16) | (uint32_t)u;
+        }
+    }
+}
+
+// Exact bilateral of one need pixel (u, v) straight from global memory: the
+// arithmetic of k_bilateral_tile / preprocess.hpp:38-56, j-major / i-minor,
+// the grey bytes and weight-table gathers of row j+1 issued before row j's
+// dependent add chain. One thread per pixel keeps every SM full of chains.
+// k/255.0 comes from shared memory; an interior window row is read as four
+// 32-bit words (the input buffers carry 16 bytes of padding).
+template <int RHO>
+__device__ __forceinline__ void refine_row(const uint8_t* g, size_t rowoff, const int (&col)[2 * RHO + 1],
+                                           bool inner, int u, uint8_t (&k)[2 * RHO + 1]) {
+    constexpr int WIN = 2 * RHO + 1;
+    static_assert(WIN <= 13, "four words cover the row");
+    if (inner) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(g + rowoff + u - RHO);
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+        const unsigned sh = 8u * (unsigned)(a & 3);
+        uint32_t x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = __ldg(w + i);
+        uint32_t y[4];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) y[i] = __funnelshift_r(x[i], x[i + 1], sh);
+        y[3] = x[3] >> sh;
+#pragma unroll
+        for (int i = 0; i < WIN; ++i) k[i] = (uint8_t)(y[i >> 2] >> (8 * (i & 3)));
+    } else {
+#pragma unroll
+        for (int i = 0; i < WIN; ++i) k[i] = __ldg(g + rowoff + col[i]);
+    }
+}
+
+template <int RHO>
+__global__ void __launch_bounds__(256) k_refine_exact(Dev d, WsParam ws) {
+    constexpr int WIN = 2 * RHO + 1;
+    __shared__ double s_val[256];
+    const int f = blockIdx.y;
+    if (frame_failed(d, f)) return;
+    const unsigned cnt = d.need_cnt[f];
+    if (blockIdx.x * blockDim.x >= cnt) return;
+    s_val[threadIdx.x] = __ldg(d.val + threadIdx.x);
+    __syncthreads();
+    const uint32_t* list = d.need + (size_t)f * d.need_cap;
+    const uint8_t* g = d.grey + (size_t)f * d.px;
+    const int W = d.W, H = d.H;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const uint32_t e = list[i];
+        const int v = (int)(e >> 16), u = (int)(e & 0xffffu);
+        const bool inner = u >= RHO && v >= RHO && u + RHO < W && v + RHO < H;
+        int col[WIN];
+#pragma unroll
+        for (int k = 0; k < WIN; ++k) col[k] = inner ? u - RHO + k : mirror(u - RHO + k, W);
+        auto rowoff = [&](int j) {
+            return (size_t)(inner ? v - RHO + j : mirror(v - RHO + j, H)) * W;
+        };
+        const double* wrow = d.wr + (int)g[(size_t)v * W + u] * 256;
+        double num = 0.0, den = 0.0;
+        uint8_t k_cur[WIN];
+        double wr_cur[WIN];
+        refine_row<RHO>(g, rowoff(0), col, inner, u, k_cur);
+#pragma unroll
+        for (int k = 0; k < WIN; ++k) wr_cur[k] = __ldg(wrow + k_cur[k]);
+#pragma unroll 1
+        for (int j = 0; j < WIN; ++j) {
+            uint8_t k_nxt[WIN];
+            double wr_nxt[WIN];
+            if (j + 1 < WIN) {
+                refine_row<RHO>(g, rowoff(j + 1), col, inner, u, k_nxt);
+#pragma unroll
+                for (int k = 0; k < WIN; ++k) wr_nxt[k] = __ldg(wrow + k_nxt[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < WIN; ++k) {
+                const double w = ws.w[j * WIN + k] * wr_cur[k];
+                num += w * s_val[k_cur[k]];
+                den += w;
+            }
+#pragma unroll
+            for (int k = 0; k < WIN; ++k) {
+                k_cur[k] = k_nxt[k];
+                wr_cur[k] = wr_nxt[k];
             }
         }
+        d.smoothed[(size_t)f * d.px + (size_t)v * W + u] = num / den;
     }
-    __syncthreads();
-    const int gx0 = u0 - 1 - RHO, gy0 = v0 - 1 - RHO;
-    for (int k = tid; k < s_nneed; k += blockDim.x) {
-        const int i = s_need[k];
-        const int r = i / FW, c = i - r * FW;
-        // ring positions outside the image hold their mirror pixel (preprocess.hpp:71-72)
-        const int v = mirror(v0 - 1 + r, H), u = mirror(u0 - 1 + c, W);
-        const double e = exact_bilateral<RHO>(d, ws, s_g, s_val, GW, gx0, gy0, u, v);
-        s_ex[i] = e;
-        d.smoothed[(size_t)f * d.px + (size_t)v * W + u] = e;  // read back by k_edge_emit
-    }
-    __syncthreads();
-    int n_edge = 0;
+}
+
+// Exact Sobel (preprocess.hpp:76-81) of the candidates of each candidate
+// tile, on the exact smoothed values k_refine_exact wrote for their 3x3
+// neighbourhoods: edge bits replace the candidate bits, then the segment and
+// edge counts the scan and the report need.
+__global__ void __launch_bounds__(256) k_sobel_decide(Dev d) {
+    constexpr int FW = SB_TW + 2, FH = SB_TH + 2;
+    constexpr int NF = (FH * FW + 255) / 256;
+    __shared__ double s_ex[FH * FW];
+    __shared__ int s_seg[SB_TH], s_tot;
+    const int f = blockIdx.y;
+    if (frame_failed(d, f)) return;
+    const unsigned cnt = d.ctile_cnt[f];
+    const int W = d.W, H = d.H, tid = threadIdx.x, lane = tid & 31;
+    const int pc = tid & (SB_TW - 1), pr0 = tid >> 7;
+    const double* sm = d.smoothed + (size_t)f * d.px;
+    const int nbx = (W + SB_TW - 1) / SB_TW;
+    for (unsigned t = blockIdx.x; t < cnt; t += gridDim.x) {
+        const int tile = (int)d.ctile[(size_t)f * d.n_stile + t];
+        const int by = tile / nbx, bx = tile - by * nbx;
+        const int u0 = bx * SB_TW, v0 = by * SB_TH;
+        const bool inner = u0 >= 1 && v0 >= 1 && u0 + FW - 1 <= W && v0 + FH - 1 <= H;
+        __syncthreads();  // the previous tile's reads of s_ex are done
+        {
+            double x[NF];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int r = pr0 + 2 * k, v = v0 + r;
-        bool edge = false;
-        if ((cand_bits >> k) & 1) {  // candidate => masked and in the image
-            const double* a = s_ex + r * FW + pc;  // row v-1, col u-1
-            const double* b = a + FW;
-            const double* cc = b + FW;
-            const double gx = (a[2] - a[0]) + 2 * (b[2] - b[0]) + (cc[2] - cc[0]);
-            const double gy = (cc[0] - a[0]) + 2 * (cc[1] - a[1]) + (cc[2] - a[2]);
-            edge = gx * gx + gy * gy >= d.sobel_s_star;
-            n_edge += edge;
+            for (int q = 0; q < NF; ++q) {
+                const int i = tid + q * 256;
+                x[q] = 0.0;
+                if (i < FH * FW) {  // positions outside the need set are never read below
+                    const int r = i / FW, c = i - r * FW;
+                    const int v = inner ? v0 - 1 + r : mirror(v0 - 1 + r, H);
+                    const int u = inner ? u0 - 1 + c : mirror(u0 - 1 + c, W);
+                    x[q] = sm[(size_t)v * W + u];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NF; ++q)
+                if (tid + q * 256 < FH * FW) s_ex[tid + q * 256] = x[q];
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, edge);
-        if (lane == 0 && v < H) {
-            const int word = (u0 + pc) >> 5;
-            if (word < d.words_per_row) d.ebits[((size_t)f * H + v) * d.words_per_row + word] = bal;
-            if (bal) atomicAdd(&s_seg[r], __popc(bal));
+        if (tid < SB_TH) s_seg[tid] = 0;
+        if (tid == 0) s_tot = 0;
+        __syncthreads();
+        int n_edge = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int r = pr0 + 2 * k, v = v0 + r, u = u0 + pc;
+            const bool in = v < H && u < W;
+            const int word = u >> 5;
+            const unsigned cw = in ? d.ebits[((size_t)f * H + v) * d.words_per_row + word] : 0u;
+            bool edge = false;
+            if ((cw >> (u & 31)) & 1) {  // candidate => masked and in the image
+                const double* a = s_ex + r * FW + pc;  // row v-1, col u-1
+                const double* b = a + FW;
+                const double* cc = b + FW;
+                const double gx = (a[2] - a[0]) + 2 * (b[2] - b[0]) + (cc[2] - cc[0]);
+                const double gy = (cc[0] - a[0]) + 2 * (cc[1] - a[1]) + (cc[2] - a[2]);
+                edge = gx * gx + gy * gy >= d.sobel_s_star;
+                n_edge += edge;
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, edge);
+            __syncwarp();
+            if (lane == 0 && v < H && word < d.words_per_row) {
+                d.ebits[((size_t)f * H + v) * d.words_per_row + word] = bal;
+                if (bal) atomicAdd(&s_seg[r], __popc(bal));
+            }
         }
-    }
-    for (int o = 16; o; o >>= 1) {
-        n_edge += __shfl_xor_sync(0xffffffffu, n_edge, o);
-        n_mask += __shfl_xor_sync(0xffffffffu, n_mask, o);
-    }
-    if (lane == 0) {
-        if (n_edge) atomicAdd(&s_tot[0], n_edge);
-        if (n_mask) atomicAdd(&s_tot[1], n_mask);
-    }
-    __syncthreads();
-    if (threadIdx.x < SB_TH && v0 + threadIdx.x < H)
-        d.seg_cnt[((size_t)f * H + v0 + threadIdx.x) * d.n_seg + blockIdx.x] = s_seg[threadIdx.x];
-    if (threadIdx.x == 0) {
-        if (s_tot[0]) atomicAdd(&d.aux[f].edge_px, (unsigned long long)s_tot[0]);
-        if (s_tot[1]) atomicAdd(&d.aux[f].mask_px, (unsigned long long)s_tot[1]);
+        for (int o = 16; o; o >>= 1) n_edge += __shfl_xor_sync(0xffffffffu, n_edge, o);
+        if (lane == 0 && n_edge) atomicAdd(&s_tot, n_edge);
+        __syncthreads();
+        if (tid < SB_TH && v0 + tid < H)
+            d.seg_cnt[((size_t)f * H + v0 + tid) * d.n_seg + bx] = s_seg[tid];
+        if (tid == 0 && s_tot) atomicAdd(&d.aux[f].edge_px, (unsigned long long)s_tot);
     }
 }
 
@@ -531,7 +658,9 @@ void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream
 
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s) {
     const dim3 g((d.W + SB_TW - 1) / SB_TW, (d.H + SB_TH - 1) / SB_TH, n);
-    k_sobel_refine<5><<<g, 256, 0, s>>>(d, lp.ws);
+    k_sobel_screen<<<g, 256, 0, s>>>(d);
+    k_refine_exact<5><<<dim3(lp.refine_ctas, n), 256, 0, s>>>(d, lp.ws);
+    k_sobel_decide<<<dim3(lp.decide_ctas, n), 256, 0, s>>>(d);
 }
 
 // Largest |s~ - s| of a batch (verification of kEpsSmooth): both maps full.

@@ -683,15 +683,11 @@ __global__ void __launch_bounds__(1024) k_edge_scan(Dev d) {
 // segment's bitmap words are walked in u order and each edge is written at
 // its scanned position, so the list order equals the reference's.
 // =====================================================================
-__global__ void __launch_bounds__(256) k_edge_emit(Dev d) {
-    const int f = blockIdx.y;
-    if (frame_failed(d, f)) return;
-    const int lane = threadIdx.x & 31;
-    const int seg = blockIdx.x * 8 + (threadIdx.x >> 5);
+// One warp emits the edges of one 128-px row segment (row v, segment sx).
+__device__ __forceinline__ void emit_segment(const Dev& d, int f, int v, int sx, int lane) {
     const int W = d.W, H = d.H;
-    if (seg >= H * d.n_seg) return;
+    const int seg = v * d.n_seg + sx;
     if (d.seg_cnt[(size_t)f * H * d.n_seg + seg] == 0) return;  // empty segment
-    const int v = seg / d.n_seg, sx = seg - v * d.n_seg;
     const int base = d.seg_off[(size_t)f * H * d.n_seg + seg];
     const double* img = d.smoothed + (size_t)f * d.px;
     const uint32_t* bits = d.ebits + ((size_t)f * H + v) * d.words_per_row;
@@ -735,6 +731,30 @@ __global__ void __launch_bounds__(256) k_edge_emit(Dev d) {
     if (lane == 0) {
         if (n_vote) atomicAdd(&d.aux[f].votes, (unsigned long long)n_vote);
         if (n_skip) atomicAdd(&d.aux[f].skipped, (unsigned long long)n_skip);
+    }
+}
+
+// Exact path: a warp per segment over the whole frame.
+__global__ void __launch_bounds__(256) k_edge_emit(Dev d) {
+    const int f = blockIdx.y;
+    if (frame_failed(d, f)) return;
+    const int seg = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (seg >= d.H * d.n_seg) return;
+    emit_segment(d, f, seg / d.n_seg, seg % d.n_seg, threadIdx.x & 31);
+}
+
+// Fast path: edges exist only in the Sobel screen's candidate tiles (one
+// 128-px segment column x SB_TH rows each), so only those are visited.
+__global__ void __launch_bounds__(32 * SB_TH) k_edge_emit_tiles(Dev d) {
+    const int f = blockIdx.y;
+    if (frame_failed(d, f)) return;
+    const unsigned cnt = d.ctile_cnt[f];
+    const int r = threadIdx.x >> 5;
+    for (unsigned t = blockIdx.x; t < cnt; t += gridDim.x) {
+        const int tile = (int)d.ctile[(size_t)f * d.n_stile + t];
+        const int by = tile / d.n_seg, bx = tile - by * d.n_seg;
+        const int v = by * SB_TH + r;
+        if (v < d.H) emit_segment(d, f, v, bx, threadIdx.x & 31);
     }
 }
 
@@ -1750,7 +1770,10 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
                         s>>>(d);
     }
     k_edge_scan<<<n, 1024, 0, s>>>(d);
-    k_edge_emit<<<dim3((d.H * d.n_seg + 7) / 8, n), 256, 0, s>>>(d);
+    if (lp.fast_front)
+        k_edge_emit_tiles<<<dim3(lp.decide_ctas, n), 32 * SB_TH, 0, s>>>(d);
+    else
+        k_edge_emit<<<dim3((d.H * d.n_seg + 7) / 8, n), 256, 0, s>>>(d);
     mark(10);
     // u-path DP: NT threads x SP consecutive states each (SP = 0: strided fallback)
 #define LK_VANISH(SP, NT) k_vanish<SP, NT><<<n, NT, lp.vanish_smem, s>>>(d)
