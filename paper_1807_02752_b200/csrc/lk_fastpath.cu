@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
     __shared__ float s_f[FH * FW];
     __shared__ unsigned s_cw[SB_TH][TWORD];
     __shared__ unsigned s_need[FH][NWORD];
-    __shared__ int s_nneed, s_base;
+    __shared__ int s_nneed, s_base, s_lo[SB_TH], s_hi[SB_TH];
     const int f = blockIdx.z;
     if (frame_failed(d, f)) return;
     if (d.W < 3 || d.H < 3) {  // preprocess.hpp:68-69
@@ -373,13 +373,38 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
     const int pc = tid & (SB_TW - 1), pr0 = tid >> 7;  // owned pixels: (pr0 + 2k, pc)
     // independent loads first: disparity and profile of the owned pixels, s~ tile
     int dv[4];
-    double fvv[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int v = v0 + pr0 + 2 * k, u = u0 + pc;
-        const bool in = v < H && u < W;
-        dv[k] = in ? d.disp[(size_t)f * d.px + (size_t)v * W + u] : 0;
-        fvv[k] = in ? d.fv[(size_t)f * H + v] : 0.0;
+        dv[k] = v < H && u < W ? d.disp[(size_t)f * d.px + (size_t)v * W + u] : 0;
+    }
+    // road_mask's test |double(d) - f(v)| <= varpi holds, for the integers d
+    // in [1, 255], on an interval [lo_v, hi_v] (fl(d - f) is monotone in d)
+    // inside [f - varpi - 1, f + varpi + 1] (the double subtraction errs by
+    // < 1e-13): thread r finds row v0 + r's interval with the reference's
+    // double expression, then each pixel's test is two integer compares
+    if (tid < SB_TH) {
+        const int v = v0 + tid;
+        int lo = 256, hi = 0;  // empty: rows above the horizon or outside the image
+        if (v < H && v >= horizon) {
+            const double fr = d.fv[(size_t)f * H + v];
+            auto test = [&](int x) { return fabs((double)x - fr) <= d.varpi; };
+            const double a = fr - d.varpi - 1.0, b = fr + d.varpi + 1.0;
+            const int l0 = a >= 1.0 ? (a <= 255.0 ? (int)ceil(a) : 256) : 1;  // NaN -> 1
+            const int h0 = b <= 255.0 ? (b >= 1.0 ? (int)floor(b) : 0) : 255;  // NaN -> 255
+            for (int x = l0; x <= h0; ++x)
+                if (test(x)) {
+                    lo = x;
+                    break;
+                }
+            for (int x = h0; x >= lo; --x)
+                if (test(x)) {
+                    hi = x;
+                    break;
+                }
+        }
+        s_lo[tid] = lo;
+        s_hi[tid] = hi;
     }
     {
         const bool inner = u0 >= 1 && v0 >= 1 && u0 + FW - 1 <= W && v0 + FH - 1 <= H;
@@ -405,9 +430,8 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
     int n_mask = 0, any_cand = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const int r = pr0 + 2 * k, v = v0 + r, u = u0 + pc;
-        const bool m = v < H && u < W && v >= horizon && dv[k] != 0 &&
-                       fabs((double)dv[k] - fvv[k]) <= d.varpi;  // road_mask, preprocess.hpp:14-25
+        const int r = pr0 + 2 * k;
+        const bool m = dv[k] >= s_lo[r] && dv[k] <= s_hi[r];  // road_mask, preprocess.hpp:14-25
         n_mask += m;
         bool cand = false;
         if (m) {
