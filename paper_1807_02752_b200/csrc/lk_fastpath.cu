@@ -322,7 +322,7 @@ __device__ __forceinline__ double exact_bilateral(const Dev& d, const WsParam& w
 // Three kernels, so that the exact FP64 refinement (a 121-tap dependent
 // chain per pixel, ~1.6 % of the pixels) runs at full occupancy instead of
 // leaving most of a tile's threads waiting at a barrier:
-//   k_sobel_screen  (tile 128 x 8): FP32 Sobel of s~ with the certified bound
+//   k_sobel_screen  (tile 128 x SB_TH): FP32 Sobel of s~ with the certified bound
 //                   below; candidate bits -> ebits, need pixels (the 3x3
 //                   neighbourhoods of candidates) -> the frame's need list,
 //                   candidate tiles -> the frame's tile list;
@@ -341,7 +341,7 @@ __device__ __forceinline__ double exact_bilateral(const Dev& d, const WsParam& w
 // +1e-9) and the test uses s*_lo = the largest float <= s*, so every pixel
 // with s >= s* is a candidate.
 //
-// Thread t of a tile owns pixels (row (t>>7) + 2k, col t & 127), k < 4, so
+// Thread t of a tile owns pixels (row (t>>7) + 2k, col t & 127), k < SB_TH / 2, so
 // each warp covers 32 consecutive pixels of a row and its ballot is a
 // candidate / edge word directly.
 __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
     constexpr int NWORD = (FW + 31) / 32;          // ring row bitmap words
     constexpr int TWORD = SB_TW / 32;              // tile row bitmap words
     constexpr int NF = (FH * FW + 255) / 256;
-    static_assert(SB_TW == 128 && SB_TH == 8, "pixel ownership assumes a 128 x 8 tile");
+    static_assert(SB_TW == 128 && SB_TH % 2 == 0, "pixel ownership assumes 128-wide tiles");
     __shared__ float s_f[FH * FW];
     __shared__ unsigned s_cw[SB_TH][TWORD];
     __shared__ unsigned s_need[FH][NWORD];
@@ -372,9 +372,9 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
     const float* sf = d.smoothed_f + (size_t)f * d.px;
     const int pc = tid & (SB_TW - 1), pr0 = tid >> 7;  // owned pixels: (pr0 + 2k, pc)
     // independent loads first: disparity and profile of the owned pixels, s~ tile
-    int dv[4];
+    int dv[SB_PPT];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < SB_PPT; ++k) {
         const int v = v0 + pr0 + 2 * k, u = u0 + pc;
         dv[k] = v < H && u < W ? d.disp[(size_t)f * d.px + (size_t)v * W + u] : 0;
     }
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
     const float D = (float)(8.0 * kEpsSmooth + 1e-6);
     int n_mask = 0, any_cand = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < SB_PPT; ++k) {
         const int r = pr0 + 2 * k;
         const bool m = dv[k] >= s_lo[r] && dv[k] <= s_hi[r];  // road_mask, preprocess.hpp:14-25
         n_mask += m;
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(256) k_sobel_decide(Dev d) {
         __syncthreads();
         int n_edge = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < SB_PPT; ++k) {
             const int r = pr0 + 2 * k, v = v0 + r, u = u0 + pc;
             const bool in = v < H && u < W;
             const int word = u >> 5;

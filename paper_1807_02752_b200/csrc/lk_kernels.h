@@ -19,7 +19,8 @@ constexpr int K4_VOTE_CAP = 8192;       // edges whose vote columns are staged i
 constexpr int BT_CHUNK = 32;            // u-path backtrack: stages per window
 constexpr int BT_SPAN = 5 * BT_CHUNK;   // max drift inside a window (|offset| <= 5)
 constexpr int M_TW = 128;               // m0/m1 tile width
-constexpr int SB_TW = 128, SB_TH = 8;   // Sobel tile; SB_TW is the edge-list segment width
+constexpr int SB_TW = 128, SB_TH = 16;  // Sobel tile; SB_TW is the edge-list segment width
+constexpr int SB_PPT = SB_TH / 2;       // fast-path Sobel pixels per thread (256 threads)
 
 // 11x11 spatial weights exp(-ds*inv_s2), passed by value (constant bank)
 struct WsParam {
