@@ -20,48 +20,60 @@ namespace lkg {
 // Also writes the transposed histogram [D1][H] the v-path DP reads.
 // =====================================================================
 
+// One pixel of build_vdisparity: run-length merged into (key, run) so a road
+// row (one disparity almost everywhere) costs one shared atomic per run.
+__device__ __forceinline__ void vd_pixel(int dv, int row, int D1, int d_max, int32_t* hist,
+                                         int& key, int& run, unsigned long long& valid,
+                                         unsigned long long& counted) {
+    valid += dv != 0;
+    const bool in = dv >= 1 && dv <= d_max;  // road_profile.hpp:42
+    counted += in;
+    const int k = in ? row * D1 + dv : -1;
+    if (k != key) {
+        if (run) atomicAdd(&hist[key], run);
+        key = k;
+        run = 0;
+    }
+    run += in;
+}
+
 __global__ void __launch_bounds__(256) k_vdisparity(Dev d, int32_t* vhistT) {
     extern __shared__ int32_t sh_hist[];  // [K1_ROWS][D1]
     const int f = blockIdx.y;
     const int v0 = blockIdx.x * K1_ROWS;
     const int rows = min(K1_ROWS, d.H - v0);
-    const int D1 = d.D1;
+    const int D1 = d.D1, W = d.W, d_max = d.d_max;
     for (int i = threadIdx.x; i < K1_ROWS * D1; i += blockDim.x) sh_hist[i] = 0;
     __syncthreads();
-    const uint8_t* disp = d.disp + (size_t)f * d.px + (size_t)v0 * d.W;
-    const int npx = rows * d.W;
+    // the CTA's rows as one byte range, read as aligned 16-byte chunks (each
+    // thread walks its chunk's 16 pixels in order) plus an unaligned head and tail
+    const uint8_t* disp = d.disp + (size_t)f * d.px + (size_t)v0 * W;
+    const int npx = rows * W;
+    const int head = min(npx, (int)((16 - (reinterpret_cast<uintptr_t>(disp) & 15)) & 15));
+    const int nchunk = (npx - head) >> 4, tail0 = head + 16 * nchunk;
     unsigned long long valid = 0, counted = 0;
-    // (row, col) of pixel base + tid, advanced incrementally (no division)
-    int row = threadIdx.x / d.W, col = threadIdx.x - row * d.W;
-    for (int base = 0; base < npx; base += blockDim.x) {
-        const int i = base + threadIdx.x;
-        int key = -1;
-        if (i < npx) {
-            const int dv = disp[i];
-            valid += dv != 0;
-            if (dv >= 1 && dv <= d.d_max) key = row * D1 + dv;
-        }
-        col += blockDim.x;
-        while (col >= d.W) {
-            col -= d.W;
-            ++row;
-        }
-        const unsigned active = __ballot_sync(0xffffffffu, key >= 0);
-        if (!active) continue;
-        // a road row has one disparity almost everywhere: one atomic per warp
-        // when every active lane holds the same key, else per distinct key
-        const int kmin = __reduce_min_sync(0xffffffffu, key >= 0 ? key : 0x7fffffff);
-        const int kmax = __reduce_max_sync(0xffffffffu, key);
-        if (key >= 0) {
-            if (kmin == kmax) {
-                if ((threadIdx.x & 31) == __ffs(active) - 1) atomicAdd(&sh_hist[key], __popc(active));
-            } else {
-                const unsigned grp = __match_any_sync(active, key);
-                if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&sh_hist[key], __popc(grp));
+    int key = -1, run = 0;
+    const uint4* chunks = reinterpret_cast<const uint4*>(disp + head);
+    for (int c = threadIdx.x; c < nchunk; c += blockDim.x) {
+        const uint4 q = __ldg(chunks + c);
+        const int i0 = head + 16 * c;
+        int row = i0 / W, col = i0 - row * W;
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            vd_pixel((w[b >> 2] >> (8 * (b & 3))) & 0xff, row, D1, d_max, sh_hist, key, run, valid,
+                     counted);
+            if (++col == W) {
+                col = 0;
+                ++row;
             }
-            counted += 1;
         }
     }
+    for (int i = threadIdx.x; i < head + (npx - tail0); i += blockDim.x) {
+        const int j = i < head ? i : tail0 + (i - head);
+        vd_pixel(disp[j], j / W, D1, d_max, sh_hist, key, run, valid, counted);
+    }
+    if (run) atomicAdd(&sh_hist[key], run);
     for (int o = 16; o; o >>= 1) {
         valid += __shfl_xor_sync(0xffffffffu, valid, o);
         counted += __shfl_xor_sync(0xffffffffu, counted, o);
@@ -145,9 +157,30 @@ __global__ void __launch_bounds__(512) k_vpath(Dev d, const int32_t* vhistT, int
     for (int s = threadIdx.x; s < H; s += blockDim.x)
         prev[s] = -(double)hT[(size_t)d.d_max * H + s];
     __syncthreads();
+    // the next stage's histogram column is loaded while this stage runs, so
+    // the 64 sequential stages do not each wait on a global load
+    constexpr int VP_MAXS = 4;  // states per thread held in registers (H <= 2048)
+    const bool regs = H <= VP_MAXS * (int)blockDim.x;
+    int cnext[VP_MAXS];
+    auto load_col = [&](int st) {
+        const int32_t* col = hT + (size_t)(d.d_max - st) * H;
+#pragma unroll
+        for (int k = 0; k < VP_MAXS; ++k) {
+            const int s = threadIdx.x + k * blockDim.x;
+            cnext[k] = s < H ? col[s] : 0;
+        }
+    };
+    if (regs && D1 > 1) load_col(1);
     for (int st = 1; st < D1; ++st) {
         const int32_t* col = hT + (size_t)(d.d_max - st) * H;
-        for (int s = threadIdx.x; s < H; s += blockDim.x) {
+        int ccur[VP_MAXS];
+#pragma unroll
+        for (int k = 0; k < VP_MAXS; ++k) ccur[k] = cnext[k];
+        if (regs && st + 1 < D1) load_col(st + 1);
+#pragma unroll
+        for (int k = 0; k < VP_MAXS; ++k) {
+            const int s = threadIdx.x + k * blockDim.x;
+            if (!regs || s >= H) break;
             double best = __longlong_as_double(0x7ff0000000000000LL);
             int bo = 0;
 #pragma unroll
@@ -160,9 +193,26 @@ __global__ void __launch_bounds__(512) k_vpath(Dev d, const int32_t* vhistT, int
                     bo = o;
                 }
             }
-            cur[s] = best + -(double)col[s];
+            cur[s] = best + -(double)ccur[k];
             choice[(size_t)st * H + s] = (int8_t)bo;
         }
+        if (!regs)
+            for (int s = threadIdx.x; s < H; s += blockDim.x) {
+                double best = __longlong_as_double(0x7ff0000000000000LL);
+                int bo = 0;
+#pragma unroll
+                for (int o = 0; o < 7; ++o) {
+                    const int ps = s + o;
+                    if (ps >= H) continue;
+                    const double e = prev[ps] + pen[o];
+                    if (e < best) {
+                        best = e;
+                        bo = o;
+                    }
+                }
+                cur[s] = best + -(double)col[s];
+                choice[(size_t)st * H + s] = (int8_t)bo;
+            }
         __syncthreads();
         double* t = prev;
         prev = cur;
