@@ -1435,13 +1435,26 @@ __global__ void __launch_bounds__(256) k_p99_bucket(Dev d) {
 }
 
 // |m1| bits of road-row pixel i (unwritten tiles are +0).
-__device__ __forceinline__ unsigned long long m1_bits(const Dev& d, int f, int t_lo, size_t i,
-                                                      bool* live) {
-    const int v = t_lo + (int)(i / d.W), u = (int)(i % d.W);
-    *live = d.m1_nz[((size_t)f * d.m_nty + (v >> d.m_tile_shift)) * d.m_ntx + (u >> 7)] != 0;
-    return *live ? (unsigned long long)__double_as_longlong(
-                       fabs(d.m1[(size_t)f * d.px + (size_t)v * d.W + u]))
-                 : 0ULL;
+// Visits |m1| of the threshold rows [t_lo, H-1] tile by tile (M_TW x tile_h,
+// the k_m0_m1 tiling): fn(bits, live) per pixel, 32-bit index arithmetic.
+// Tiles k_m0_m1 flagged all-zero are only visited when zeros matter
+// (want_zero: the selection key is the zero bucket).
+template <class Fn>
+__device__ __forceinline__ void for_m1_rows(const Dev& d, int f, int t_lo, bool want_zero, Fn fn) {
+    const int th = 1 << d.m_tile_shift, ty0 = t_lo >> d.m_tile_shift;
+    const int ntile = (d.m_nty - ty0) * d.m_ntx;
+    const uint8_t* nz = d.m1_nz + ((size_t)f * d.m_nty + ty0) * d.m_ntx;
+    const double* m1 = d.m1 + (size_t)f * d.px;
+    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        const bool live = nz[t] != 0;
+        if (!live && !want_zero) continue;
+        const int ty = ty0 + t / d.m_ntx, tx = t % d.m_ntx;
+        for (int p = threadIdx.x; p < th * M_TW; p += blockDim.x) {
+            const int v = ty * th + (p >> 7), u = tx * M_TW + (p & (M_TW - 1));
+            if (v < t_lo || v >= d.H || u >= d.W) continue;
+            fn(live ? (unsigned long long)__double_as_longlong(fabs(m1[(size_t)v * d.W + u])) : 0ULL, live);
+        }
+    }
 }
 
 __global__ void __launch_bounds__(256) k_p99_hist2(Dev d) {
@@ -1453,13 +1466,10 @@ __global__ void __launch_bounds__(256) k_p99_hist2(Dev d) {
     int t_lo;
     const size_t n = p99_n(d, f, &t_lo);
     const unsigned bucket = d.aux[f].p99_bucket;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (size_t)gridDim.x * blockDim.x) {
-        bool live;
-        const unsigned long long b = m1_bits(d, f, t_lo, i, &live);
-        if (!live && bucket != 0) continue;
+    (void)n;
+    for_m1_rows(d, f, t_lo, bucket == 0, [&](unsigned long long b, bool) {
         if ((b >> 52) == bucket) atomicAdd(&h[(b >> 40) & 0xfff], 1u);
-    }
+    });
     __syncthreads();
     unsigned int* gh = d.p99hist2 + (size_t)f * 4096;
     for (int i = threadIdx.x; i < 4096; i += blockDim.x)
@@ -1489,21 +1499,20 @@ __global__ void __launch_bounds__(256) k_p99_collect(Dev d) {
                                             d.aux[f].p99_bucket2
                                       : (unsigned long long)d.aux[f].p99_bucket;
     unsigned long long* out = d.p99cand + (size_t)f * d.px;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (size_t)gridDim.x * blockDim.x) {
-        bool live;
-        const unsigned long long b = m1_bits(d, f, t_lo, i, &live);
-        if (!live && key != 0) continue;  // a zero can only be a candidate of key 0
+    (void)n;
+    // a zero can only be a candidate of key 0
+    for_m1_rows(d, f, t_lo, key == 0, [&](unsigned long long b, bool) {
         const bool hit = (b >> ksh) == key;
-        const unsigned bal = __ballot_sync(__activemask(), hit);
-        if (!bal) continue;
+        const unsigned act = __activemask();
+        const unsigned bal = __ballot_sync(act, hit);
+        if (!bal) return;
         const int lane = threadIdx.x & 31;
         const int leader = __ffs(bal) - 1;
         unsigned base = 0;
         if (lane == leader) base = atomicAdd(&d.aux[f].p99_cands, (unsigned)__popc(bal));
-        base = __shfl_sync(__activemask(), base, leader);
+        base = __shfl_sync(act, base, leader);
         if (hit) out[base + __popc(bal & ((1u << lane) - 1u))] = b;
-    }
+    });
 }
 
 __global__ void __launch_bounds__(256) k_p99_select(Dev d) {
