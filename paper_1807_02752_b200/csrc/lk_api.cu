@@ -82,7 +82,7 @@ constexpr int kMaxIter = 200;  // pipeline.hpp:198, 244
 constexpr int kMaxBranches = 16;      // concurrent frame ranges (streams) per batch
 constexpr int kMinBranchFrames = 16;  // smallest range worth a branch
 constexpr int kH2dChunksDefault = 12; // host-fed batches: copy/compute pipeline depth
-constexpr int kBranchesDefault = 4;   // device-resident batches: concurrent frame ranges
+constexpr int kBranchesDefault = 8;   // device-resident batches: concurrent frame ranges
 constexpr int kFastTableDefault = 27;  // tap pairs of the fast bilateral served by the range table
 
 }  // namespace
