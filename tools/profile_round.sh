@@ -21,7 +21,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
 LK_BRANCHES=1 LK_H2D_CHUNKS=1 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
     --log-file "$OUT/launches_single_range.csv" python tools/kernel_times.py kitti 3 \
     > "$OUT/ncu_launches_sr.log" 2>&1
-for k in k_bilateral_fast k_sobel_refine; do
+for k in k_bilateral_fast k_refine_exact k_sobel_screen; do
     LK_BRANCHES=1 LK_H2D_CHUNKS=1 ncu --set full --clock-control none --import-source on -k "regex:$k" -s 2 -c 1 \
         -o "$OUT/${k}_full" -f python tools/kernel_times.py kitti 2 \
         > "$OUT/ncu_${k}.log" 2>&1
