@@ -215,7 +215,9 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     fps = steps * per_step / dt
     line = {
-        "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": 0,
+        # n_gpus mirrors the launch (--gpus N); the reference arm runs on rank 0's host cores
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": max(world, args.gpus),
+        "device": "host cpu (rank 0 only)",
         "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": dt / steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
