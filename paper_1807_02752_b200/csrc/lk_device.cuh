@@ -115,6 +115,7 @@ struct Dev {
     unsigned int* p99hist2; // [B][4096]
     unsigned long long* p99cand;  // [B][px]
     double* energy;         // [B][ext_cols]
+    int32_t* track_np;      // [B][ext_cols] finite points of each column's lane_track
     lk_lane* lanes;         // [B][lane_cap]
     double* polylines;      // [B][lane_cap][H] (hooks)
     // hooks (LK_FLAG_HOOKS)

@@ -1605,6 +1605,7 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
     const int v_alive = max(v_top, s_dead + 1);  // rows v_alive..v_max carry the track
     double u = (double)(d.ext_lo + ci);
     double e = 0.0;
+    int np = 1;  // lane_track's finite points (lanes.hpp:83-96), for k_select
     // Chunks of EC rows: the track recursion (lane_track, lanes.hpp:83-96)
     // yields EC gather indices, the EC m1 loads are then all in flight
     // together, and the decayed sum consumes them in row order.
@@ -1626,6 +1627,7 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
                 } else {
                     u = a / rw.z;
                 }
+                np += !isnan(u);
             }
             // llround(u) in [0, W)  <=>  -0.5 < u < W - 0.5 (NaN fails); then
             // llround = trunc + (frac >= 0.5), exact for these magnitudes
@@ -1645,6 +1647,7 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
     // rows after the track stops contribute +0.0 (kept: 0 + (-0.0) is +0.0)
     for (int v = v_alive - 1; v >= v_top; --v) e = 0.0 + lg * e;
     d.energy[(size_t)f * d.ext_cols + ci] = e;
+    d.track_np[(size_t)f * d.ext_cols + ci] = np;
 }
 
 // =====================================================================
@@ -1750,6 +1753,10 @@ __global__ void __launch_bounds__(256) k_select(Dev d, int sort_cap) {
     const double* vpx = d.vpx + (size_t)f * H;
     const double* vpy = d.vpy + (size_t)f * H;
     for (int k = threadIdx.x; k < min(s_kept, d.lane_cap); k += blockDim.x) {
+        if (!d.hooks) {  // the same recursion already ran in k_energy for this column
+            lanes[k].n_points = d.track_np[(size_t)f * n + (lanes[k].bottom_col - d.ext_lo)];
+            continue;
+        }
         double u = (double)lanes[k].bottom_col;
         double* poly = d.hooks ? d.polylines + ((size_t)f * d.lane_cap + k) * H : nullptr;
         int np = 1;
