@@ -524,6 +524,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     d.m_ntx = (W + lkg::M_TW - 1) / lkg::M_TW;
     d.m_nty = (H + lp.m_tile_h - 1) / lp.m_tile_h;
     A(&d.m1_nz, (size_t)B * d.m_ntx * d.m_nty);
+    A(&d.wg_nz, (size_t)B * d.m_ntx * d.m_nty);
     lp.collect_blocks = 32;
     lp.sort_cap = sort_cap;
     lp.select_smem = (size_t)sort_cap * 12 + (size_t)((C + 31) / 32) * 4 + 16;
@@ -697,6 +698,7 @@ static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     sh(v.gamma_inl, H * 2);
     sh(v.m1, px);
     sh(v.m1_nz, (size_t)d.m_ntx * d.m_nty);
+    sh(v.wg_nz, (size_t)d.m_ntx * d.m_nty);
     sh(v.p99hist, 2048);
     sh(v.p99hist2, 4096);
     sh(v.p99cand, px);

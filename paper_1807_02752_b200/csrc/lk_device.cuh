@@ -116,6 +116,7 @@ struct Dev {
     unsigned long long* p99cand;  // [B][px]
     double* energy;         // [B][ext_cols]
     int32_t* track_np;      // [B][ext_cols] finite points of each column's lane_track
+    uint8_t* wg_nz;         // [B][m_nty][m_ntx] m0/m1 tiles with a non-zero w_g in reach
     lk_lane* lanes;         // [B][lane_cap]
     double* polylines;      // [B][lane_cap][H] (hooks)
     // hooks (LK_FLAG_HOOKS)

@@ -1153,6 +1153,8 @@ __global__ void __launch_bounds__(32 * GAMMA_NW, 2) k_gamma_fit(Dev d) {
         px[i] = up[2 * i];
         pv[i] = up[2 * i + 1];
     }
+    uint8_t* wnz = d.wg_nz + (size_t)f * d.m_nty * d.m_ntx;  // marked after w_g below
+    for (int i = threadIdx.x; i < d.m_nty * d.m_ntx; i += blockDim.x) wnz[i] = 0;
     __syncthreads();
 #ifdef LK_GAMMA_PROF
     const long long t0 = clock64();
@@ -1212,6 +1214,16 @@ __global__ void __launch_bounds__(32 * GAMMA_NW, 2) k_gamma_fit(Dev d) {
             }
         }
         d.e_wg[eb + e] = wg;
+        if (wg != 0.0) {
+            // the m0/m1 tiles whose w_g window (k_m0_m1: rows v0-1-vs .. v0+th+vs,
+            // cols u0-1-nu .. u0+M_TW+nu) holds this edge: k_m0_m1's non-zero test
+            const int th = 1 << d.m_tile_shift;
+            const int ax = u - M_TW - d.nu, ay = v - th - d.varsigma;  // first tiles: ceil(a / size)
+            const int tx0 = ax > 0 ? (ax + M_TW - 1) / M_TW : 0, tx1 = min(d.m_ntx - 1, (u + 1 + d.nu) / M_TW);
+            const int ty0 = ay > 0 ? (ay + th - 1) / th : 0, ty1 = min(d.m_nty - 1, (v + 1 + d.varsigma) / th);
+            for (int ty = ty0; ty <= ty1; ++ty)
+                for (int tx = tx0; tx <= tx1; ++tx) wnz[ty * d.m_ntx + tx] = 1;
+        }
     }
 #ifdef LK_GAMMA_PROF
     __syncthreads();
@@ -1275,13 +1287,8 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
     // A tile without a non-zero w_g in reach has m0 = m1 = +0 everywhere: it
     // is flagged instead of written (readers of m1 consult the flag). The test
     // runs first, so such tiles (most of them) skip the staging entirely.
-    int nonzero = 0;
-    if (r_lo <= r_hi)
-        for (int e = roff[r_lo] + threadIdx.x; e < roff[r_hi + 1] && !nonzero; e += blockDim.x) {
-            const int u = d.e_uv[eb + e] & 0xffff;
-            nonzero = u >= gc0 && u < gc0 + GW && d.e_wg[eb + e] != 0.0;
-        }
-    nonzero = __syncthreads_or(nonzero);
+    // k_gamma_fit marked the tiles with a non-zero w_g in reach
+    const int nonzero = d.wg_nz[((size_t)f * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x];
     if (nonzero) {
         for (int i = threadIdx.x; i < GH * GW; i += blockDim.x) gw[i] = 0.0;
         if (want_hist)
