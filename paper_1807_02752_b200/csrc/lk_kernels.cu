@@ -1290,7 +1290,11 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
     // k_gamma_fit marked the tiles with a non-zero w_g in reach
     const int nonzero = d.wg_nz[((size_t)f * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x];
     if (nonzero) {
-        for (int i = threadIdx.x; i < GH * GW; i += blockDim.x) gw[i] = 0.0;
+        if ((GH * GW & 1) == 0)
+            for (int i = threadIdx.x; i < GH * GW / 2; i += blockDim.x)
+                reinterpret_cast<double2*>(gw)[i] = make_double2(0.0, 0.0);
+        else
+            for (int i = threadIdx.x; i < GH * GW; i += blockDim.x) gw[i] = 0.0;
         if (want_hist)
             for (int i = threadIdx.x; i < 2048; i += blockDim.x) hist[i] = 0;
         __syncthreads();
@@ -1326,13 +1330,40 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
     // box sum, y-major / x-minor (lanes.hpp:46-60). Positions outside the image
     // hold zeros in gw: adding +-0.0 to a running sum that starts at +0.0 never
     // changes it, so summing them instead of skipping is bit-identical.
-    for (int i = threadIdx.x; i < MH * MW; i += blockDim.x) {
-        const int r = i / MW, c = i - r * MW;
-        const double* g0 = gw + r * GW + c;  // row v-vs, col u-nu
-        double s = 0.0;
-        for (int y = 0; y <= 2 * vs; ++y)
-            for (int x = 0; x <= 2 * nu; ++x) s += g0[y * GW + x];
-        m0[i] = s;
+    if (nu == 1 && (GW & 1) == 0) {
+        // 3-wide window: a thread sums 4 consecutive outputs of a row, each
+        // in its own y-major / x-minor order, from 16-byte loads of the 6
+        // columns they span (each loaded value serves up to 3 of the sums)
+        constexpr int Q = 4;
+        const int per_row = (MW + Q - 1) / Q;
+        for (int i = threadIdx.x; i < MH * per_row; i += blockDim.x) {
+            const int r = i / per_row, c = (i - r * per_row) * Q;
+            const double2* g0 = reinterpret_cast<const double2*>(gw + r * GW + c);  // 16-byte aligned
+            double s[Q] = {0.0, 0.0, 0.0, 0.0};
+            for (int y = 0; y <= 2 * vs; ++y) {
+                const double2 a = g0[0], b = g0[1], e = g0[2];  // columns c .. c+5
+                const double g[6] = {a.x, a.y, b.x, b.y, e.x, e.y};
+#pragma unroll
+                for (int k = 0; k < Q; ++k) {
+                    s[k] += g[k];
+                    s[k] += g[k + 1];
+                    s[k] += g[k + 2];
+                }
+                g0 += GW / 2;
+            }
+#pragma unroll
+            for (int k = 0; k < Q; ++k)
+                if (c + k < MW) m0[r * MW + c + k] = s[k];
+        }
+    } else {
+        for (int i = threadIdx.x; i < MH * MW; i += blockDim.x) {
+            const int r = i / MW, c = i - r * MW;
+            const double* g0 = gw + r * GW + c;  // row v-vs, col u-nu
+            double s = 0.0;
+            for (int y = 0; y <= 2 * vs; ++y)
+                for (int x = 0; x <= 2 * nu; ++x) s += g0[y * GW + x];
+            m0[i] = s;
+        }
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
