@@ -403,6 +403,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     A(&d.p99hist2, (size_t)B * 4096);
     A(&d.p99cand, (size_t)B * d.px);
     A(&d.energy, (size_t)B * C);
+    A(&d.mrange, (size_t)B * H);
     A(&d.track_np, (size_t)B * C);
     int sort_cap = 1;
     while (sort_cap < C / 2 + 2) sort_cap <<= 1;
@@ -703,6 +704,7 @@ static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     sh(v.p99hist2, 4096);
     sh(v.p99cand, px);
     sh(v.energy, C);
+    sh(v.mrange, H);
     sh(v.track_np, C);
     sh(v.lanes, (size_t)d.lane_cap);
     sh(v.polylines, (size_t)d.lane_cap * H);

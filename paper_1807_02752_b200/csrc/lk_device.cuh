@@ -115,6 +115,7 @@ struct Dev {
     unsigned int* p99hist2; // [B][4096]
     unsigned long long* p99cand;  // [B][px]
     double* energy;         // [B][ext_cols]
+    int2* mrange;           // [B][H] road-mask disparity interval per row (empty above the horizon)
     int32_t* track_np;      // [B][ext_cols] finite points of each column's lane_track
     uint8_t* wg_nz;         // [B][m_nty][m_ntx] m0/m1 tiles with a non-zero w_g in reach
     lk_lane* lanes;         // [B][lane_cap]
@@ -144,6 +145,29 @@ __device__ __forceinline__ int mirror(int i, int n) {
         if (i >= n) i = 2 * n - 1 - i;
     }
     return i;
+}
+
+// road_mask's test |double(d) - f(v)| <= varpi (preprocess.hpp:14-25) over the
+// integers d in [1, 255] holds on an interval [lo, hi] (fl(d - f) is monotone
+// in d) inside [f - varpi - 1, f + varpi + 1] (the double subtraction errs by
+// < 1e-13): found by evaluating the reference's expression; lo > hi = empty.
+__device__ __forceinline__ int2 mask_interval(double fr, double varpi) {
+    auto test = [&](int x) { return fabs((double)x - fr) <= varpi; };
+    const double a = fr - varpi - 1.0, b = fr + varpi + 1.0;
+    const int l0 = a >= 1.0 ? (a <= 255.0 ? (int)ceil(a) : 256) : 1;  // NaN -> 1
+    const int h0 = b <= 255.0 ? (b >= 1.0 ? (int)floor(b) : 0) : 255;  // NaN -> 255
+    int lo = 256, hi = 0;
+    for (int x = l0; x <= h0; ++x)
+        if (test(x)) {
+            lo = x;
+            break;
+        }
+    for (int x = h0; x >= lo; --x)
+        if (test(x)) {
+            hi = x;
+            break;
+        }
+    return make_int2(lo, hi);
 }
 
 __device__ __forceinline__ bool frame_failed(const Dev& d, int f) {

@@ -249,8 +249,10 @@ __global__ void __launch_bounds__(256) k_bf_flags(Dev d) {
         return;
     }
     const uint8_t* dp = d.disp + (size_t)f * d.px;
-    const double* fv = d.fv + (size_t)f * d.H;
     const int ra = max(max(v0 - 1, horizon), 0), rb = min(v0 + BT_H, d.H - 1);
+    __shared__ int2 s_mr[BT_H + 2];  // road_mask intervals of rows ra .. rb (k_road_fit)
+    if (threadIdx.x <= rb - ra) s_mr[threadIdx.x] = d.mrange[(size_t)f * d.H + ra + threadIdx.x];
+    __syncthreads();
     const int nw = (d.W + 31) / 32;
     for (int c0 = threadIdx.x & ~31; c0 < nw * 32; c0 += blockDim.x) {
         const int c = c0 + (threadIdx.x & 31);
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(256) k_bf_flags(Dev d) {
         if (c < d.W)
             for (int r = ra; r <= rb && !any; ++r) {
                 const int dv = dp[(size_t)r * d.W + c];
-                any = dv != 0 && fabs((double)dv - fv[r]) <= d.varpi;
+                any = dv >= s_mr[r - ra].x && dv <= s_mr[r - ra].y;  // road_mask, preprocess.hpp:14-25
             }
         const unsigned b = __ballot_sync(0xffffffffu, any);
         if ((threadIdx.x & 31) == 0) s_bits[c0 >> 5] = b;
@@ -341,7 +343,7 @@ __device__ __forceinline__ double exact_bilateral(const Dev& d, const WsParam& w
 // +1e-9) and the test uses s*_lo = the largest float <= s*, so every pixel
 // with s >= s* is a candidate.
 //
-// Thread t of a tile owns pixels (row (t>>7) + 2k, col t & 127), k < SB_TH / 2, so
+// Thread t of a tile owns pixels (row (t>>7) * SB_TH / 2 + k, col t & 127), k < SB_TH / 2, so
 // each warp covers 32 consecutive pixels of a row and its ballot is a
 // candidate / edge word directly.
 __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
@@ -350,7 +352,8 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
     constexpr int TWORD = SB_TW / 32;              // tile row bitmap words
     constexpr int NF = (FH * FW + 255) / 256;
     static_assert(SB_TW == 128 && SB_TH % 2 == 0, "pixel ownership assumes 128-wide tiles");
-    __shared__ float s_f[FH * FW];
+    constexpr int FWP = FW + 2;  // staged row pitch (even: 8-byte pairs)
+    __shared__ __align__(8) float s_f[FH * FWP];
     __shared__ unsigned s_cw[SB_TH][TWORD];
     __shared__ unsigned s_need[FH][NWORD];
     __shared__ int s_nneed, s_base, s_lo[SB_TH], s_hi[SB_TH];
@@ -370,44 +373,40 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
         return;
     }
     const float* sf = d.smoothed_f + (size_t)f * d.px;
-    const int pc = tid & (SB_TW - 1), pr0 = tid >> 7;  // owned pixels: (pr0 + 2k, pc)
+    // owned pixels: rows pr0 * SB_PPT + k (consecutive, so the 3x3 window slides
+    // down one row per pixel), column pc
+    const int pc = tid & (SB_TW - 1), pr0 = (tid >> 7) * SB_PPT;
     // independent loads first: disparity and profile of the owned pixels, s~ tile
     int dv[SB_PPT];
 #pragma unroll
     for (int k = 0; k < SB_PPT; ++k) {
-        const int v = v0 + pr0 + 2 * k, u = u0 + pc;
+        const int v = v0 + pr0 + k, u = u0 + pc;
         dv[k] = v < H && u < W ? d.disp[(size_t)f * d.px + (size_t)v * W + u] : 0;
     }
-    // road_mask's test |double(d) - f(v)| <= varpi holds, for the integers d
-    // in [1, 255], on an interval [lo_v, hi_v] (fl(d - f) is monotone in d)
-    // inside [f - varpi - 1, f + varpi + 1] (the double subtraction errs by
-    // < 1e-13): thread r finds row v0 + r's interval with the reference's
-    // double expression, then each pixel's test is two integer compares
+    // road_mask as per-row disparity intervals (k_road_fit, mask_interval): each
+    // pixel's test is two integer compares
     if (tid < SB_TH) {
-        const int v = v0 + tid;
-        int lo = 256, hi = 0;  // empty: rows above the horizon or outside the image
-        if (v < H && v >= horizon) {
-            const double fr = d.fv[(size_t)f * H + v];
-            auto test = [&](int x) { return fabs((double)x - fr) <= d.varpi; };
-            const double a = fr - d.varpi - 1.0, b = fr + d.varpi + 1.0;
-            const int l0 = a >= 1.0 ? (a <= 255.0 ? (int)ceil(a) : 256) : 1;  // NaN -> 1
-            const int h0 = b <= 255.0 ? (b >= 1.0 ? (int)floor(b) : 0) : 255;  // NaN -> 255
-            for (int x = l0; x <= h0; ++x)
-                if (test(x)) {
-                    lo = x;
-                    break;
-                }
-            for (int x = h0; x >= lo; --x)
-                if (test(x)) {
-                    hi = x;
-                    break;
-                }
-        }
-        s_lo[tid] = lo;
-        s_hi[tid] = hi;
+        const int2 m = v0 + tid < H ? d.mrange[(size_t)f * H + v0 + tid] : make_int2(256, 0);
+        s_lo[tid] = m.x;
+        s_hi[tid] = m.y;
     }
-    {
-        const bool inner = u0 >= 1 && v0 >= 1 && u0 + FW - 1 <= W && v0 + FH - 1 <= H;
+    // s~ tile + ring: s_f[r][j] holds column u0 - 2 + j (j = c + 1 for ring column c),
+    // so interior tiles stage aligned 8-byte pairs (row starts are 8-byte aligned)
+    if (u0 >= 2 && v0 >= 1 && u0 + FWP - 2 <= W && v0 + FH - 1 <= H && (W & 1) == 0) {
+        constexpr int NP = FWP / 2, NF2 = (FH * NP + 255) / 256;
+        float2 t[NF2];
+#pragma unroll
+        for (int q = 0; q < NF2; ++q) {
+            const int i = tid + q * 256;
+            if (i < FH * NP) {
+                const int r = i / NP, m = i - r * NP;
+                t[q] = *reinterpret_cast<const float2*>(sf + (size_t)(v0 - 1 + r) * W + u0 - 2 + 2 * m);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NF2; ++q)
+            if (tid + q * 256 < FH * NP) reinterpret_cast<float2*>(s_f)[tid + q * 256] = t[q];
+    } else {
         float t[NF];
 #pragma unroll
         for (int q = 0; q < NF; ++q) {
@@ -415,29 +414,41 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
             t[q] = 0.f;
             if (i < FH * FW) {
                 const int r = i / FW, c = i - r * FW;
-                const int v = inner ? v0 - 1 + r : mirror(v0 - 1 + r, H);
-                const int u = inner ? u0 - 1 + c : mirror(u0 - 1 + c, W);
-                t[q] = sf[(size_t)v * W + u];
+                t[q] = sf[(size_t)mirror(v0 - 1 + r, H) * W + mirror(u0 - 1 + c, W)];
             }
         }
 #pragma unroll
-        for (int q = 0; q < NF; ++q)
-            if (tid + q * 256 < FH * FW) s_f[tid + q * 256] = t[q];
+        for (int q = 0; q < NF; ++q) {
+            const int i = tid + q * 256;
+            if (i < FH * FW) s_f[(i / FW) * FWP + i % FW + 1] = t[q];
+        }
     }
     if (tid == 0) s_nneed = 0;
     __syncthreads();
     const float D = (float)(8.0 * kEpsSmooth + 1e-6);
     int n_mask = 0, any_cand = 0;
+    // window rows v-1, v, v+1 at columns u-1, u, u+1 (ring row r holds image row v0 - 1 + r)
+    float a[3], b[3], cc[3];
+    {
+        const float* p = s_f + pr0 * FWP + pc + 1;
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+            a[x] = p[x];
+            b[x] = p[FWP + x];
+        }
+    }
 #pragma unroll
     for (int k = 0; k < SB_PPT; ++k) {
-        const int r = pr0 + 2 * k;
+        const int r = pr0 + k;
+        {
+            const float* p = s_f + (r + 2) * FWP + pc + 1;
+#pragma unroll
+            for (int x = 0; x < 3; ++x) cc[x] = p[x];
+        }
         const bool m = dv[k] >= s_lo[r] && dv[k] <= s_hi[r];  // road_mask, preprocess.hpp:14-25
         n_mask += m;
         bool cand = false;
         if (m) {
-            const float* a = s_f + r * FW + pc;  // row v-1, col u-1
-            const float* b = a + FW;
-            const float* cc = b + FW;
             const float gx = ((a[2] - a[0]) + 2.f * (b[2] - b[0])) + (cc[2] - cc[0]);
             const float gy = ((cc[0] - a[0]) + 2.f * (cc[1] - a[1])) + (cc[2] - a[2]);
             const float s = gx * gx + gy * gy;
@@ -448,6 +459,11 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
         const unsigned bal = __ballot_sync(0xffffffffu, cand);
         if (lane == 0) s_cw[r][pc >> 5] = bal;
         any_cand |= cand;
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+            a[x] = b[x];
+            b[x] = cc[x];
+        }
     }
     for (int o = 16; o; o >>= 1) n_mask += __shfl_xor_sync(0xffffffffu, n_mask, o);
     if (lane == 0 && n_mask) atomicAdd(&d.aux[f].mask_px, (unsigned long long)n_mask);

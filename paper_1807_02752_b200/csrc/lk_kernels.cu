@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(128) k_road_fit(Dev d) {
         d.vpy[(size_t)f * H + v] = vpy;
         d.vsing[(size_t)f * H + v] = sing;
         d.fv[(size_t)f * H + v] = fvv;
+        d.mrange[(size_t)f * H + v] = v >= horizon ? mask_interval(fvv, d.varpi) : make_int2(256, 0);
     }
     if (bad != 0x7fffffff) atomicMin(&s_bad_row, bad);
     for (int i = threadIdx.x; i < st.n_inl; i += blockDim.x) {
