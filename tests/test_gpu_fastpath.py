@@ -31,7 +31,7 @@ def _runs(params, cfg):
     return out
 
 
-@pytest.mark.parametrize("family", ["batch", "stress", "acceptance", "hires"])
+@pytest.mark.parametrize("family", ["batch", "stress", "acceptance", "hires", "odd"])
 def test_fast_path_is_bit_identical_to_exact(family):
     if family == "batch":
         params, cfg = [scenes.batch_scene(i) for i in range(8)], abi.default_config()
@@ -39,6 +39,8 @@ def test_fast_path_is_bit_identical_to_exact(family):
         params, cfg = [scenes.stress_scene(i) for i in range(4)], abi.default_config()
     elif family == "acceptance":
         params, cfg = [scenes.acceptance_scene(i) for i in range(20)], scenes.acceptance_config()
+    elif family == "odd":
+        params, cfg = [scenes.batch_scene(i, width=1241, height=373) for i in range(4)], abi.default_config()
     else:
         params, cfg = [scenes.hires_scene(i) for i in range(2)], scenes.hires_config()
     r = _runs(params, cfg)

@@ -79,6 +79,17 @@ def test_no_hooks_mode_matches(oracle):
     assert not problems, "\n".join(problems)
 
 
+@pytest.mark.parametrize("size", [(1241, 373), (333, 251)])
+def test_odd_sizes_fast_path(oracle, size):
+    """Odd widths and heights through the throughput path (no hooks): partial
+    tiles, the mirrored staging fallbacks and unaligned rows vs the oracle."""
+    W, H = size
+    params = [scenes.batch_scene(i, width=W, height=H) for i in range(3)]
+    reps, problems = _run_and_compare(oracle, params, abi.default_config(), hooks=False)
+    assert not problems, "\n".join(problems)
+    assert all(r.status == 0 for r in reps)
+
+
 def test_paper_sign_and_manual_threshold(oracle):
     params = [scenes.batch_scene(i) for i in range(2)]
     cfg = abi.default_config(paper_sign=True, tr_lpv=-400.0, lambda_g=0.98, nu=2, chi=10)
