@@ -309,34 +309,29 @@ def run_ours(args):
     # few steps that one-time fill dominates (4.3 ms of copy before any compute)
     e2_steps = max(3, args.steps)
     # host-fed stream through the public API: every step copies its inputs from
-    # pinned host memory and reads its reports back; lk_submit_batch overlaps a
-    # step's copy with the previous step's kernels (stereo: lk_run_stereo_batch)
+    # pinned host memory and reads its reports back; lk_submit_batch /
+    # lk_submit_stereo_batch overlap a step's copy with the previous step's kernels
     rbufs = []
     for _ in range(2):
         rp = C.c_void_p()
         L.lk_host_alloc(C.byref(rp), B * C.sizeof(abi.LkFrameReport))
         rbufs.append(C.cast(rp, C.POINTER(abi.LkFrameReport)))
-    if not stereo:
-        for k in range(2):
-            L.lk_submit_batch(h, hg, hd, B, rbufs[k % 2])
-        for _ in range(2):
-            L.lk_wait_batch(h)
+    submit = L.lk_submit_stereo_batch if stereo else L.lk_submit_batch
+    for k in range(2):
+        submit(h, hg, hd, B, rbufs[k % 2])
+    for _ in range(2):
+        L.lk_wait_batch(h)
     torch.cuda.synchronize()
     e2.record(stream)
     for k in range(e2_steps):
-        if stereo:
-            run_fn(h, hg, hd, B, abi.LK_MEM_HOST, reps)
-        else:
-            L.lk_submit_batch(h, hg, hd, B, rbufs[k % 2])
-            if k >= 1:
-                L.lk_wait_batch(h)
-    if not stereo:
-        L.lk_wait_batch(h)
+        submit(h, hg, hd, B, rbufs[k % 2])
+        if k >= 1:
+            L.lk_wait_batch(h)
+    L.lk_wait_batch(h)
     e3.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)
-    if not stereo:
-        failed = max(failed, sum(1 for i in range(B) if rbufs[(e2_steps - 1) % 2][i].status))
+    failed = max(failed, sum(1 for i in range(B) if rbufs[(e2_steps - 1) % 2][i].status))
     for rb in rbufs:
         L.lk_host_free(C.cast(rb, C.c_void_p))
 
@@ -402,7 +397,8 @@ def run_ours(args):
         "stage_ms": {str(k): round(float(stage_ms[k]), 4) for k in range(first, 13)},
         "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": 2 * B * px,
                 "d2h_bytes_per_step": B * C.sizeof(abi.LkFrameReport),
-                "api": ("lk_run_stereo_batch(pinned host left+right) -> reports" if stereo else
+                "api": ("lk_submit_stereo_batch / lk_wait_batch: pinned host left+right in, "
+                        "reports out; step k+1's copy overlaps step k's kernels" if stereo else
                         "lk_submit_batch / lk_wait_batch: pinned host grey+disparity in, "
                         "reports out; step k+1's copy overlaps step k's kernels")},
         "roofline": {

@@ -251,6 +251,10 @@ lk_status lk_enqueue(lk_ctx* ctx, int n);
  * buffers of a batch must stay untouched until it has been waited for. */
 lk_status lk_submit_batch(lk_ctx* ctx, const uint8_t* grey, const uint8_t* disparity, int n,
                           lk_frame_report* reports);
+/* The same stream of stereo pairs (LK_FLAG_STEREO contexts): left/right u8
+ * [n][H][W] in, stages 1-12 (run_pipeline, pipeline.hpp:118-270) per batch. */
+lk_status lk_submit_stereo_batch(lk_ctx* ctx, const uint8_t* left, const uint8_t* right, int n,
+                                 lk_frame_report* reports);
 lk_status lk_wait_batch(lk_ctx* ctx);
 lk_status lk_fetch_reports(lk_ctx* ctx, lk_frame_report* reports, int n);
 lk_status lk_synchronize(lk_ctx* ctx);

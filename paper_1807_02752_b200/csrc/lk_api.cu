@@ -114,6 +114,7 @@ struct lk_ctx {
     // streaming API (lk_submit_batch / lk_wait_batch): two input slots
     uint8_t* slot_grey[2] = {};
     uint8_t* slot_disp[2] = {};
+    uint8_t* slot_right[2] = {};  // stereo submits: the right grey (slot 0 = in_right)
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t slot_copied[2] = {}, slot_free[2] = {}, slot_done[2] = {};
     struct Pending {
@@ -881,9 +882,14 @@ lk_status lk_wait_batch(lk_ctx* c) {
     return any ? LK_ERR_FRAME : LK_OK;
 }
 
-lk_status lk_submit_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* disparity, int n,
-                          lk_frame_report* reports) {
-    if (!c || !grey || !disparity) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+// Streaming submit shared by the mono (grey + disparity) and stereo (left +
+// right) entry points: the copy goes to one of two input slots on the copy
+// stream, the kernels wait for it, and the next submit's copy overlaps them.
+static lk_status submit(lk_ctx* c, const uint8_t* a, const uint8_t* b, int n,
+                        lk_frame_report* reports, bool stereo) {
+    if (!c || !a || !b) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    if (stereo && !c->d.stereo)
+        return fail(LK_ERR_INVALID_ARGUMENT, "context was created without LK_FLAG_STEREO");
     if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
     CU(cudaSetDevice(c->device));
     if (!c->copy_stream) {  // first use: the second input slot and the copy stream
@@ -899,6 +905,10 @@ lk_status lk_submit_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* dispari
             CU(cudaEventRecord(c->slot_free[k], c->stream));
         }
     }
+    if (stereo && !c->slot_right[0]) {
+        if (lk_status s = c->alloc(&c->slot_right[1], (size_t)c->max_batch * c->d.px)) return s;
+        c->slot_right[0] = c->in_right;
+    }
     if (c->n_pending == 2) {  // at most two batches in flight
         const lk_status s = lk_wait_batch(c);
         if (s != LK_OK && s != LK_ERR_FRAME) return s;
@@ -906,23 +916,31 @@ lk_status lk_submit_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* dispari
     const int sl = c->next_slot;
     c->next_slot ^= 1;
     const size_t bytes = (size_t)n * c->d.px;
+    uint8_t* second = stereo ? c->slot_right[sl] : c->slot_disp[sl];
     // inputs into the slot once the batch that last read it has finished
     CU(cudaStreamWaitEvent(c->copy_stream, c->slot_free[sl], 0));
-    CU(cudaMemcpyAsync(c->slot_grey[sl], grey, bytes, cudaMemcpyHostToDevice, c->copy_stream));
-    CU(cudaMemcpyAsync(c->slot_disp[sl], disparity, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+    CU(cudaMemcpyAsync(c->slot_grey[sl], a, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+    CU(cudaMemcpyAsync(second, b, bytes, cudaMemcpyHostToDevice, c->copy_stream));
     CU(cudaEventRecord(c->slot_copied[sl], c->copy_stream));
-    // kernels on the slot (graphs are keyed by slot), then the reports
+    // kernels on the slot (graphs are keyed by slot), then the reports. A
+    // stereo batch's stage 4 writes the context's disparity buffer as before.
     CU(cudaStreamWaitEvent(c->stream, c->slot_copied[sl], 0));
     const uint8_t* g0 = c->d.grey;
     const uint8_t* d0 = c->d.disp;
+    const uint8_t* r0 = c->d.right;
     c->d.grey = c->slot_grey[sl];
-    c->d.disp = c->slot_disp[sl];
+    if (stereo)
+        c->d.right = second;
+    else
+        c->d.disp = second;
     c->slot = sl;
-    c->run_stereo = false;
+    c->run_stereo = stereo;
     const lk_status s = enqueue_mode(c, n);
     c->d.grey = g0;
     c->d.disp = d0;
+    c->d.right = r0;
     c->slot = 0;
+    c->run_stereo = false;
     if (s != LK_OK) return s;
     CU(cudaEventRecord(c->slot_free[sl], c->stream));
     if (reports)
@@ -931,6 +949,16 @@ lk_status lk_submit_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* dispari
     CU(cudaEventRecord(c->slot_done[sl], c->stream));
     c->pending[c->n_pending++] = {sl, n, reports};
     return LK_OK;
+}
+
+lk_status lk_submit_batch(lk_ctx* c, const uint8_t* grey, const uint8_t* disparity, int n,
+                          lk_frame_report* reports) {
+    return submit(c, grey, disparity, n, reports, false);
+}
+
+lk_status lk_submit_stereo_batch(lk_ctx* c, const uint8_t* left, const uint8_t* right, int n,
+                                 lk_frame_report* reports) {
+    return submit(c, left, right, n, reports, true);
 }
 
 lk_status lk_enqueue_stereo(lk_ctx* c, int n) {

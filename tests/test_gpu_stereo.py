@@ -146,3 +146,38 @@ def test_stereo_hires_frame(oracle):
         assert pipe.stage(0, k).tobytes() == o[k].tobytes(), k
     r = chk.run(left[0], o["DISPARITY"], cfg)
     assert not compare_reports(reps[0], r.report)
+
+
+def test_stereo_streaming_submit_matches_run_stereo_batch():
+    """lk_submit_stereo_batch / lk_wait_batch: stereo pairs through the two
+    input slots (the right image in its own slot buffers) give the same reports
+    as lk_run_stereo_batch, across slot reuse, the auto-wait of a third
+    submit, and a mono submit interleaved on the same context."""
+    import ctypes as C
+
+    cfg = abi.default_config()
+    batches = []
+    for b in range(4):
+        params = [scenes.batch_scene(300 + 8 * b + i) for i in range(8)]
+        left, right, _ = lanekit.synth_stereo_batch(params)
+        batches.append((np.ascontiguousarray(left), np.ascontiguousarray(right)))
+    with lanekit.GpuPipeline(1242, 375, cfg, max_batch=8, stereo=True) as pipe:
+        want = [[bytes(r) for r in pipe.run_stereo(l, r)] for l, r in batches]
+        L = lanekit.library()
+        got = [(abi.LkFrameReport * 8)() for _ in batches]
+        for b, (l, r) in enumerate(batches):
+            st = L.lk_submit_stereo_batch(pipe._h, l.ctypes.data, r.ctypes.data, 8, got[b])
+            assert st == abi.LK_OK, L.lk_last_error()
+        assert L.lk_wait_batch(pipe._h) in (abi.LK_OK, abi.LK_ERR_FRAME)
+        assert L.lk_wait_batch(pipe._h) in (abi.LK_OK, abi.LK_ERR_FRAME)
+        for b in range(4):
+            assert [bytes(x) for x in got[b]] == want[b], b
+        # a mono batch (grey + the disparity of batch 0) on the same slots afterwards
+        disp0 = np.stack([pipe.stage(i, "DISPARITY") for i in range(8)])  # from the last run_stereo
+        mono = (abi.LkFrameReport * 8)()
+        g = np.ascontiguousarray(batches[3][0])
+        dd = np.ascontiguousarray(disp0)
+        assert L.lk_submit_batch(pipe._h, g.ctypes.data, dd.ctypes.data, 8, mono) == abi.LK_OK
+        assert L.lk_wait_batch(pipe._h) in (abi.LK_OK, abi.LK_ERR_FRAME)
+        for i in range(8):  # same grey + same disparity -> the stereo batch's lanes
+            assert mono[i].lane_count == got[3][i].lane_count, i
