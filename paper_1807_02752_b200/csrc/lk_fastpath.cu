@@ -159,69 +159,75 @@ __global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p,
         const int nxt = need ? tile0 + __ffs(need) - 1 : -1;
         need &= need - 1;
         if (nxt >= 0) bf_issue<RHO>(d, nbx, nb, nxt, pb);  // in flight during the taps below
-        float va[BT_R];
-        float2 nva[BT_R], num[BT_R], den[BT_R];
-#pragma unroll
-        for (int r = 0; r < BT_R; ++r) {
-            va[r] = base[(r0 + r + RHO) * TWh + RHO];
-            nva[r] = make_float2(-va[r], -va[r]);
-            num[r] = den[r] = make_float2(0.f, 0.f);
-        }
-        float2 n11[BT_R / 2], d11[BT_R / 2], nv11[BT_R / 2];
-#pragma unroll
-        for (int m = 0; m < BT_R / 2; ++m) {
-            n11[m] = d11[m] = make_float2(0.f, 0.f);
-            nv11[m] = make_float2(-va[2 * m], -va[2 * m + 1]);
-        }
-#pragma unroll
-        for (int jj = 0; jj < BT_R + 2 * RHO; ++jj) {
-            const float* row = base + (r0 + jj) * TWh;
-            float2 vp[5];
-#pragma unroll
-            for (int q = 0; q < 5; ++q) vp[q] = *reinterpret_cast<const float2*>(row + 2 * q);
-            const float vl = row[10];
+        // the Sobel screen reads s~ only on rows >= horizon - 1 (3x3 of masked
+        // pixels, which lie at rows >= horizon): warps whose BT_R rows are all
+        // above that, or below the image, skip their taps (warp-uniform rows)
+        const int row_lo = all ? 0 : (int)d.rep[f].horizon - 1;
+        if (v0 + r0 + BT_R - 1 >= row_lo && v0 + r0 < d.H) {
+            float va[BT_R];
+            float2 nva[BT_R], num[BT_R], den[BT_R];
 #pragma unroll
             for (int r = 0; r < BT_R; ++r) {
-                const int dj = jj - r;
-                if (dj < 0 || dj >= WIN) continue;
-#pragma unroll
-                for (int q = 0; q < 5; ++q) {
-                    const float2 dr = __fadd2_rn(vp[q], nva[r]);
-                    float2 w;
-                    if ((TB >> q) & 1) {
-                        const float2 t = __ffma2_rn(make_float2(fabsf(dr.x), fabsf(dr.y)), kA2, cb2);
-                        w = __fmul2_rn(p.sp[dj][q], make_float2(lds_f32(__float_as_uint(t.x)),
-                                                                lds_f32(__float_as_uint(t.y))));
-                    } else {
-                        const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.cp[dj][q]);
-                        w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-                    }
-                    num[r] = __ffma2_rn(w, vp[q], num[r]);
-                    den[r] = __fadd2_rn(w, den[r]);
-                }
+                va[r] = base[(r0 + r + RHO) * TWh + RHO];
+                nva[r] = make_float2(-va[r], -va[r]);
+                num[r] = den[r] = make_float2(0.f, 0.f);
             }
-            // 11th column: outputs (2m, 2m + 1) use window rows (jj - 2m, jj - 2m - 1)
+            float2 n11[BT_R / 2], d11[BT_R / 2], nv11[BT_R / 2];
 #pragma unroll
             for (int m = 0; m < BT_R / 2; ++m) {
-                const int k = jj - 2 * m;
-                if (k < 0 || k > WIN) continue;
-                const float2 vl2 = make_float2(vl, vl);
-                const float2 dr = __fadd2_rn(vl2, nv11[m]);
-                const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.c10[k]);
-                const float2 w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-                n11[m] = __ffma2_rn(w, vl2, n11[m]);
-                d11[m] = __fadd2_rn(w, d11[m]);
+                n11[m] = d11[m] = make_float2(0.f, 0.f);
+                nv11[m] = make_float2(-va[2 * m], -va[2 * m + 1]);
             }
-        }
-        const int u = u0 + tx;
 #pragma unroll
-        for (int r = 0; r < BT_R; ++r) {
-            const int v = v0 + r0 + r;
-            const float a = (r & 1) ? n11[r / 2].y : n11[r / 2].x;
-            const float b = (r & 1) ? d11[r / 2].y : d11[r / 2].x;
-            if (u < d.W && v < d.H)
-                d.smoothed_f[(size_t)f * d.px + (size_t)v * d.W + u] =
-                    __fdiv_rn((num[r].x + num[r].y) + a, (den[r].x + den[r].y) + b);
+            for (int jj = 0; jj < BT_R + 2 * RHO; ++jj) {
+                const float* row = base + (r0 + jj) * TWh;
+                float2 vp[5];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) vp[q] = *reinterpret_cast<const float2*>(row + 2 * q);
+                const float vl = row[10];
+#pragma unroll
+                for (int r = 0; r < BT_R; ++r) {
+                    const int dj = jj - r;
+                    if (dj < 0 || dj >= WIN) continue;
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) {
+                        const float2 dr = __fadd2_rn(vp[q], nva[r]);
+                        float2 w;
+                        if ((TB >> q) & 1) {
+                            const float2 t = __ffma2_rn(make_float2(fabsf(dr.x), fabsf(dr.y)), kA2, cb2);
+                            w = __fmul2_rn(p.sp[dj][q], make_float2(lds_f32(__float_as_uint(t.x)),
+                                                                    lds_f32(__float_as_uint(t.y))));
+                        } else {
+                            const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.cp[dj][q]);
+                            w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                        }
+                        num[r] = __ffma2_rn(w, vp[q], num[r]);
+                        den[r] = __fadd2_rn(w, den[r]);
+                    }
+                }
+                // 11th column: outputs (2m, 2m + 1) use window rows (jj - 2m, jj - 2m - 1)
+#pragma unroll
+                for (int m = 0; m < BT_R / 2; ++m) {
+                    const int k = jj - 2 * m;
+                    if (k < 0 || k > WIN) continue;
+                    const float2 vl2 = make_float2(vl, vl);
+                    const float2 dr = __fadd2_rn(vl2, nv11[m]);
+                    const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.c10[k]);
+                    const float2 w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                    n11[m] = __ffma2_rn(w, vl2, n11[m]);
+                    d11[m] = __fadd2_rn(w, d11[m]);
+                }
+            }
+            const int u = u0 + tx;
+#pragma unroll
+            for (int r = 0; r < BT_R; ++r) {
+                const int v = v0 + r0 + r;
+                const float a = (r & 1) ? n11[r / 2].y : n11[r / 2].x;
+                const float b = (r & 1) ? d11[r / 2].y : d11[r / 2].x;
+                if (u < d.W && v < d.H)
+                    d.smoothed_f[(size_t)f * d.px + (size_t)v * d.W + u] =
+                        __fdiv_rn((num[r].x + num[r].y) + a, (den[r].x + den[r].y) + b);
+            }
         }
         if (nxt < 0) break;
         cur = nxt;
