@@ -617,9 +617,6 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, WsParam ws) {
 // neighbourhoods: edge bits replace the candidate bits, then the segment and
 // edge counts the scan and the report need.
 __global__ void __launch_bounds__(256) k_sobel_decide(Dev d) {
-    constexpr int FW = SB_TW + 2, FH = SB_TH + 2;
-    constexpr int NF = (FH * FW + 255) / 256;
-    __shared__ double s_ex[FH * FW];
     __shared__ int s_seg[SB_TH], s_tot;
     const int f = blockIdx.y;
     if (frame_failed(d, f)) return;
@@ -632,25 +629,7 @@ __global__ void __launch_bounds__(256) k_sobel_decide(Dev d) {
         const int tile = (int)d.ctile[(size_t)f * d.n_stile + t];
         const int by = tile / nbx, bx = tile - by * nbx;
         const int u0 = bx * SB_TW, v0 = by * SB_TH;
-        const bool inner = u0 >= 1 && v0 >= 1 && u0 + FW - 1 <= W && v0 + FH - 1 <= H;
-        __syncthreads();  // the previous tile's reads of s_ex are done
-        {
-            double x[NF];
-#pragma unroll
-            for (int q = 0; q < NF; ++q) {
-                const int i = tid + q * 256;
-                x[q] = 0.0;
-                if (i < FH * FW) {  // positions outside the need set are never read below
-                    const int r = i / FW, c = i - r * FW;
-                    const int v = inner ? v0 - 1 + r : mirror(v0 - 1 + r, H);
-                    const int u = inner ? u0 - 1 + c : mirror(u0 - 1 + c, W);
-                    x[q] = sm[(size_t)v * W + u];
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < NF; ++q)
-                if (tid + q * 256 < FH * FW) s_ex[tid + q * 256] = x[q];
-        }
+        __syncthreads();  // the previous tile's counters have been written out
         if (tid < SB_TH) s_seg[tid] = 0;
         if (tid == 0) s_tot = 0;
         __syncthreads();
@@ -663,11 +642,17 @@ __global__ void __launch_bounds__(256) k_sobel_decide(Dev d) {
             const unsigned cw = in ? d.ebits[((size_t)f * H + v) * d.words_per_row + word] : 0u;
             bool edge = false;
             if ((cw >> (u & 31)) & 1) {  // candidate => masked and in the image
-                const double* a = s_ex + r * FW + pc;  // row v-1, col u-1
-                const double* b = a + FW;
-                const double* cc = b + FW;
-                const double gx = (a[2] - a[0]) + 2 * (b[2] - b[0]) + (cc[2] - cc[0]);
-                const double gy = (cc[0] - a[0]) + 2 * (cc[1] - a[1]) + (cc[2] - a[2]);
+                // its 3x3 neighbourhood (mirrored at the border, preprocess.hpp:71-72)
+                // holds exact values: k_refine_exact computed every need pixel
+                const double* ra = sm + (size_t)mirror(v - 1, H) * W;
+                const double* rb = sm + (size_t)v * W;
+                const double* rc = sm + (size_t)mirror(v + 1, H) * W;
+                const int ul = mirror(u - 1, W), ur = mirror(u + 1, W);
+                const double a0 = ra[ul], a1 = ra[u], a2 = ra[ur];
+                const double b0 = rb[ul], b2 = rb[ur];
+                const double c0 = rc[ul], c1 = rc[u], c2 = rc[ur];
+                const double gx = (a2 - a0) + 2 * (b2 - b0) + (c2 - c0);
+                const double gy = (c0 - a0) + 2 * (c1 - a1) + (c2 - a2);
                 edge = gx * gx + gy * gy >= d.sobel_s_star;
                 n_edge += edge;
             }
