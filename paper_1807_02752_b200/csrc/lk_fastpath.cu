@@ -62,6 +62,8 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // border stays within that pixel). Tiles whose one-pixel ring holds no masked
 // pixel are skipped; the test is the exact mask of k_sobel_refine
 // (road_mask, preprocess.hpp:14-25). all = 1 computes every tile (lk_fast_path_error).
+__device__ __forceinline__ float2 fabs2(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
+
 __device__ __forceinline__ float lds_f32(unsigned addr) {
     float v;
     asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
@@ -106,13 +108,19 @@ __device__ __forceinline__ void bf_issue(const Dev& d, int nbx, int nb, int t, u
     }
 }
 
-template <int RHO, int TB>
-__global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p, int n, int tpc, int all) {
+// SG (signed table): R[k_q - k_p] over 511 entries x 32 copies (64 KB of
+// dynamic shared memory, 2 CTAs per SM). The index FFMA2 then takes v_q
+// itself with a per-output constant, so table pairs need no dr: 4 packed FMA
+// ops per pair instead of 5.
+template <int RHO, int TB, bool SG>
+__global__ void __launch_bounds__(256, SG ? 2 : 3) k_bilateral_fast(Dev d, FastBfParam p, int n, int tpc, int all) {
     constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
     constexpr int NPX = TWh * THh;
     static_assert(WIN == 11 && BT_R % 2 == 0 && TWh % 2 == 0, "packed pairs assume an 11-wide window");
     __shared__ __align__(16) float s_v[2][NPX + 2];
-    __shared__ __align__(16) float s_R[TB ? 256 * 32 : 4];
+    __shared__ __align__(16) float s_Rs[(TB && !SG) ? 256 * 32 : 4];
+    extern __shared__ __align__(16) float s_dyn[];  // SG: [511][32]
+    float* s_R = SG ? s_dyn : s_Rs;
     const int nbx = (d.W + BT_W - 1) / BT_W, nb = nbx * ((d.H + BT_H - 1) / BT_H);
     const int tile0 = blockIdx.x * tpc, tile1 = min(tile0 + tpc, n * nb);
     // needed tiles of this chunk (tpc <= 32): one ballot, the same in every warp
@@ -130,17 +138,25 @@ __global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p,
     // base[row * TWh + k] in both cases (copy 1 holds element i at i + 1)
     const float* base = (tx & 1) ? &s_v[1][tx + 1] : &s_v[0][tx];
     const float kA = __int_as_float(128 * 255);  // |dr| * 32640 * 2^-149 = 128 |delta| (subnormal)
-    const float cb = __int_as_float((int)((unsigned)__cvta_generic_to_shared(s_R) + 4u * (threadIdx.x % 32)));
+    // SG: RN(v_q kA + cidx_r) = A_lane + 128 (k_q - k_p + 255) with cidx_r = A_lane + 32640 - v_p kA
+    const float cb = __int_as_float((int)((unsigned)__cvta_generic_to_shared(s_R) + 4u * (threadIdx.x % 32) +
+                                          (SG ? 128u * 255u : 0u)));
     const float2 c2 = make_float2(p.c2, p.c2), kA2 = make_float2(kA, kA), cb2 = make_float2(cb, cb);
     uint32_t pb[BF_PF];
     int cur = tile0 + __ffs(need) - 1;
     need &= need - 1;
     bf_issue<RHO>(d, nbx, nb, cur, pb);
     if (TB) {
-        const float r = __ldg(d.fast_tab + 256 + 255 + threadIdx.x);  // R[|delta| = tid]
 #pragma unroll
-        for (int k = 0; k < 32; k += 4)
-            *reinterpret_cast<float4*>(&s_R[threadIdx.x * 32 + k]) = make_float4(r, r, r, r);
+        for (int h = 0; h < (SG ? 2 : 1); ++h) {
+            const int e = threadIdx.x + 256 * h;  // SG: entry e <-> delta = e - 255; else |delta| = e
+            if (e < (SG ? 511 : 256)) {
+                const float r = __ldg(d.fast_tab + 256 + (SG ? 0 : 255) + e);
+#pragma unroll
+                for (int k = 0; k < 32; k += 4)
+                    *reinterpret_cast<float4*>(&s_R[e * 32 + k]) = make_float4(r, r, r, r);
+            }
+        }
     }
     while (true) {
         __syncthreads();  // the previous tile's taps are done with s_v
@@ -165,12 +181,16 @@ __global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p,
         const int row_lo = all ? 0 : (int)d.rep[f].horizon - 1;
         if (v0 + r0 + BT_R - 1 >= row_lo && v0 + r0 < d.H) {
             float va[BT_R];
-            float2 nva[BT_R], num[BT_R], den[BT_R];
+            float2 nva[BT_R], num[BT_R], den[BT_R], cidx[BT_R];
 #pragma unroll
             for (int r = 0; r < BT_R; ++r) {
                 va[r] = base[(r0 + r + RHO) * TWh + RHO];
                 nva[r] = make_float2(-va[r], -va[r]);
                 num[r] = den[r] = make_float2(0.f, 0.f);
+                if (SG) {
+                    const float c = fmaf(-va[r], kA, cb);  // exact integer (x 2^-149)
+                    cidx[r] = make_float2(c, c);
+                }
             }
             float2 n11[BT_R / 2], d11[BT_R / 2], nv11[BT_R / 2];
 #pragma unroll
@@ -191,13 +211,14 @@ __global__ void __launch_bounds__(256, 3) k_bilateral_fast(Dev d, FastBfParam p,
                     if (dj < 0 || dj >= WIN) continue;
 #pragma unroll
                     for (int q = 0; q < 5; ++q) {
-                        const float2 dr = __fadd2_rn(vp[q], nva[r]);
                         float2 w;
                         if ((TB >> q) & 1) {
-                            const float2 t = __ffma2_rn(make_float2(fabsf(dr.x), fabsf(dr.y)), kA2, cb2);
+                            const float2 t = SG ? __ffma2_rn(vp[q], kA2, cidx[r])
+                                                : __ffma2_rn(fabs2(__fadd2_rn(vp[q], nva[r])), kA2, cb2);
                             w = __fmul2_rn(p.sp[dj][q], make_float2(lds_f32(__float_as_uint(t.x)),
                                                                     lds_f32(__float_as_uint(t.y))));
                         } else {
+                            const float2 dr = __fadd2_rn(vp[q], nva[r]);
                             const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.cp[dj][q]);
                             w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
                         }
@@ -672,18 +693,38 @@ __global__ void __launch_bounds__(256) k_sobel_decide(Dev d) {
     }
 }
 
+cudaError_t configure_fastpath() {
+    cudaError_t e = cudaSuccess;
+    for (auto fn : {k_bilateral_fast<5, 10, true>, k_bilateral_fast<5, 21, true>,
+                    k_bilateral_fast<5, 27, true>, k_bilateral_fast<5, 31, true>})
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 511 * 32 * 4);
+    return e;
+}
+
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all) {
     const dim3 g((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n);
     const int tpc = std::min(32, std::max(1, lp.fast_tpc));
     const int pg = (int)((g.x * g.y * g.z + tpc - 1) / tpc);
     if (!all)
         k_bf_flags<<<dim3((d.H + BT_H - 1) / BT_H, n), 256, 0, s>>>(d);
+    constexpr size_t kSgSmem = 511 * 32 * 4;
+    if (lp.fast_signed) {
+        switch (lp.fast_table) {
+#define LK_BF(M) \
+    case M: k_bilateral_fast<5, M, true><<<pg, 256, kSgSmem, s>>>(d, lp.fbf, n, tpc, all); break;
+            LK_BF(10) LK_BF(21) LK_BF(27) LK_BF(31)
+#undef LK_BF
+            default: k_bilateral_fast<5, 27, true><<<pg, 256, kSgSmem, s>>>(d, lp.fbf, n, tpc, all); break;
+        }
+        return;
+    }
     switch (lp.fast_table) {
 #define LK_BF(M) \
-    case M: k_bilateral_fast<5, M><<<pg, 256, 0, s>>>(d, lp.fbf, n, tpc, all); break;
+    case M: k_bilateral_fast<5, M, false><<<pg, 256, 0, s>>>(d, lp.fbf, n, tpc, all); break;
         LK_BF(0) LK_BF(10) LK_BF(14) LK_BF(21) LK_BF(27) LK_BF(31)
 #undef LK_BF
-        default: k_bilateral_fast<5, 21><<<pg, 256, 0, s>>>(d, lp.fbf, n, tpc, all); break;
+        default: k_bilateral_fast<5, 21, false><<<pg, 256, 0, s>>>(d, lp.fbf, n, tpc, all); break;
     }
 }
 

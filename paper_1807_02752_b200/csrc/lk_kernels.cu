@@ -1958,7 +1958,7 @@ cudaError_t configure_kernels(const LaunchPlan& lp) {
     if ((e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lp.select_smem)))
         return e;
-    return cudaSuccess;
+    return configure_fastpath();
 }
 
 }  // namespace lkg

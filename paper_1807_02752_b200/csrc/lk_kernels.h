@@ -43,6 +43,7 @@ struct LaunchPlan {
     int fast_front;           // certified fast bilateral + exact refinement (lk_fastpath.cu)
     int fast_table;           // mask of tap pairs whose range factor comes from the smem table
     int fast_tpc;             // fast-bilateral tiles per CTA (LK_BF_TPC)
+    int fast_signed;          // signed 64 KB range table (LK_BF_SIGNED)
     int refine_ctas, decide_ctas;  // per-frame grids of k_refine_exact / k_sobel_decide
     int32_t* vhistT;          // [B][D1][H] transposed v-disparity for the v-path DP
     size_t vpath_smem;
@@ -72,6 +73,7 @@ cudaError_t configure_stereo(const Dev& d);
 size_t stereo_smem(const Dev& d);
 int stereo_launches();
 cudaError_t configure_kernels(const LaunchPlan& lp);
+cudaError_t configure_fastpath();
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all = 0);
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
 void launch_exact_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
