@@ -487,8 +487,6 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         lp.fast_table = m ? std::atoi(m) & 31 : kFastTableDefault;
         const char* tpc = std::getenv("LK_BF_TPC");  // tiles per CTA
         lp.fast_tpc = tpc ? std::atoi(tpc) : 24;
-        const char* sg = std::getenv("LK_BF_SIGNED");
-        lp.fast_signed = sg ? std::atoi(sg) : 1;
         d.bf_ntiles = ((W + lkg::BT_W - 1) / lkg::BT_W) * ((H + lkg::BT_H - 1) / lkg::BT_H);
         d.n_stile = ((W + lkg::SB_TW - 1) / lkg::SB_TW) * ((H + lkg::SB_TH - 1) / lkg::SB_TH);
         d.need_cap = d.n_stile * (lkg::SB_TW + 2) * (lkg::SB_TH + 2);  // every ring pixel of every tile

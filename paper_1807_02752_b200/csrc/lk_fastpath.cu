@@ -6,16 +6,17 @@
 // come from the edge list, preprocess.hpp:103-113), and the only integer
 // decision taken on non-edge pixels is "not an edge". So:
 //
-//  1. k_bilateral_fast computes every pixel approximately: weights
-//     2^(c_t + c2*dr^2) with MUFU ex2 and FP32 row-partial sums. A rigorous
-//     bound |s~ - s| <= kEpsSmooth holds against the exact double result
-//     (derivation in DESIGN.md §3; the worst error measured on 10^8 pixels is
-//     recorded in profiles/).
-//  2. k_sobel_refine evaluates Sobel on s~ and propagates the bound to
+//  1. k_bilateral_fast computes every needed pixel approximately: weights
+//     2^(c_t + c2*dr^2) (MUFU ex2 or an exact-index shared table) and FP32
+//     sums. A rigorous bound |s~ - s| <= kEpsSmooth holds against the exact
+//     double result (derivation in DESIGN.md §3; the worst error measured is
+//     checked by tests/test_gpu_fastpath.py).
+//  2. k_sobel_screen evaluates Sobel on s~ and propagates the bound to
 //     s = gx^2 + gy^2. A masked pixel whose s can still reach the threshold is
-//     a candidate. Every pixel in a candidate's 3x3 neighbourhood gets its
-//     EXACT bilateral (the LUT arithmetic of k_bilateral_tile), and the
-//     candidate's edge decision and gradients use those exact values.
+//     a candidate; its 3x3 neighbourhood goes to the frame's need list.
+//  3. k_refine_exact gives every need pixel its EXACT bilateral (the LUT
+//     arithmetic of k_bilateral_tile), and k_sobel_decide takes each
+//     candidate's edge decision from those exact values.
 //
 // The edge set, every edge's gx/gy, and everything downstream are therefore
 // bit-identical to the exact path; only the (unexported) smoothed values of
@@ -42,28 +43,27 @@ __device__ __forceinline__ float ex2_approx(float x) {
 //
 // Issue-slot budget per (output, window row): 5 packed tap pairs + the 11th
 // column, where every instruction counts (the kernel is issue-, LSU- and
-// MUFU-bound at once):
+// MUFU-bound at once; the FMA pipe binds first):
 //  - window values come in as 8-byte pairs (LDS.64). The tile is staged twice,
 //    the second copy shifted by one pixel, so an odd column's pair is aligned too;
 //  - MUFU pairs: dr = v_q - v_p (FADD2), c2*dr^2 + c_t (FMUL2, FFMA2), 2x ex2;
 //  - table pairs: one FFMA2 turns v_q into the shared-memory byte ADDRESS of
-//    R[k_q - k_p]. The FMA lands in the subnormal range, where a float's bit
-//    pattern is the integer multiple of 2^-149, so RN(v_q*1020*2^-149 + C_p)
-//    has bits A_R + 4(k_q - k_p + 255) exactly (v_q*1020 is within 1e-4 of
-//    4 k_q; C_p = RN((A_R + 1020 - v_p*1020) * 2^-149) is an exact integer).
-//    The LDS takes that register as its address: no integer adds, no keys;
+//    R[k_q - k_p] in this lane's copy. The FMA lands in the subnormal range,
+//    where a float's bit pattern is the integer multiple of 2^-149, so
+//    RN(v_q*32640*2^-149 + C_p) has bits A_lane + 128(k_q - k_p + 255) exactly
+//    (v_q*32640 is within 6e-3 of 128 k_q; C_p = RN((A_lane + 32640 -
+//    v_p*32640) * 2^-149) is an exact integer). The LDS takes that register as
+//    its address: no differences, no integer adds, no keys;
 //  - sums go straight into float2 accumulators (no per-row combine);
 //  - the 11th column of outputs r and r+1 runs as one packed pair (the window
 //    row offsets differ by one; a -inf exponent zeroes a row outside a window).
 // The FP32 error of the longer sum chains is budgeted in DESIGN.md §3.
 //
 // all = 0 (the pipeline): s~ is consumed only by the Sobel of road-mask pixels
-// (k_sobel_refine), i.e. within one pixel of a masked pixel (mirroring at the
+// (k_sobel_screen), i.e. within one pixel of a masked pixel (mirroring at the
 // border stays within that pixel). Tiles whose one-pixel ring holds no masked
-// pixel are skipped; the test is the exact mask of k_sobel_refine
-// (road_mask, preprocess.hpp:14-25). all = 1 computes every tile (lk_fast_path_error).
-__device__ __forceinline__ float2 fabs2(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
-
+// pixel are skipped (k_bf_flags, the exact road_mask test of preprocess.hpp:14-25).
+// all = 1 computes every tile (lk_fast_path_error).
 __device__ __forceinline__ float lds_f32(unsigned addr) {
     float v;
     asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
@@ -71,13 +71,15 @@ __device__ __forceinline__ float lds_f32(unsigned addr) {
 }
 
 //
-// Range table: R[|k_q - k_p|] (R is even: the reference's dr * dr), 256
-// entries replicated 32 times, entry-major (word 32 |delta| + lane): lane L
+// Range table: R[k_q - k_p] (511 entries) replicated 32 times entry-major
+// (word 32 i + lane) in 64 KB of dynamic shared memory, 2 CTAs per SM: lane L
 // always reads bank L, so a warp's lookup is one wavefront whatever the
 // differences (a single copy averaged ~3.1 wavefronts per lookup). The index
-// FFMA2 takes |dr| (dr is already there for the MUFU pairs' exponent), so the
-// address constant is per lane, not per output. The 32 KB table is staged once
-// per CTA, which walks TPC consecutive tiles to amortise it.
+// FFMA2 takes v_q itself with a per-output constant (the address formula is
+// above), so a table pair costs 4 packed FMA-pipe ops (index, S_t * R, num,
+// den) against 5 for a MUFU pair; a 256-entry R[|k_q - k_p|] table that fits
+// 3 CTAs in 48 KB needs |dr| for its index and measured 2.39 vs 2.30 ms.
+// The table is staged once per CTA, which walks TPC consecutive tiles.
 //
 // Staging is software-pipelined: the grey bytes of the CTA's next needed tile
 // are loaded into registers before the current tile's taps run, so their
@@ -108,19 +110,13 @@ __device__ __forceinline__ void bf_issue(const Dev& d, int nbx, int nb, int t, u
     }
 }
 
-// SG (signed table): R[k_q - k_p] over 511 entries x 32 copies (64 KB of
-// dynamic shared memory, 2 CTAs per SM). The index FFMA2 then takes v_q
-// itself with a per-output constant, so table pairs need no dr: 4 packed FMA
-// ops per pair instead of 5.
-template <int RHO, int TB, bool SG>
-__global__ void __launch_bounds__(256, SG ? 2 : 3) k_bilateral_fast(Dev d, FastBfParam p, int n, int tpc, int all) {
+template <int RHO, int TB>
+__global__ void __launch_bounds__(256, 2) k_bilateral_fast(Dev d, FastBfParam p, int n, int tpc, int all) {
     constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
     constexpr int NPX = TWh * THh;
     static_assert(WIN == 11 && BT_R % 2 == 0 && TWh % 2 == 0, "packed pairs assume an 11-wide window");
     __shared__ __align__(16) float s_v[2][NPX + 2];
-    __shared__ __align__(16) float s_Rs[(TB && !SG) ? 256 * 32 : 4];
-    extern __shared__ __align__(16) float s_dyn[];  // SG: [511][32]
-    float* s_R = SG ? s_dyn : s_Rs;
+    extern __shared__ __align__(16) float s_R[];  // [511][32]: R[k_q - k_p + 255], lane-replicated
     const int nbx = (d.W + BT_W - 1) / BT_W, nb = nbx * ((d.H + BT_H - 1) / BT_H);
     const int tile0 = blockIdx.x * tpc, tile1 = min(tile0 + tpc, n * nb);
     // needed tiles of this chunk (tpc <= 32): one ballot, the same in every warp
@@ -138,20 +134,20 @@ __global__ void __launch_bounds__(256, SG ? 2 : 3) k_bilateral_fast(Dev d, FastB
     // base[row * TWh + k] in both cases (copy 1 holds element i at i + 1)
     const float* base = (tx & 1) ? &s_v[1][tx + 1] : &s_v[0][tx];
     const float kA = __int_as_float(128 * 255);  // |dr| * 32640 * 2^-149 = 128 |delta| (subnormal)
-    // SG: RN(v_q kA + cidx_r) = A_lane + 128 (k_q - k_p + 255) with cidx_r = A_lane + 32640 - v_p kA
+    // RN(v_q kA + cidx_r) = A_lane + 128 (k_q - k_p + 255) with cidx_r = A_lane + 32640 - v_p kA
     const float cb = __int_as_float((int)((unsigned)__cvta_generic_to_shared(s_R) + 4u * (threadIdx.x % 32) +
-                                          (SG ? 128u * 255u : 0u)));
-    const float2 c2 = make_float2(p.c2, p.c2), kA2 = make_float2(kA, kA), cb2 = make_float2(cb, cb);
+                                          128u * 255u));
+    const float2 c2 = make_float2(p.c2, p.c2), kA2 = make_float2(kA, kA);
     uint32_t pb[BF_PF];
     int cur = tile0 + __ffs(need) - 1;
     need &= need - 1;
     bf_issue<RHO>(d, nbx, nb, cur, pb);
     if (TB) {
 #pragma unroll
-        for (int h = 0; h < (SG ? 2 : 1); ++h) {
-            const int e = threadIdx.x + 256 * h;  // SG: entry e <-> delta = e - 255; else |delta| = e
-            if (e < (SG ? 511 : 256)) {
-                const float r = __ldg(d.fast_tab + 256 + (SG ? 0 : 255) + e);
+        for (int h = 0; h < 2; ++h) {
+            const int e = threadIdx.x + 256 * h;  // entry e <-> delta = e - 255
+            if (e < 511) {
+                const float r = __ldg(d.fast_tab + 256 + e);
 #pragma unroll
                 for (int k = 0; k < 32; k += 4)
                     *reinterpret_cast<float4*>(&s_R[e * 32 + k]) = make_float4(r, r, r, r);
@@ -187,10 +183,8 @@ __global__ void __launch_bounds__(256, SG ? 2 : 3) k_bilateral_fast(Dev d, FastB
                 va[r] = base[(r0 + r + RHO) * TWh + RHO];
                 nva[r] = make_float2(-va[r], -va[r]);
                 num[r] = den[r] = make_float2(0.f, 0.f);
-                if (SG) {
-                    const float c = fmaf(-va[r], kA, cb);  // exact integer (x 2^-149)
-                    cidx[r] = make_float2(c, c);
-                }
+                const float c = fmaf(-va[r], kA, cb);  // exact integer (x 2^-149)
+                cidx[r] = make_float2(c, c);
             }
             float2 n11[BT_R / 2], d11[BT_R / 2], nv11[BT_R / 2];
 #pragma unroll
@@ -213,8 +207,7 @@ __global__ void __launch_bounds__(256, SG ? 2 : 3) k_bilateral_fast(Dev d, FastB
                     for (int q = 0; q < 5; ++q) {
                         float2 w;
                         if ((TB >> q) & 1) {
-                            const float2 t = SG ? __ffma2_rn(vp[q], kA2, cidx[r])
-                                                : __ffma2_rn(fabs2(__fadd2_rn(vp[q], nva[r])), kA2, cb2);
+                            const float2 t = __ffma2_rn(vp[q], kA2, cidx[r]);
                             w = __fmul2_rn(p.sp[dj][q], make_float2(lds_f32(__float_as_uint(t.x)),
                                                                     lds_f32(__float_as_uint(t.y))));
                         } else {
@@ -256,10 +249,10 @@ __global__ void __launch_bounds__(256, SG ? 2 : 3) k_bilateral_fast(Dev d, FastB
 }
 
 // Which fast-bilateral tiles the pipeline needs: s~ is read only by the Sobel
-// of road-mask pixels (k_sobel_refine), i.e. within one pixel of a masked
+// of road-mask pixels (k_sobel_screen), i.e. within one pixel of a masked
 // pixel (mirroring at the border stays within that pixel). Flag = some pixel
 // of the tile's one-pixel ring is in road_mask (preprocess.hpp:14-25, the exact
-// test k_sobel_refine applies). One CTA per (tile row, frame); failed frames
+// test k_sobel_screen applies). One CTA per (tile row, frame); failed frames
 // and bands above the horizon get 0.
 __global__ void __launch_bounds__(256) k_bf_flags(Dev d) {
     __shared__ unsigned s_bits[(65536 + 31) / 32];
@@ -695,8 +688,8 @@ __global__ void __launch_bounds__(256) k_sobel_decide(Dev d) {
 
 cudaError_t configure_fastpath() {
     cudaError_t e = cudaSuccess;
-    for (auto fn : {k_bilateral_fast<5, 10, true>, k_bilateral_fast<5, 21, true>,
-                    k_bilateral_fast<5, 27, true>, k_bilateral_fast<5, 31, true>})
+    for (auto fn : {k_bilateral_fast<5, 0>, k_bilateral_fast<5, 10>, k_bilateral_fast<5, 21>,
+                    k_bilateral_fast<5, 27>, k_bilateral_fast<5, 31>})
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 511 * 32 * 4);
     return e;
@@ -708,23 +701,13 @@ void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream
     const int pg = (int)((g.x * g.y * g.z + tpc - 1) / tpc);
     if (!all)
         k_bf_flags<<<dim3((d.H + BT_H - 1) / BT_H, n), 256, 0, s>>>(d);
-    constexpr size_t kSgSmem = 511 * 32 * 4;
-    if (lp.fast_signed) {
-        switch (lp.fast_table) {
-#define LK_BF(M) \
-    case M: k_bilateral_fast<5, M, true><<<pg, 256, kSgSmem, s>>>(d, lp.fbf, n, tpc, all); break;
-            LK_BF(10) LK_BF(21) LK_BF(27) LK_BF(31)
-#undef LK_BF
-            default: k_bilateral_fast<5, 27, true><<<pg, 256, kSgSmem, s>>>(d, lp.fbf, n, tpc, all); break;
-        }
-        return;
-    }
+    constexpr size_t kTableSmem = 511 * 32 * 4;
     switch (lp.fast_table) {
 #define LK_BF(M) \
-    case M: k_bilateral_fast<5, M, false><<<pg, 256, 0, s>>>(d, lp.fbf, n, tpc, all); break;
-        LK_BF(0) LK_BF(10) LK_BF(14) LK_BF(21) LK_BF(27) LK_BF(31)
+    case M: k_bilateral_fast<5, M><<<pg, 256, kTableSmem, s>>>(d, lp.fbf, n, tpc, all); break;
+        LK_BF(0) LK_BF(10) LK_BF(21) LK_BF(27) LK_BF(31)
 #undef LK_BF
-        default: k_bilateral_fast<5, 21, false><<<pg, 256, 0, s>>>(d, lp.fbf, n, tpc, all); break;
+        default: k_bilateral_fast<5, 27><<<pg, 256, kTableSmem, s>>>(d, lp.fbf, n, tpc, all); break;
     }
 }
 

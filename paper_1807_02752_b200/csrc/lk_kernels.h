@@ -43,7 +43,6 @@ struct LaunchPlan {
     int fast_front;           // certified fast bilateral + exact refinement (lk_fastpath.cu)
     int fast_table;           // mask of tap pairs whose range factor comes from the smem table
     int fast_tpc;             // fast-bilateral tiles per CTA (LK_BF_TPC)
-    int fast_signed;          // signed 64 KB range table (LK_BF_SIGNED)
     int refine_ctas, decide_ctas;  // per-frame grids of k_refine_exact / k_sobel_decide
     int32_t* vhistT;          // [B][D1][H] transposed v-disparity for the v-path DP
     size_t vpath_smem;
