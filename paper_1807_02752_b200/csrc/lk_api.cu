@@ -632,7 +632,7 @@ void* lk_stream(lk_ctx* c) { return c ? (void*)c->stream : nullptr; }
 static int branch_count(const lk_ctx* c, int n);
 
 int lk_launches_per_batch(lk_ctx* c) {
-    return c ? (lkg::launches_per_batch(c->d) + (c->last_stereo ? lkg::stereo_launches() : 0)) *
+    return c ? (lkg::launches_per_batch(c->d, c->lp) + (c->last_stereo ? lkg::stereo_launches() : 0)) *
                    branch_count(c, c->last_n ? c->last_n : c->max_batch)
              : 0;
 }

@@ -1197,11 +1197,35 @@ __global__ void __launch_bounds__(32 * GAMMA_NW, 2) k_gamma_fit(Dev d) {
         rep.gamma_inlier_count = st.n_inl;
     }
     __syncthreads();
-    // w_g per edge (lanes.hpp:35-44)
+    // w_g per edge: k_wg (all frames' edges in parallel)
+#ifdef LK_GAMMA_PROF
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        rep.gamma_kappa = (double)(st.t_loop - t0);
+        rep.gamma_v_normalizer = (double)(t1 - st.t_loop);
+        rep.gamma_inlier_fraction = (double)(clock64() - t1);
+        rep.beta[0] = (double)st.t_fit;
+        rep.beta[1] = (double)st.t_cls;
+        rep.beta[2] = (double)st.t_commit;
+        rep.vpath_energy = (double)st.rounds;
+    }
+#endif
+}
+
+// w_g per edge (build_m0's weight, lanes.hpp:35-44), after k_gamma_fit has
+// written V_px: grid (X, frames), threads stride over the frame's edges. Also
+// marks the m0/m1 tiles whose w_g window (k_m0_m1: rows v0-1-vs .. v0+th+vs,
+// cols u0-1-nu .. u0+M_TW+nu) holds a non-zero w_g (k_gamma_fit zeroed them).
+__global__ void __launch_bounds__(256) k_wg(Dev d) {
+    const int f = blockIdx.y;
+    if (frame_failed(d, f)) return;
+    const int H = d.H, v_top = (int)d.rep[f].horizon, v_max = H - 1;
+    const double* vpx = d.vpx + (size_t)f * H;
     const double* vpy = d.vpy + (size_t)f * H;
+    uint8_t* wnz = d.wg_nz + (size_t)f * d.m_nty * d.m_ntx;
     const int n_edges = d.row_off[(size_t)f * (H + 1) + H];
     const size_t eb = (size_t)f * d.px;
-    for (int e = threadIdx.x; e < n_edges; e += blockDim.x) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_edges; e += gridDim.x * blockDim.x) {
         const int uv = d.e_uv[eb + e];
         const int u = uv & 0xffff, v = uv >> 16;
         double wg = 0.0;
@@ -1216,8 +1240,6 @@ __global__ void __launch_bounds__(32 * GAMMA_NW, 2) k_gamma_fit(Dev d) {
         }
         d.e_wg[eb + e] = wg;
         if (wg != 0.0) {
-            // the m0/m1 tiles whose w_g window (k_m0_m1: rows v0-1-vs .. v0+th+vs,
-            // cols u0-1-nu .. u0+M_TW+nu) holds this edge: k_m0_m1's non-zero test
             const int th = 1 << d.m_tile_shift;
             const int ax = u - M_TW - d.nu, ay = v - th - d.varsigma;  // first tiles: ceil(a / size)
             const int tx0 = ax > 0 ? (ax + M_TW - 1) / M_TW : 0, tx1 = min(d.m_ntx - 1, (u + 1 + d.nu) / M_TW);
@@ -1226,18 +1248,6 @@ __global__ void __launch_bounds__(32 * GAMMA_NW, 2) k_gamma_fit(Dev d) {
                 for (int tx = tx0; tx <= tx1; ++tx) wnz[ty * d.m_ntx + tx] = 1;
         }
     }
-#ifdef LK_GAMMA_PROF
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        rep.gamma_kappa = (double)(st.t_loop - t0);
-        rep.gamma_v_normalizer = (double)(t1 - st.t_loop);
-        rep.gamma_inlier_fraction = (double)(clock64() - t1);
-        rep.beta[0] = (double)st.t_fit;
-        rep.beta[1] = (double)st.t_cls;
-        rep.beta[2] = (double)st.t_commit;
-        rep.vpath_energy = (double)st.rounds;
-    }
-#endif
 }
 
 // =====================================================================
@@ -1902,6 +1912,7 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     }
 #undef LK_VANISH
     k_gamma_fit<<<n, 32 * GAMMA_NW, lp.gamma_smem, s>>>(d);
+    k_wg<<<dim3(8, n), 256, 0, s>>>(d);
     mark(11);
     const bool auto_tr = isnan(d.tr_lpv);
     k_m0_m1<<<dim3((d.W + M_TW - 1) / M_TW, (d.H + lp.m_tile_h - 1) / lp.m_tile_h, n), 256,
@@ -1926,7 +1937,12 @@ void launch_exact_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     k_bilateral_tile<5, 0><<<g, 256, lp.bt_smem, s>>>(d, lp.ws);
 }
 
-int launches_per_batch(const Dev& d) { return isnan(d.tr_lpv) ? 18 : 13; }
+// Kernels per frame range: the exact path (k_bilateral_tile, k_sobel_edges) or
+// the certified fast path (k_bf_flags, k_bilateral_fast, k_sobel_screen,
+// k_refine_exact, k_sobel_decide: 3 more), 5 more with the auto threshold.
+int launches_per_batch(const Dev& d, const LaunchPlan& lp) {
+    return (isnan(d.tr_lpv) ? 19 : 14) + (lp.fast_front ? 3 : 0);
+}
 
 cudaError_t configure_kernels(const LaunchPlan& lp) {
     cudaError_t e;

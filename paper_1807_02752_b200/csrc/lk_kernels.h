@@ -77,6 +77,6 @@ void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
 void launch_exact_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
 cudaError_t fast_error(const Dev& d, int n, cudaStream_t s, double* out_dev);
-int launches_per_batch(const Dev& d);
+int launches_per_batch(const Dev& d, const LaunchPlan& lp);
 
 }  // namespace lkg
