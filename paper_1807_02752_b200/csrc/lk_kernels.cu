@@ -755,12 +755,9 @@ __device__ __forceinline__ void emit_segment(const Dev& d, int f, int v, int sx,
             const size_t e = (size_t)f * d.px + base + run + __popc(b & ((1u << lane) - 1u));
             double gx, gy;
             sobel_at(img, W, H, u, v, gx, gy);
-            double th = atan2(gy, gx);
-            if (th <= -kPi) th = kPi;
-            d.e_uv[e] = u | (v << 16);
+            d.e_uv[e] = u | (v << 16);  // theta (atan2) is k_wg's, over all edges in parallel
             d.e_gx[e] = gx;
             d.e_gy[e] = gy;
-            d.e_th[e] = th;
             int col = kSkipCol;
             if (!(sing || fabs(gx) < 1e-3)) {  // kGradientFloor, vanish.hpp:20, 59
                 const double c = (double)u + ((double)v - vpy) * (gy / gx);
@@ -1212,13 +1209,18 @@ __global__ void __launch_bounds__(32 * GAMMA_NW, 2) k_gamma_fit(Dev d) {
 #endif
 }
 
-// w_g per edge (build_m0's weight, lanes.hpp:35-44), after k_gamma_fit has
-// written V_px: grid (X, frames), threads stride over the frame's edges. Also
+// Per edge: theta = atan2(gy, gx) (sobel_gradients, preprocess.hpp:85-87; it
+// feeds only w_g and the EDGES hook) and w_g (build_m0's weight,
+// lanes.hpp:35-44) after k_gamma_fit has written V_px. Grid (X, frames),
+// threads stride over the frame's edges. Also
 // marks the m0/m1 tiles whose w_g window (k_m0_m1: rows v0-1-vs .. v0+th+vs,
 // cols u0-1-nu .. u0+M_TW+nu) holds a non-zero w_g (k_gamma_fit zeroed them).
 __global__ void __launch_bounds__(256) k_wg(Dev d) {
     const int f = blockIdx.y;
-    if (frame_failed(d, f)) return;
+    const lk_frame_report& rep = d.rep[f];
+    // edges exist once stage 10 has passed; a stage-11 failure still exports them
+    if (rep.status != 0 && rep.failed_stage <= 10) return;
+    const bool fit = rep.status == 0;
     const int H = d.H, v_top = (int)d.rep[f].horizon, v_max = H - 1;
     const double* vpx = d.vpx + (size_t)f * H;
     const double* vpy = d.vpy + (size_t)f * H;
@@ -1228,14 +1230,19 @@ __global__ void __launch_bounds__(256) k_wg(Dev d) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_edges; e += gridDim.x * blockDim.x) {
         const int uv = d.e_uv[eb + e];
         const int u = uv & 0xffff, v = uv >> 16;
+        const double gx = d.e_gx[eb + e];
+        double th = atan2(d.e_gy[eb + e], gx);  // sobel_gradients' theta (preprocess.hpp:85-87)
+        if (th <= -kPi) th = kPi;
+        d.e_th[eb + e] = th;
+        if (!fit) continue;
         double wg = 0.0;
         if (v >= v_top && v <= v_max) {
             const double dx = vpx[v] - (double)u;
             const double dy = vpy[v] - (double)v;
             if (!(fabs(dx) < 1e-12 && fabs(dy) < 1e-12)) {
                 const double theta_ray = atan2(dy, dx);
-                const double theta_tangent = d.e_th[eb + e] + kPi / 2;
-                wg = d.e_gx[eb + e] * piecewise_weight(theta_tangent, theta_ray, d.sigma_g);
+                const double theta_tangent = th + kPi / 2;
+                wg = gx * piecewise_weight(theta_tangent, theta_ray, d.sigma_g);
             }
         }
         d.e_wg[eb + e] = wg;
