@@ -7,7 +7,7 @@
 
 namespace lkg {
 
-constexpr int K1_ROWS = 8;              // rows per v-disparity CTA
+constexpr int K1_ROWS = 32;             // rows per v-disparity CTA
 constexpr int BF_TW = 32, BF_TH = 8;    // bilateral tile (generic window)
 constexpr int BT_W = 64, BT_H = 16, BT_R = 4;  // bilateral tile (11x11), outputs per thread
 constexpr int BT_TRI_N = 128;           // max distinct values per tile for the smem sub-table
