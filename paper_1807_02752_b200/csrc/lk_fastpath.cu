@@ -630,13 +630,14 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, WsParam ws) {
 // tile, on the exact smoothed values k_refine_exact wrote for their 3x3
 // neighbourhoods: edge bits replace the candidate bits, then the segment and
 // edge counts the scan and the report need.
-__global__ void __launch_bounds__(256) k_sobel_decide(Dev d) {
+__global__ void __launch_bounds__(128) k_sobel_decide(Dev d) {
     __shared__ int s_seg[SB_TH], s_tot;
     const int f = blockIdx.y;
     if (frame_failed(d, f)) return;
     const unsigned cnt = d.ctile_cnt[f];
     const int W = d.W, H = d.H, tid = threadIdx.x, lane = tid & 31;
-    const int pc = tid & (SB_TW - 1), pr0 = tid >> 7;
+    // thread t: column t & 127 of rows (t >> 7) + rstep * k (128 threads: every row)
+    const int pc = tid & (SB_TW - 1), pr0 = tid >> 7, rstep = blockDim.x >> 7;
     const double* sm = d.smoothed + (size_t)f * d.px;
     const int nbx = (W + SB_TW - 1) / SB_TW;
     for (unsigned t = blockIdx.x; t < cnt; t += gridDim.x) {
@@ -648,9 +649,8 @@ __global__ void __launch_bounds__(256) k_sobel_decide(Dev d) {
         if (tid == 0) s_tot = 0;
         __syncthreads();
         int n_edge = 0;
-#pragma unroll
-        for (int k = 0; k < SB_PPT; ++k) {
-            const int r = pr0 + 2 * k, v = v0 + r, u = u0 + pc;
+        for (int r = pr0; r < SB_TH; r += rstep) {
+            const int v = v0 + r, u = u0 + pc;
             const bool in = v < H && u < W;
             const int word = u >> 5;
             const unsigned cw = in ? d.ebits[((size_t)f * H + v) * d.words_per_row + word] : 0u;
@@ -715,7 +715,7 @@ void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t
     const dim3 g((d.W + SB_TW - 1) / SB_TW, (d.H + SB_TH - 1) / SB_TH, n);
     k_sobel_screen<<<g, 256, 0, s>>>(d);
     k_refine_exact<5><<<dim3(lp.refine_ctas, n), 256, 0, s>>>(d, lp.ws);
-    k_sobel_decide<<<dim3(lp.decide_ctas, n), 256, 0, s>>>(d);
+    k_sobel_decide<<<dim3(lp.decide_ctas, n), 128, 0, s>>>(d);
 }
 
 // Largest |s~ - s| of a batch (verification of kEpsSmooth): both maps full.

@@ -793,16 +793,18 @@ __global__ void __launch_bounds__(256) k_edge_emit(Dev d) {
 
 // Fast path: edges exist only in the Sobel screen's candidate tiles (one
 // 128-px segment column x SB_TH rows each), so only those are visited.
-__global__ void __launch_bounds__(32 * SB_TH) k_edge_emit_tiles(Dev d) {
+__global__ void __launch_bounds__(256) k_edge_emit_tiles(Dev d) {
     const int f = blockIdx.y;
     if (frame_failed(d, f)) return;
     const unsigned cnt = d.ctile_cnt[f];
-    const int r = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (unsigned t = blockIdx.x; t < cnt; t += gridDim.x) {
         const int tile = (int)d.ctile[(size_t)f * d.n_stile + t];
         const int by = tile / d.n_seg, bx = tile - by * d.n_seg;
-        const int v = by * SB_TH + r;
-        if (v < d.H) emit_segment(d, f, v, bx, threadIdx.x & 31);
+        for (int r = warp; r < SB_TH; r += nw) {  // a warp per 128-px row segment
+            const int v = by * SB_TH + r;
+            if (v < d.H) emit_segment(d, f, v, bx, threadIdx.x & 31);
+        }
     }
 }
 
@@ -1893,7 +1895,7 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     }
     k_edge_scan<<<n, 1024, 0, s>>>(d);
     if (lp.fast_front)
-        k_edge_emit_tiles<<<dim3(lp.decide_ctas, n), 32 * SB_TH, 0, s>>>(d);
+        k_edge_emit_tiles<<<dim3(lp.decide_ctas, n), 128, 0, s>>>(d);
     else
         k_edge_emit<<<dim3((d.H * d.n_seg + 7) / 8, n), 256, 0, s>>>(d);
     mark(10);
