@@ -837,8 +837,9 @@ __device__ __forceinline__ int upath_off(int oi) { return (oi & 1) ? -((oi + 1) 
 // on each side, so no bounds tests). INT: exact packed keys
 // (energy << 4 | offset index), whose minimum is the smallest energy and,
 // among ties, the earliest offset in list order — the strict-'<' scan of
-// dp.hpp:43-51; keys are prev * 16 + d.upk[oi] with upk = pen * 16 + oi from
-// the host (constant-bank operands), reduced with 3-input mins. Otherwise
+// dp.hpp:43-51; energies are stored x16, so keys are prev16 + d.upk[oi] with
+// upk = pen * 16 + oi from the host (constant-bank operands), reduced with
+// 3-input mins. Otherwise
 // doubles with the reference's scan verbatim. ch[s] receives the winning
 // offset INDEX (the backtrack maps it to the offset).
 template <int SP, bool INT>
@@ -852,7 +853,7 @@ __device__ __forceinline__ void upath_stage(const Dev& d, const void* prevv, voi
         int* cur = (int*)curv;
         int w16[SP + 10];
 #pragma unroll
-        for (int k = 0; k < SP + 10; ++k) w16[k] = prev[s0 - 5 + k] * 16;
+        for (int k = 0; k < SP + 10; ++k) w16[k] = prev[s0 - 5 + k];  // stored x16 already
 #pragma unroll
         for (int j = 0; j < SP; ++j) {
             const int s = s0 + j;
@@ -864,7 +865,7 @@ __device__ __forceinline__ void upath_stage(const Dev& d, const void* prevv, voi
             const int m1 = __vimin3_s32(key[3], key[4], key[5]);
             const int m2 = __vimin3_s32(key[6], key[7], key[8]);
             const int best = __vimin3_s32(__vimin3_s32(m0, m1, m2), key[9], key[10]);
-            cur[s] = (best >> 4) + nrv_i * cnt[s];
+            cur[s] = (best & ~15) + nrv_i * cnt[s];  // x16: prev*16 + pen*16 + 16 nrv cnt
             ch[s] = (int8_t)(best & 15);
         }
     } else {
@@ -969,12 +970,13 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
     const double lx = d.lambda_x, rv = d.rho_vote;
     const bool use_int = SP > 0 && lx == floor(lx) && rv == floor(rv) && lx < 1e6 && rv < 1e6 &&
                          (double)nrows * (rv * (double)d.aux[f].votes + 5.0 * lx) < 33554432.0;
-    const int nrv_i = use_int ? -(int)rv : 0;
+    // int path: energies are stored x16 (< 2^29), so a stage's keys need no multiply
+    const int nrv_i = use_int ? -16 * (int)rv : 0;
     if (threadIdx.x < 10) {  // sentinels: states outside [0, C) never win
         const int k = threadIdx.x < 5 ? (int)threadIdx.x - 5 : C + (int)threadIdx.x - 5;
         if (use_int) {
-            ((int*)prev)[k] = 1 << 26;
-            ((int*)cur)[k] = 1 << 26;
+            ((int*)prev)[k] = 1 << 30;
+            ((int*)cur)[k] = 1 << 30;
         } else {
             prev[k] = __longlong_as_double(0x7ff0000000000000LL);
             cur[k] = __longlong_as_double(0x7ff0000000000000LL);
@@ -1057,7 +1059,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
     double mv = __longlong_as_double(0x7ff0000000000000LL);
     int mi = 0x7fffffff;
     for (int s = threadIdx.x; s < C; s += blockDim.x) {
-        const double e = use_int ? (double)((const int*)prev)[s] : prev[s];
+        const double e = use_int ? (double)(((const int*)prev)[s] >> 4) : prev[s];
         if (e < mv) {
             mv = e;
             mi = s;
@@ -1067,7 +1069,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
     const long long t2 = clock64();
 #endif
     const int term = block_argmin(mv, mi, sv, si);
-    const double energy = use_int ? (double)((const int*)prev)[term] : prev[term];
+    const double energy = use_int ? (double)(((const int*)prev)[term] >> 4) : prev[term];
     // backtrack (dp.hpp:67-71) in windows of BT_CHUNK stages staged in smem
     int p = term;
     if (threadIdx.x == 0) {
