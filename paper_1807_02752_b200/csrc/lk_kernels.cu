@@ -1272,7 +1272,11 @@ __global__ void __launch_bounds__(256) k_wg(Dev d) {
 __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist) {
     extern __shared__ double sh5[];
     const int f = blockIdx.z;
-    if (frame_failed(d, f)) return;
+    // independent loads issued together: most tiles need only these (one memory latency)
+    const int status = d.rep[f].status, v_top = (int)d.rep[f].horizon;
+    // k_wg marked the tiles with a non-zero w_g in reach
+    const int nonzero = d.wg_nz[((size_t)f * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x];
+    if (status != 0) return;
     if (d.W < 3 || d.H < 3) {  // lanes.hpp:68 (stage 10 already rejects this)
         if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
             fail_frame(d, f, 12, LK_MSG_M1_TOO_SMALL);
@@ -1280,7 +1284,7 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
     }
     const int W = d.W, H = d.H, nu = d.nu, vs = d.varsigma;
     const int u0 = blockIdx.x * M_TW, v0 = blockIdx.y * tile_h;
-    const int v_top = (int)d.rep[f].horizon, v_max = H - 1;
+    const int v_max = H - 1;
     // w_g is zero above v_top, so m0 vanishes on rows < v_top - vs and m1 on
     // rows < v_top - vs - 1: without hooks those rows are skipped (zero).
     const int first_row = d.hooks ? 0 : max(0, v_top - vs - 1);
@@ -1307,10 +1311,8 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
     const size_t eb = (size_t)f * d.px;
     const int r_lo = max(max(gr0, 0), v_top), r_hi = min(gr0 + GH - 1, v_max);
     // A tile without a non-zero w_g in reach has m0 = m1 = +0 everywhere: it
-    // is flagged instead of written (readers of m1 consult the flag). The test
-    // runs first, so such tiles (most of them) skip the staging entirely.
-    // k_gamma_fit marked the tiles with a non-zero w_g in reach
-    const int nonzero = d.wg_nz[((size_t)f * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x];
+    // is flagged instead of written (readers of m1 consult the flag), so such
+    // tiles (most of them) skip the staging entirely.
     if (nonzero) {
         if ((GH * GW & 1) == 0)
             for (int i = threadIdx.x; i < GH * GW / 2; i += blockDim.x)
