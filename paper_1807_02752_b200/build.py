@@ -62,7 +62,7 @@ def build_cli(force: bool = False, verbose: bool = False) -> Path:
     if not force and CLI.exists() and CLI.stat().st_mtime >= max(
             src.stat().st_mtime, LIB.stat().st_mtime):
         return CLI
-    cmd = [os.environ.get("CXX", "g++"), "-std=c++17", "-O2", "-Wall", str(src),
+    cmd = [os.environ.get("CXX", "g++"), "-std=c++17", "-O2", "-Wall", "-pthread", str(src),
            f"-L{PKG}", "-llanekit_b200", "-lz", "-Wl,-rpath,$ORIGIN", "-o", str(CLI)]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

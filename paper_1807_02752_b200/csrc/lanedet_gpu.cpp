@@ -2,8 +2,12 @@
 // the reference's `lanedet` (tools/lanedet.cpp:51-178):
 //
 //   lanedet_gpu detect --left L --right R --out-dir D [--config F] [--set k=v]... [--emit-all]
+//   lanedet_gpu stream --list PAIRS --out CSV [--batch N] [--config F] [--set k=v]... [--threads N]
 //   lanedet_gpu synth  --out-dir D [--seed S] [--width W] [--height H]
 //
+// stream feeds many KITTI-style pairs (image_io.hpp:75-149 decode on host
+// threads, pinned double-buffered slots) through lk_submit_stereo_batch and
+// writes one lane-result line per pair (see cmd_stream).
 // detect runs run_pipeline on the GPU (stages 1-12, LK_FLAG_STEREO | LK_FLAG_HOOKS)
 // and writes the reference's artifact set (artifacts.hpp:140-228): disparity.pgm,
 // vdisparity.pgm, vpx_accumulator.pgm, edges.png, lanes.csv, overlay.png and
@@ -19,6 +23,8 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
+#include <chrono>
 #include <charconv>
 #include <cmath>
 #include <cstdint>
@@ -27,9 +33,11 @@
 #include <filesystem>
 #include <fstream>
 #include <limits>
+#include <memory>
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/lanekit_b200.h"
@@ -656,10 +664,171 @@ int cmd_synth(const std::string& out_dir, uint64_t seed, int width, int height) 
     return 0;
 }
 
+// ---------------------------------------------------------------- stream
+//
+// Many stereo pairs (one "left right" pair of 8-bit PGM/PNG paths per line of
+// --list) through lk_submit_stereo_batch, one CSV line of lane results per
+// pair (the report fields of artifacts.hpp:59-107 that a fleet run keeps).
+// Two pinned input slots: while the GPU runs batch k from one slot, host
+// threads decode batch k+1 into the other, after batch k-1 (its last user)
+// has been waited for and written out. A pair that fails to decode, or whose
+// size differs from the first pair's, is reported as a stage-1 error and its
+// slot frame is zero-filled (the batch still runs; its result is dropped).
+
+struct PinnedBuf {
+    void* p = nullptr;
+    explicit PinnedBuf(size_t bytes) {
+        if (lk_host_alloc(&p, bytes)) throw Error(lk_last_error());
+    }
+    ~PinnedBuf() {
+        if (p) lk_host_free(p);
+    }
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+};
+
+std::string csv_quote(const std::string& s) {
+    std::string q = "\"";
+    for (char ch : s) q += ch == '"' ? std::string("\"\"") : std::string(1, ch);
+    return q + "\"";
+}
+
+int cmd_stream(const std::string& list_path, const std::string& out_path, const std::string& cfgp,
+               int batch, int threads, const std::vector<std::string>& overrides) {
+    const lk_config cfg = make_config(cfgp, overrides, 0);
+    std::vector<std::pair<std::string, std::string>> pairs;
+    {
+        std::ifstream in(list_path);
+        if (!in) throw Error("stream: cannot open " + list_path);
+        std::string line;
+        while (std::getline(in, line)) {
+            std::istringstream ls(line);
+            std::string l, r;
+            if (!(ls >> l)) continue;
+            if (l[0] == '#') continue;
+            if (!(ls >> r)) throw Error("stream: line without a right image: '" + line + "'");
+            pairs.emplace_back(l, r);
+        }
+    }
+    if (pairs.empty()) throw Error("stream: no stereo pairs in " + list_path);
+    auto load = [](const std::string& p) {
+        const auto ext = std::filesystem::path(p).extension().string();
+        return (ext == ".pgm" || ext == ".PGM") ? read_pgm8(p) : read_png8(p);
+    };
+    int W = 0, H = 0;
+    {
+        const Gray8 g = load(pairs[0].first);
+        W = g.w;
+        H = g.h;
+    }
+    if (W <= 0 || H <= 0) throw Error("stage 1 (block statistics): empty input image");
+    batch = std::max(1, std::min<int>(batch, (int)pairs.size()));
+    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    const size_t frame = (size_t)W * H;
+
+    Ctx c;
+    if (lk_create(&c.h, 0, &cfg, W, H, batch, LK_FLAG_STEREO)) throw Error(lk_last_error());
+    std::vector<std::unique_ptr<PinnedBuf>> lbuf, rbuf, repbuf;
+    std::vector<std::vector<std::string>> decode_err(2, std::vector<std::string>(batch));
+    for (int s = 0; s < 2; ++s) {
+        lbuf.emplace_back(new PinnedBuf(frame * batch));
+        rbuf.emplace_back(new PinnedBuf(frame * batch));
+        repbuf.emplace_back(new PinnedBuf(sizeof(lk_frame_report) * batch));
+    }
+    std::ofstream out(out_path);
+    if (!out) throw Error("stream: cannot open " + out_path);
+    out << "index,left,status,failed_stage,horizon,lane_count,bottom_cols,lane_energies,message\n";
+
+    // Decodes pairs [first, first+n) into slot s with `threads` workers.
+    auto decode = [&](int s, size_t first, int n) {
+        std::atomic<int> next{0};
+        auto work = [&]() {
+            for (int i; (i = next.fetch_add(1)) < n;) {
+                uint8_t* L = (uint8_t*)lbuf[s]->p + frame * i;
+                uint8_t* R = (uint8_t*)rbuf[s]->p + frame * i;
+                std::string& err = decode_err[s][i];
+                err.clear();
+                try {
+                    const Gray8 a = load(pairs[first + i].first), b = load(pairs[first + i].second);
+                    if (a.w != W || a.h != H || b.w != W || b.h != H)
+                        throw Error("stage 1 (block statistics): pair size differs from the stream's " +
+                                    std::to_string(W) + "x" + std::to_string(H));
+                    std::memcpy(L, a.px.data(), frame);
+                    std::memcpy(R, b.px.data(), frame);
+                } catch (const std::exception& e) {
+                    err = e.what();
+                    std::memset(L, 0, frame);
+                    std::memset(R, 0, frame);
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < std::min(threads, n); ++t) pool.emplace_back(work);
+        work();
+        for (auto& t : pool) t.join();
+    };
+    auto emit = [&](int s, size_t first, int n) {
+        const auto* rep = (const lk_frame_report*)repbuf[s]->p;
+        char msg[256];
+        for (int i = 0; i < n; ++i) {
+            const lk_frame_report& r = rep[i];
+            out << (first + i) << "," << csv_quote(pairs[first + i].first) << ",";
+            if (!decode_err[s][i].empty()) {
+                out << "error,1,,,,," << csv_quote(decode_err[s][i]) << "\n";
+                continue;
+            }
+            if (r.status) {
+                lk_frame_message(&r, msg, sizeof msg);
+                out << "error," << r.failed_stage << ",,,,," << csv_quote(msg) << "\n";
+                continue;
+            }
+            out << "ok,0," << r.horizon << "," << r.lane_count << ",";
+            const int shown = (int)std::min<int64_t>(r.lane_count, LK_MAX_INLINE_LANES);
+            for (int k = 0; k < shown; ++k) out << (k ? ";" : "") << r.lane_bottom_col[k];
+            out << ",";
+            for (int k = 0; k < shown; ++k) {
+                std::snprintf(msg, sizeof msg, "%s%.17g", k ? ";" : "", r.lane_energy[k]);
+                out << msg;
+            }
+            out << ",\n";
+        }
+    };
+
+    const auto t0 = std::chrono::steady_clock::now();
+    const size_t N = pairs.size();
+    const size_t nb = (N + batch - 1) / batch;
+    auto count = [&](size_t k) { return (int)std::min<size_t>(batch, N - k * batch); };
+    decode(0, 0, count(0));
+    for (size_t k = 0; k < nb; ++k) {
+        const int s = (int)(k & 1);
+        const lk_status st = lk_submit_stereo_batch(c.h, (const uint8_t*)lbuf[s]->p,
+                                                    (const uint8_t*)rbuf[s]->p, count(k),
+                                                    (lk_frame_report*)repbuf[s]->p);
+        if (st != LK_OK && st != LK_ERR_FRAME) throw Error(lk_last_error());
+        if (k >= 1) {  // batch k-1 owns slot s^1: finish it before decoding into that slot
+            const lk_status w = lk_wait_batch(c.h);
+            if (w != LK_OK && w != LK_ERR_FRAME) throw Error(lk_last_error());
+            emit(s ^ 1, (k - 1) * batch, count(k - 1));
+        }
+        if (k + 1 < nb) decode(s ^ 1, (k + 1) * batch, count(k + 1));  // overlaps batch k on the GPU
+    }
+    const lk_status w = lk_wait_batch(c.h);
+    if (w != LK_OK && w != LK_ERR_FRAME) throw Error(lk_last_error());
+    emit((int)((nb - 1) & 1), (nb - 1) * batch, count(nb - 1));
+    out.flush();
+    if (!out) throw Error("stream: write failed on " + out_path);
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "stream: %zu pairs (%dx%d) in %zu batches of <= %d, %.3f s, %.1f pairs/s, %d decode threads\n",
+                 N, W, H, nb, batch, s, N / s, threads);
+    return 0;
+}
+
 int usage() {
     std::fprintf(stderr,
                  "usage: lanedet_gpu detect --left L --right R --out-dir D [--config F] "
                  "[--set key=value]... [--emit-all] [--threads N]\n"
+                 "       lanedet_gpu stream --list PAIRS --out CSV [--batch N] [--config F] "
+                 "[--set key=value]... [--threads N]\n"
                  "       lanedet_gpu synth --out-dir D [--seed S] [--width W] [--height H]\n");
     return 2;
 }
@@ -669,9 +838,9 @@ int usage() {
 int main(int argc, char** argv) {
     if (argc < 2) return usage();
     const std::string cmd = argv[1];
-    std::string left, right, cfg, out_dir;
+    std::string left, right, cfg, out_dir, list, out_csv;
     bool emit_all = false;
-    int threads = 0, width = 640, height = 360;
+    int threads = 0, width = 640, height = 360, batch = 64;
     uint64_t seed = 1;
     std::vector<std::string> overrides;
     try {
@@ -686,6 +855,9 @@ int main(int argc, char** argv) {
             else if (a == "--config") cfg = val();
             else if (a == "--out-dir") out_dir = val();
             else if (a == "--set") overrides.push_back(val());
+            else if (a == "--list") list = val();
+            else if (a == "--out") out_csv = val();
+            else if (a == "--batch") batch = std::stoi(val());
             else if (a == "--threads") threads = std::stoi(val());
             else if (a == "--emit-all") emit_all = true;
             else if (a == "--seed") seed = std::stoull(val());
@@ -696,6 +868,10 @@ int main(int argc, char** argv) {
         if (cmd == "detect") {
             if (left.empty() || right.empty() || out_dir.empty()) return usage();
             return cmd_detect(left, right, cfg, out_dir, emit_all, threads, overrides);
+        }
+        if (cmd == "stream") {
+            if (list.empty() || out_csv.empty()) return usage();
+            return cmd_stream(list, out_csv, cfg, batch, threads, overrides);
         }
         if (cmd == "synth") {
             if (out_dir.empty()) return usage();

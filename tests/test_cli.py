@@ -116,3 +116,64 @@ def test_cli_detect_artifacts_match_reference(tmp_path, oracle):
     for f in ("overlay.png", "vpx_accumulator.pgm", "road_fit.csv", "smoothed.png", "m1.png",
               "energy_histogram.csv", "upath.csv", "vpath.csv", "block_sigma.png"):
         assert (od / f).exists(), f
+
+
+def test_cli_stream_rejects_bad_list(tmp_path):
+    out = subprocess.run([str(CLI), "stream", "--list", str(tmp_path / "none.txt"), "--out",
+                          str(tmp_path / "o.csv")], capture_output=True, text=True)
+    assert out.returncode == 1 and "stream: cannot open" in out.stderr
+    (tmp_path / "l.txt").write_text("# only a comment\n\n")
+    out = subprocess.run([str(CLI), "stream", "--list", str(tmp_path / "l.txt"), "--out",
+                          str(tmp_path / "o.csv")], capture_output=True, text=True)
+    assert out.returncode == 1 and "no stereo pairs" in out.stderr
+
+
+@pytest.mark.gpu
+def test_cli_stream_matches_reference(tmp_path, oracle):
+    """stream: pairs decoded on host threads into two pinned slots, batches of 2
+    through lk_submit_stereo_batch; every ok line equals the reference's
+    run_pipeline on that pair, bad pairs become stage-1 error lines in order."""
+    import csv
+
+    from checkers import Checker, ref_available
+
+    chk = Checker("ref") if ref_available() else oracle
+    pairs, scenes = [], {}
+    for seed in (1, 2, 3):
+        d = tmp_path / f"s{seed}"
+        out = subprocess.run([str(CLI), "synth", "--out-dir", str(d), "--seed", str(seed),
+                              "--width", "640", "--height", "360"], capture_output=True, text=True)
+        assert out.returncode == 0, out.stderr
+        scenes[seed] = d
+    small = tmp_path / "small"
+    subprocess.run([str(CLI), "synth", "--out-dir", str(small), "--seed", "9", "--width", "320",
+                    "--height", "240"], check=True, capture_output=True)
+    order = [1, 2, None, 3, "small", 1]
+    for o in order:
+        if o is None:
+            pairs.append(f"{tmp_path / 'missing.png'} {tmp_path / 'missing.png'}")
+        else:
+            d = small if o == "small" else scenes[o]
+            pairs.append(f"{d / 'left.png'} {d / 'right.png'}")
+    (tmp_path / "pairs.txt").write_text("\n".join(pairs) + "\n")
+    res = tmp_path / "lanes.csv"
+    out = subprocess.run([str(CLI), "stream", "--list", str(tmp_path / "pairs.txt"), "--out",
+                          str(res), "--batch", "2", "--threads", "3"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    rows = list(csv.DictReader(res.open()))
+    assert [int(r["index"]) for r in rows] == list(range(len(order)))
+    cfg = abi.default_config()
+    for o, r in zip(order, rows):
+        if o is None or o == "small":
+            assert r["status"] == "error" and r["failed_stage"] == "1"
+            assert ("png: cannot open" if o is None else "pair size differs") in r["message"]
+            continue
+        assert r["status"] == "ok", r
+        left, right = read_png(scenes[o] / "left.png"), read_png(scenes[o] / "right.png")
+        st = chk.stereo(left, right, cfg)
+        ref = chk.run(left, st["DISPARITY"], cfg)
+        rep = ref.report
+        assert int(r["horizon"]) == rep.horizon and int(r["lane_count"]) == rep.lane_count
+        cols = [int(x) for x in r["bottom_cols"].split(";")] if r["bottom_cols"] else []
+        n = min(rep.lane_count, abi.LK_MAX_INLINE_LANES)
+        assert cols == list(ref.get("LANES")["bottom_col"])[:n]
