@@ -83,7 +83,7 @@ constexpr int kMaxBranches = 16;      // concurrent frame ranges (streams) per b
 constexpr int kMinBranchFrames = 16;  // smallest range worth a branch
 constexpr int kH2dChunksDefault = 12; // host-fed batches: copy/compute pipeline depth
 constexpr int kBranchesDefault = 8;   // device-resident batches: concurrent frame ranges
-constexpr int kFastTableDefault = 27;  // tap pairs of the fast bilateral served by the range table
+constexpr int kFastTableDefault = 63;  // tap pairs of the fast bilateral served by the range table
 
 }  // namespace
 
@@ -470,6 +470,10 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         for (int k = 0; k < 12; ++k) {
             auto c10 = [&](int dj) { return dj < 0 || dj > 10 ? -INFINITY : lp.fbf.c[dj * 11 + 10]; };
             lp.fbf.c10[k] = make_float2(c10(k), c10(k - 1));
+            auto s10 = [&](int dj) {
+                return dj < 0 || dj > 10 ? 0.f : (float)std::exp(-(double)(25 + (dj - 5) * (dj - 5)) * inv_s2);
+            };
+            lp.fbf.s10[k] = make_float2(s10(k), s10(k - 1));
         }
         lp.fbf.c2 = (float)(-inv_r2 * log2e);
         for (int dj = -5; dj <= 5; ++dj)
@@ -484,7 +488,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
             fast_tab[256 + i] = i < 511 ? (float)std::exp(-dr * dr * inv_r2) : 0.f;
         }
         const char* m = std::getenv("LK_BF_TABLE");
-        lp.fast_table = m ? std::atoi(m) & 31 : kFastTableDefault;
+        lp.fast_table = m ? std::atoi(m) & 63 : kFastTableDefault;
         const char* tpc = std::getenv("LK_BF_TPC");  // tiles per CTA
         lp.fast_tpc = tpc ? std::atoi(tpc) : 24;
         d.bf_ntiles = ((W + lkg::BT_W - 1) / lkg::BT_W) * ((H + lkg::BT_H - 1) / lkg::BT_H);

@@ -115,7 +115,13 @@ __global__ void __launch_bounds__(256, 2) k_bilateral_fast(Dev d, FastBfParam p,
     constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
     constexpr int NPX = TWh * THh;
     static_assert(WIN == 11 && BT_R % 2 == 0 && TWh % 2 == 0, "packed pairs assume an 11-wide window");
-    __shared__ __align__(16) float s_v[2][NPX + 2];
+    // copy 1 starts 14 banks after copy 0 (mod 32): a half-warp's float2 row
+    // loads (even lanes from copy 0, odd lanes from copy 1) then hit 32
+    // distinct banks; NPX + 2 (bank offset 6) cost two wavefronts per
+    // half-warp, ~25 % of the kernel's shared-memory wavefronts
+    constexpr int SV = NPX + ((14 - NPX % 32) + 32) % 32;
+    static_assert(SV >= NPX + 1 && SV % 2 == 0 && SV % 32 == 14, "copy-1 bank offset");
+    __shared__ __align__(16) float s_v[2][SV];
     extern __shared__ __align__(16) float s_R[];  // [511][32]: R[k_q - k_p + 255], lane-replicated
     const int nbx = (d.W + BT_W - 1) / BT_W, nb = nbx * ((d.H + BT_H - 1) / BT_H);
     const int tile0 = blockIdx.x * tpc, tile1 = min(tile0 + tpc, n * nb);
@@ -186,11 +192,12 @@ __global__ void __launch_bounds__(256, 2) k_bilateral_fast(Dev d, FastBfParam p,
                 const float c = fmaf(-va[r], kA, cb);  // exact integer (x 2^-149)
                 cidx[r] = make_float2(c, c);
             }
-            float2 n11[BT_R / 2], d11[BT_R / 2], nv11[BT_R / 2];
+            float2 n11[BT_R / 2], d11[BT_R / 2], nv11[BT_R / 2], cidx11[BT_R / 2];
 #pragma unroll
             for (int m = 0; m < BT_R / 2; ++m) {
                 n11[m] = d11[m] = make_float2(0.f, 0.f);
                 nv11[m] = make_float2(-va[2 * m], -va[2 * m + 1]);
+                cidx11[m] = make_float2(cidx[2 * m].x, cidx[2 * m + 1].x);
             }
 #pragma unroll
             for (int jj = 0; jj < BT_R + 2 * RHO; ++jj) {
@@ -225,9 +232,16 @@ __global__ void __launch_bounds__(256, 2) k_bilateral_fast(Dev d, FastBfParam p,
                     const int k = jj - 2 * m;
                     if (k < 0 || k > WIN) continue;
                     const float2 vl2 = make_float2(vl, vl);
-                    const float2 dr = __fadd2_rn(vl2, nv11[m]);
-                    const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.c10[k]);
-                    const float2 w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                    float2 w;
+                    if ((TB >> 5) & 1) {  // table: index pair from outputs 2m, 2m + 1
+                        const float2 t = __ffma2_rn(vl2, kA2, cidx11[m]);
+                        w = __fmul2_rn(p.s10[k], make_float2(lds_f32(__float_as_uint(t.x)),
+                                                             lds_f32(__float_as_uint(t.y))));
+                    } else {
+                        const float2 dr = __fadd2_rn(vl2, nv11[m]);
+                        const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.c10[k]);
+                        w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                    }
                     n11[m] = __ffma2_rn(w, vl2, n11[m]);
                     d11[m] = __fadd2_rn(w, d11[m]);
                 }
@@ -689,7 +703,7 @@ __global__ void __launch_bounds__(128) k_sobel_decide(Dev d) {
 cudaError_t configure_fastpath() {
     cudaError_t e = cudaSuccess;
     for (auto fn : {k_bilateral_fast<5, 0>, k_bilateral_fast<5, 10>, k_bilateral_fast<5, 21>,
-                    k_bilateral_fast<5, 27>, k_bilateral_fast<5, 31>})
+                    k_bilateral_fast<5, 27>, k_bilateral_fast<5, 31>, k_bilateral_fast<5, 63>})
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 511 * 32 * 4);
     return e;
@@ -705,9 +719,9 @@ void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream
     switch (lp.fast_table) {
 #define LK_BF(M) \
     case M: k_bilateral_fast<5, M><<<pg, 256, kTableSmem, s>>>(d, lp.fbf, n, tpc, all); break;
-        LK_BF(0) LK_BF(10) LK_BF(21) LK_BF(27) LK_BF(31)
+        LK_BF(0) LK_BF(10) LK_BF(21) LK_BF(27) LK_BF(31) LK_BF(63)
 #undef LK_BF
-        default: k_bilateral_fast<5, 27><<<pg, 256, kTableSmem, s>>>(d, lp.fbf, n, tpc, all); break;
+        default: k_bilateral_fast<5, 63><<<pg, 256, kTableSmem, s>>>(d, lp.fbf, n, tpc, all); break;
     }
 }
 

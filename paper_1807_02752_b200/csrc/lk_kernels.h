@@ -34,6 +34,7 @@ struct FastBfParam {
     float2 sp[11][5];  // the same taps' spatial factors 2^c (range-table taps)
     float c[121];  // -ds * inv_s2 * log2(e) per tap
     float2 c10[12];  // 11th-column pair (c[k][10], c[k-1][10]), -inf outside the window
+    float2 s10[12];  // the same pair's spatial factors 2^c (0 outside the window; table taps)
     float c2;      // -inv_r2 * log2(e)
 };
 
