@@ -418,9 +418,9 @@ def run_ours(args):
                           if dom == 9 else f"stage {dom} kernels (see stage_ms)",
                 "taps_per_s": taps / (dom_ms * 1e-3) if dom == 9 else None,
                 "mufu_ex2_only_ceiling_per_s": xu_ex2_peak,
-                "note": "range weights split between MUFU ex2 and a conflict-free shared-"
-                        "memory table (LK_BF_TABLE tap-pair mask, default 27: pairs 0, 1, 3, 4 "
-                        "from the table; pair 2 and the 11th column on MUFU); FMA-pipe- and "
+                "note": "range weights from a conflict-free shared-memory table "
+                        "(LK_BF_TABLE tap-pair mask, default 63: all five pairs and the 11th "
+                        "column from the table; MUFU ex2 is the per-pair alternative); FMA-pipe- and "
                         "LSU-bound (profiles/r01_k_bilateral_fast_ncu.txt). taps are nominal: "
                         "tiles with no road-mask pixel within one pixel are skipped"},
         },
