@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
 // arithmetic of k_bilateral_tile / preprocess.hpp:38-56, j-major / i-minor,
 // the grey bytes and weight-table gathers of row j+1 issued before row j's
 // dependent add chain. One thread per pixel keeps every SM full of chains.
-// k/255.0 comes from shared memory; an interior window row is read as four
+// k/255.0 is computed exactly (grey_value); an interior window row is read as four
 // 32-bit words (the input buffers carry 16 bytes of padding).
 template <int RHO>
 __device__ __forceinline__ void refine_row(const uint8_t* g, size_t rowoff, const int (&col)[2 * RHO + 1],
@@ -585,16 +585,26 @@ __device__ __forceinline__ void refine_row(const uint8_t* g, size_t rowoff, cons
     }
 }
 
+// k / 255.0 correctly rounded without a table: q0 = RN(k y), y = RN(1/255),
+// then one Markstein step q = RN(q0 + RN(k - q0 255) y) (both FMAs). Exact for
+// all 256 k (checked exhaustively; 24 of the plain products q0 are off by one
+// ulp). The FP64 pipe is ~14 % busy in this kernel while a shared-memory table
+// of doubles cost ~1.5 bank-conflict wavefronts per lookup on the LSU pipe,
+// which the weight-table gathers already keep ~77 % busy.
+__device__ __forceinline__ double grey_value(uint8_t k) {
+    constexpr double y = 1.0 / 255.0;
+    const double x = (double)k;
+    const double q0 = __dmul_rn(x, y);
+    return __fma_rn(__fma_rn(-q0, 255.0, x), y, q0);
+}
+
 template <int RHO>
 __global__ void __launch_bounds__(256) k_refine_exact(Dev d, WsParam ws) {
     constexpr int WIN = 2 * RHO + 1;
-    __shared__ double s_val[256];
     const int f = blockIdx.y;
     if (frame_failed(d, f)) return;
     const unsigned cnt = d.need_cnt[f];
     if (blockIdx.x * blockDim.x >= cnt) return;
-    s_val[threadIdx.x] = __ldg(d.val + threadIdx.x);
-    __syncthreads();
     const uint32_t* list = d.need + (size_t)f * d.need_cap;
     const uint8_t* g = d.grey + (size_t)f * d.px;
     const int W = d.W, H = d.H;
@@ -627,7 +637,7 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, WsParam ws) {
 #pragma unroll
             for (int k = 0; k < WIN; ++k) {
                 const double w = ws.w[j * WIN + k] * wr_cur[k];
-                num += w * s_val[k_cur[k]];
+                num += w * grey_value(k_cur[k]);
                 den += w;
             }
 #pragma unroll
