@@ -1355,18 +1355,20 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
     // hold zeros in gw: adding +-0.0 to a running sum that starts at +0.0 never
     // changes it, so summing them instead of skipping is bit-identical.
     if (nu == 1 && (GW & 1) == 0) {
-        // 3-wide window: a thread sums 4 consecutive outputs of a row, each
-        // in its own y-major / x-minor order, from 16-byte loads of the 6
-        // columns they span (each loaded value serves up to 3 of the sums)
-        constexpr int Q = 4;
+        // 3-wide window: a thread sums 2 consecutive outputs of a row, each
+        // in its own y-major / x-minor order, from two 16-byte loads of the 4
+        // columns they span. Consecutive lanes' loads are then contiguous (16 B
+        // apart): with 4 outputs per thread they were 32 B apart and every
+        // load took twice the shared-memory wavefronts (ncu: 25 M conflicts).
+        constexpr int Q = 2;
         const int per_row = (MW + Q - 1) / Q;
         for (int i = threadIdx.x; i < MH * per_row; i += blockDim.x) {
             const int r = i / per_row, c = (i - r * per_row) * Q;
             const double2* g0 = reinterpret_cast<const double2*>(gw + r * GW + c);  // 16-byte aligned
-            double s[Q] = {0.0, 0.0, 0.0, 0.0};
+            double s[Q] = {0.0, 0.0};
             for (int y = 0; y <= 2 * vs; ++y) {
-                const double2 a = g0[0], b = g0[1], e = g0[2];  // columns c .. c+5
-                const double g[6] = {a.x, a.y, b.x, b.y, e.x, e.y};
+                const double2 a = g0[0], b = g0[1];  // columns c .. c+3
+                const double g[4] = {a.x, a.y, b.x, b.y};
 #pragma unroll
                 for (int k = 0; k < Q; ++k) {
                     s[k] += g[k];
