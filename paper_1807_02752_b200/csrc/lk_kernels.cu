@@ -1694,10 +1694,12 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
                 np += !isnan(u);
             }
             // llround(u) in [0, W)  <=>  -0.5 < u < W - 0.5 (NaN fails); then
-            // llround = trunc + (frac >= 0.5), exact for these magnitudes
+            // llround = trunc(RN(u + 0.5)): the sum is exact or rounds within
+            // its unit interval for every such u except 0.5 - 2^-54, whose sum
+            // rounds up to 1.0 (llround gives 0). One instruction fewer than
+            // trunc + (frac >= 0.5) on this issue-bound loop.
             if (u > -0.5 && u < w_hi) {
-                const int t = (int)u;
-                const int r = t + (u - (double)t >= 0.5);
+                const int r = (int)(u + 0.5) - (u == 0x1.fffffffffffffp-2);
                 if (s_nz[(v >> d.m_tile_shift) * d.m_ntx + (r >> 7)]) idx[k] = v * W + r;  // < 2^31
             }
         }

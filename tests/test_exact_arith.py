@@ -22,3 +22,39 @@ def test_grey_value_markstein_is_exact_for_every_grey_level():
         q = _fma(_fma(-q0, 255.0, x), y, q0)
         assert q == x / 255.0, k
     assert plain_off == 24  # the correction step is needed: the bare product is off for 24 levels
+
+
+def test_energy_track_llround_via_half_add():
+    """k_energy (csrc/lk_kernels.cu): llround(u) for -0.5 < u < W - 0.5 as
+    trunc(RN(u + 0.5)) minus the one u whose sum rounds up (0.5 - 2^-54).
+    Checked on the binade edges and half-integers where it could break."""
+    import math
+
+    import numpy as np
+
+    def fast(u):
+        return int(u + 0.5) - (u == float.fromhex("0x1.fffffffffffffp-2"))
+
+    cases = []
+    for n in range(0, 4100):
+        for base in (n - 0.5, n + 0.5, float(n)):
+            x = base
+            for _ in range(4):
+                cases += [x]
+                x = np.nextafter(x, -np.inf)
+            x = base
+            for _ in range(4):
+                x = np.nextafter(x, np.inf)
+                cases += [x]
+    for k in range(-60, 13):
+        p = 2.0 ** k
+        cases += [p, np.nextafter(p, 0), np.nextafter(p, np.inf), p - 0.5, p + 0.5]
+    rng = np.random.default_rng(0)
+    cases += list(rng.uniform(-0.5, 4096, 200000))
+    for u in cases:
+        u = float(u)
+        if not (-0.5 < u < 4095.5):
+            continue
+        # C llround (half away from zero) on -0.5 < u: 0 for negatives, else floor + (frac >= 0.5)
+        exact = 0 if u < 0 else math.floor(u) + (1 if u - math.floor(u) >= 0.5 else 0)
+        assert fast(u) == exact, u
