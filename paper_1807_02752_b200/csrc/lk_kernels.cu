@@ -1633,6 +1633,19 @@ __global__ void __launch_bounds__(256) k_p99_select(Dev d) {
 // one thread per extended bottom column, the track recursion and the decayed
 // m1 sum run together from the bottom row upward.
 // =====================================================================
+// One lane_track step (lanes.hpp:91-94): u' = ((vpx + v u) - vpy u) / denom,
+// the quotient as RN(a y) + one Markstein correction (= IEEE a / denom, see
+// k_energy) unless an operand is zero, non-finite or extreme.
+__device__ __forceinline__ double track_step(const double4 rw, int v, double u) {
+    const double a = rw.x + (double)v * u - rw.y * u;
+    const double aa = fabs(a);
+    if (aa >= 0x1p-500 && aa <= 0x1p500 && fabs(rw.z) <= 0x1p500) {
+        const double q0 = __dmul_rn(a, rw.w);
+        return __fma_rn(__fma_rn(-q0, rw.z, a), rw.w, q0);
+    }
+    return a / rw.z;
+}
+
 __global__ void __launch_bounds__(128) k_energy(Dev d) {
     extern __shared__ double4 sh_e4[];  // per row v: (vpx[v+1], vpy[v+1], denom, 1/denom)
     __shared__ int s_dead;
@@ -1667,9 +1680,9 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
     const double lg = d.lambda_g;
     const double w_hi = (double)W - 0.5;
     const int v_alive = max(v_top, s_dead + 1);  // rows v_alive..v_max carry the track
-    double u = (double)(d.ext_lo + ci);
+    const double u_bottom = (double)(d.ext_lo + ci);
+    double u = u_bottom;
     double e = 0.0;
-    int np = 1;  // lane_track's finite points (lanes.hpp:83-96), for k_select
     // Chunks of EC rows: the track recursion (lane_track, lanes.hpp:83-96)
     // yields EC gather indices, the EC m1 loads are then all in flight
     // together, and the decayed sum consumes them in row order.
@@ -1681,18 +1694,7 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
             const int v = vc - k;
             idx[k] = -1;
             if (v < v_alive) continue;
-            if (v < v_max) {
-                const double4 rw = sh_e4[v];
-                const double a = rw.x + (double)v * u - rw.y * u;
-                const double aa = fabs(a);
-                if (aa >= 0x1p-500 && aa <= 0x1p500 && fabs(rw.z) <= 0x1p500) {
-                    const double q0 = __dmul_rn(a, rw.w);
-                    u = __fma_rn(__fma_rn(-q0, rw.z, a), rw.w, q0);
-                } else {
-                    u = a / rw.z;
-                }
-                np += !isnan(u);
-            }
+            if (v < v_max) u = track_step(sh_e4[v], v, u);
             // llround(u) in [0, W)  <=>  -0.5 < u < W - 0.5 (NaN fails); then
             // llround = trunc(RN(u + 0.5)): the sum is exact or rounds within
             // its unit interval for every such u except 0.5 - 2^-54, whose sum
@@ -1713,6 +1715,18 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
     // rows after the track stops contribute +0.0 (kept: 0 + (-0.0) is +0.0)
     for (int v = v_alive - 1; v >= v_top; --v) e = 0.0 + lg * e;
     d.energy[(size_t)f * d.ext_cols + ci] = e;
+    // lane_track's finite points (lanes.hpp:83-96), for k_select: NaN is
+    // absorbing in track_step (every operation propagates it), so a non-NaN
+    // final u means every step was finite; otherwise (rare) recount.
+    int np = 1 + max(0, v_max - v_alive);
+    if (isnan(u)) {
+        np = 1;
+        double w = u_bottom;
+        for (int v = v_max - 1; v >= v_alive; --v) {
+            w = track_step(sh_e4[v], v, w);
+            np += !isnan(w);
+        }
+    }
     d.track_np[(size_t)f * d.ext_cols + ci] = np;
 }
 
