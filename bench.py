@@ -87,6 +87,17 @@ def make_frames(scene_fn, n_pool: int, batch: int, seed0: int, stereo: bool = Fa
     return np.ascontiguousarray(grey), np.ascontiguousarray(disp)
 
 
+def ref_frames(chk, scene_fn, n: int, seed0: int):
+    """(grey, disparity) [n, H, W] from the reference's gen_scene + 8-bit
+    quantisation (oracle/ref_wrapper.cpp lkref_gen_scene)."""
+    gs, ds = [], []
+    for i in range(n):
+        left, _, disp, _ = chk.gen_scene(scene_fn(seed0 + i))
+        gs.append(left)
+        ds.append(disp)
+    return np.ascontiguousarray(np.stack(gs)), np.ascontiguousarray(np.stack(ds))
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -200,12 +211,16 @@ def run_reference(args):
     scene_fn, cfg, W, H, B, desc = workload(args.config, args.batch)
     cores = os.cpu_count() or 1
     per_step = cores  # one frame per host thread per step: a bounded sample
-    grey, disp = make_frames(scene_fn, per_step, per_step, 1)
     sys.path.insert(0, str(ROOT / "tests"))
     from checkers import Checker, ref_available
 
     kind = "reference" if ref_available() else "port"
     chk = Checker("ref" if kind == "reference" else "oracle")
+    # the same frames as the GPU arm's first per_step (seeds 1..), rendered by the
+    # reference's own gen_scene (synth.hpp:103) so this process never loads the
+    # product library; the port falls back to the repo's restatement of it
+    grey, disp = (ref_frames(chk, scene_fn, per_step, 1) if kind == "reference"
+                  else make_frames(scene_fn, per_step, per_step, 1))
     for _ in range(max(0, min(args.warmup, 1))):
         chk.run_batch(grey, disp, cfg, threads=cores)
     steps = max(1, min(args.steps, 8))
@@ -275,6 +290,7 @@ def run_ours(args):
     if st not in (abi.LK_OK, abi.LK_ERR_FRAME):
         raise RuntimeError(L.lk_last_error().decode())
     failed = sum(1 for r in reps if r.status)
+    gpu_reps = [abi.LkFrameReport.from_buffer_copy(r) for r in reps]
 
     launches = pipe.launches_per_batch
     for _ in range(args.warmup):
@@ -322,16 +338,23 @@ def run_ours(args):
     for _ in range(2):
         L.lk_wait_batch(h)
     torch.cuda.synchronize()
+    e2e_failed = []  # failed frames of every streamed batch, counted after its wait
+
+    def drain(k):
+        if L.lk_wait_batch(h) not in (abi.LK_OK, abi.LK_ERR_FRAME):
+            raise RuntimeError(L.lk_last_error().decode())
+        e2e_failed.append(sum(1 for i in range(B) if rbufs[k % 2][i].status))
+
     e2.record(stream)
     for k in range(e2_steps):
         submit(h, hg, hd, B, rbufs[k % 2])
         if k >= 1:
-            L.lk_wait_batch(h)
-    L.lk_wait_batch(h)
+            drain(k - 1)
+    drain(e2_steps - 1)
     e3.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)
-    failed = max(failed, sum(1 for i in range(B) if rbufs[(e2_steps - 1) % 2][i].status))
+    failed = max([failed] + e2e_failed)
     for rb in rbufs:
         L.lk_host_free(C.cast(rb, C.c_void_p))
 
@@ -436,8 +459,19 @@ def run_ours(args):
         except Exception:
             pass
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb, _ = cpu_baseline(grey, disp, cfg, frames=2 * (os.cpu_count() or 8), stereo=stereo)
+        cb, ref_reps = cpu_baseline(grey, disp, cfg, frames=2 * (os.cpu_count() or 8),
+                                    stereo=stereo)
         line["cpu_baseline"] = cb
+        # the frames the baseline just ran, compared report field by report field
+        # with this run's GPU reports (tests/parity.py rules: integers exact,
+        # FP within 1e-5)
+        from parity import compare_reports
+
+        bad = [(i, b) for i, r in enumerate(ref_reps)
+               for b in compare_reports(gpu_reps[i], r)]
+        line["parity"] = {"frames": len(ref_reps), "against": cb["kind"],
+                          "mismatches": len({i for i, _ in bad}),
+                          "first": bad[0][1] if bad else None}
     if rank == 0:
         print(json.dumps(line), flush=True)
     pipe.close()

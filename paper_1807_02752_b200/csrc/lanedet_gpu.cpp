@@ -128,8 +128,14 @@ Gray8 read_png8(const std::string& path) {
         if (o + 12 + len > f.size()) throw Error("png: truncated chunk in " + path);
         const uint8_t* d = &f[o + 8];
         if (type == "IHDR") {
-            g.w = (int)be32(d);
-            g.h = (int)be32(d + 4);
+            if (len != 13) throw Error("png: malformed IHDR in " + path);
+            const uint32_t w = be32(d), h = be32(d + 4);
+            // the GPU context's limits (lk_create): checked before any allocation
+            if (w < 1 || w > 65535 || h < 1 || h > 32767)
+                throw Error("png: " + path + ": size " + std::to_string(w) + "x" +
+                            std::to_string(h) + " outside 1..65535 x 1..32767");
+            g.w = (int)w;
+            g.h = (int)h;
             if (d[8] != 8 || d[9] != 0 || d[12] != 0)
                 throw Error("png: " + path + ": only 8-bit greyscale, non-interlaced PNG maps "
                             "exactly onto the u8 GPU input");
@@ -141,6 +147,7 @@ Gray8 read_png8(const std::string& path) {
         o += 12 + len;
     }
     if (g.w < 1 || g.h < 1) throw Error("png: missing IHDR in " + path);
+    if (idat.empty()) throw Error("png: no IDAT chunk in " + path);
     std::vector<uint8_t> raw((size_t)g.h * (g.w + 1));
     uLongf n = (uLongf)raw.size();
     if (uncompress(raw.data(), &n, idat.data(), (uLong)idat.size()) != Z_OK || n != raw.size())

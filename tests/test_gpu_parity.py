@@ -203,3 +203,32 @@ def test_streaming_submit_wait_matches_run_batch():
         assert L.lk_wait_batch(pipe._h) == abi.LK_ERR_INVALID_ARGUMENT  # nothing pending
         for b in range(4):
             assert [bytes(r) for r in got[b]] == want[b], b
+
+
+def test_headline_batch_256_vs_reference(oracle):
+    """All 256 frames of the bench's config-2 batch (batch_scene seeds 1..256,
+    bench.py make_frames) through the throughput path in one batch, against
+    the reference's own code (oracle/_ref; the restatement when it is absent):
+    every report field, plus the LANES, ENERGY, M1, VOTES, UPATH and the other
+    throughput-mode hooks of every frame (tests/parity.py rules)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from checkers import Checker, ref_available
+
+    chk = Checker("ref") if ref_available() else oracle
+    params = [scenes.batch_scene(1 + i) for i in range(256)]
+    grey, disp = lanekit.synth_batch(params, threads=8)
+    cfg = abi.default_config()
+    problems = []
+    with lanekit.GpuPipeline(1242, 375, cfg, max_batch=256) as pipe, \
+            ThreadPoolExecutor(8) as pool:
+        reps = pipe.run(grey, disp)
+        for c0 in range(0, 256, 16):  # ctypes drops the GIL: checker frames run in parallel
+            res = list(pool.map(lambda i: chk.run(grey[i], disp[i], cfg), range(c0, c0 + 16)))
+            for i, o in zip(range(c0, c0 + 16), res):
+                p = compare_reports(reps[i], o.report)
+                p += compare_frame(lambda name: pipe.stage(i, name), o, hooks=False)
+                problems += [f"frame {i}: {x}" for x in p]
+            del res
+    assert not problems, "\n".join(problems[:20])
+    assert all(r.status == 0 for r in reps)
