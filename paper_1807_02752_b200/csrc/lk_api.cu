@@ -363,7 +363,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     A(&d_val, val.size());
     A(&d_rng, rng.size());
     A(&c->in_grey, (size_t)B * d.px + 16);  // +16: k_refine_exact reads rows as whole words
-    A(&c->in_disp, (size_t)B * d.px);
+    A(&c->in_disp, (size_t)B * d.px + 16);  // +16: k_vdisparity stages 16-byte aligned spans
     if (d.stereo) {
         A(&c->in_right, (size_t)B * d.px);
         A(&d.sat, (size_t)B * 4 * d.px);
@@ -376,7 +376,6 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     }
     A(&d.rep, (size_t)B);
     A(&d.aux, (size_t)B);
-    A(&d.vhist, (size_t)B * H * D1);
     A(&c->lp.vhistT, (size_t)B * H * D1);
     A(&d.vpath, (size_t)B * D1 * 2);
     A(&d.beta_inl, (size_t)B * D1 * 2);
@@ -440,6 +439,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     lp.vpath_choice_smem = vp_base + (size_t)D1 * H <= 160 * 1024;
     lp.vpath_smem = vp_base + (lp.vpath_choice_smem ? (size_t)D1 * H : 0);
     if (!lp.vpath_choice_smem) A(&d.vchoice, (size_t)B * D1 * H);
+    lp.vdisp_smem = lkg::vdisparity_smem(W, D1);
     lp.road_smem = (size_t)(8 * D1 + 2) * 4 + (size_t)4 * D1 * 8 + 16;  // tbuf: (K+1) rows
     lp.bf_smem = (size_t)(256 + win * win) * 8 +
                  (size_t)(lkg::BF_TH + 2 * rho) * (lkg::BF_TW + 2 * rho) + 16;
@@ -535,7 +535,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     lp.sort_cap = sort_cap;
     lp.select_smem = (size_t)sort_cap * 12 + (size_t)((C + 31) / 32) * 4 + 16;
     const size_t smem_cap = prop.sharedMemPerBlockOptin;
-    if (lp.vpath_smem > smem_cap || lp.road_smem > smem_cap || lp.bf_smem > smem_cap || lp.bt_smem > smem_cap ||
+    if (lp.vdisp_smem > smem_cap || lp.vpath_smem > smem_cap || lp.road_smem > smem_cap || lp.bf_smem > smem_cap || lp.bt_smem > smem_cap ||
         lp.vanish_smem > smem_cap || lp.gamma_smem > smem_cap || lp.m_smem > smem_cap || lp.select_smem > smem_cap) {
         lk_destroy(c);
         return fail(LK_ERR_CONFIG, "frame geometry / window sizes exceed shared memory");
@@ -673,7 +673,6 @@ static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     sh(v.disp_out, px);
     sh(v.rep, 1);
     sh(v.aux, 1);
-    sh(v.vhist, H * D1);
     sh(lp.vhistT, H * D1);
     sh(v.vchoice, D1 * H);
     sh(v.vpath, D1 * 2);
@@ -798,6 +797,15 @@ static lk_status launch_range_graph(lk_ctx* c, size_t f0, int n, cudaStream_t st
 // copy is done (the copies share the link), and range k's graph starts as
 // soon as its own inputs are resident, so copies overlap the compute of the
 // ranges before them instead of preceding the whole batch.
+// Input slot 0 of the streaming API is the buffer the direct entry points
+// (lk_run_batch, lk_enqueue, ...) read. Once streaming has started, every batch
+// that reads slot 0 marks it free only after its kernels, so a later submit's
+// copy into slot 0 cannot overwrite the inputs of a batch still running.
+static lk_status release_slot0(lk_ctx* c) {
+    if (c->copy_stream && c->slot == 0) CU(cudaEventRecord(c->slot_free[0], c->stream));
+    return LK_OK;
+}
+
 static lk_status run_host_pipelined(lk_ctx* c, const uint8_t* grey, const uint8_t* disp, int n) {
     uint8_t* second = c->run_stereo ? c->in_right : c->in_disp;  // right grey or disparity
     int nk = c->h2d_chunks;
@@ -829,18 +837,23 @@ static lk_status run_host_pipelined(lk_ctx* c, const uint8_t* grey, const uint8_
         CU(cudaEventRecord(c->join[k - 1], c->side[k - 1]));
         CU(cudaStreamWaitEvent(c->stream, c->join[k - 1], 0));
     }
-    return LK_OK;
+    return release_slot0(c);
 }
+
+static lk_status enqueue_graph(lk_ctx* c, int n);
 
 static lk_status enqueue_mode(lk_ctx* c, int n) {
     CU(cudaSetDevice(c->device));
     c->last_n = n;
     c->last_stereo = c->run_stereo;
-    if (c->flags & LK_FLAG_NO_GRAPH) {
-        c->timed = true;
-        return enqueue_direct(c, n, true);
-    }
     c->timed = true;
+    const lk_status s = (c->flags & LK_FLAG_NO_GRAPH) ? enqueue_direct(c, n, true)
+                                                      : enqueue_graph(c, n);
+    if (s != LK_OK) return s;
+    return release_slot0(c);
+}
+
+static lk_status enqueue_graph(lk_ctx* c, int n) {
     const int key = 4 * n + 2 * c->slot + (c->run_stereo ? 1 : 0);
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
@@ -874,9 +887,12 @@ lk_status lk_wait_batch(lk_ctx* c) {
     if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
     if (c->n_pending == 0) return fail(LK_ERR_INVALID_ARGUMENT, "no submitted batch to wait for");
     const lk_ctx::Pending p = c->pending[0];
+    if (cudaError_t e = cudaEventSynchronize(c->slot_done[p.slot]); e != cudaSuccess) {
+        c->n_pending = 0;  // the stream is broken: no submitted batch can be reported
+        return fail(LK_ERR_CUDA, std::string("lk_wait_batch: ") + cudaGetErrorString(e));
+    }
     c->pending[0] = c->pending[1];
     --c->n_pending;
-    CU(cudaEventSynchronize(c->slot_done[p.slot]));
     bool any = false;
     if (p.reports)
         for (int i = 0; i < p.n; ++i) {
@@ -898,7 +914,7 @@ static lk_status submit(lk_ctx* c, const uint8_t* a, const uint8_t* b, int n,
     CU(cudaSetDevice(c->device));
     if (!c->copy_stream) {  // first use: the second input slot and the copy stream
         if (lk_status s = c->alloc(&c->slot_grey[1], (size_t)c->max_batch * c->d.px + 16)) return s;
-        if (lk_status s = c->alloc(&c->slot_disp[1], (size_t)c->max_batch * c->d.px)) return s;
+        if (lk_status s = c->alloc(&c->slot_disp[1], (size_t)c->max_batch * c->d.px + 16)) return s;
         c->slot_grey[0] = c->in_grey;
         c->slot_disp[0] = c->in_disp;
         CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
@@ -1101,7 +1117,17 @@ lk_status lk_get_stage(lk_ctx* c, int frame, int stage, void* dst, size_t capaci
         case LK_STAGE_DISP_LEFT: s = grab(d.disp_l + f * px, px); break;
         case LK_STAGE_DISP_RIGHT: s = grab(d.disp_r + f * px, px); break;
         case LK_STAGE_DISPARITY: s = grab(d.disp_out + f * px, px); break;
-        case LK_STAGE_VDISPARITY: s = grab(d.vhist + f * H * D1, H * D1 * 4); break;
+        case LK_STAGE_VDISPARITY: {  // stored transposed [D1][H] for the v-path DP
+            s = grab(c->lp.vhistT + f * H * D1, H * D1 * 4);
+            if (s != LK_OK) break;
+            std::vector<char> t(buf.size());
+            const int32_t* src = reinterpret_cast<const int32_t*>(buf.data());
+            int32_t* dst = reinterpret_cast<int32_t*>(t.data());
+            for (size_t v = 0; v < H; ++v)
+                for (size_t k = 0; k < D1; ++k) dst[v * D1 + k] = src[k * H + v];
+            buf.swap(t);
+            break;
+        }
         case LK_STAGE_VPATH: s = grab(d.vpath + f * D1 * 2, D1 * 8); break;
         case LK_STAGE_BETA_INLIERS:
             s = grab(d.beta_inl + f * D1 * 2, (size_t)rep.beta_inlier_count * 8);

@@ -75,7 +75,6 @@ struct Dev {
     // outputs / intermediates
     lk_frame_report* rep;
     FrameAux* aux;
-    int32_t* vhist;         // [B][H][D1]
     int8_t* vchoice;        // [B][D1][H]
     int32_t* vpath;         // [B][D1][2]
     int32_t* beta_inl;      // [B][D1][2]

@@ -15,86 +15,267 @@ namespace lkg {
 
 // =====================================================================
 // K1  build_vdisparity (road_profile.hpp:32-45) + valid-disparity count.
-// grid (ceil(H/K1_ROWS), n), 256 threads. Warp-aggregated shared atomics:
-// lanes holding the same (row, d) key add once via __match_any_sync.
-// Also writes the transposed histogram [D1][H] the v-path DP reads.
+// grid (ceil(H/R), n), 256 threads = 8 warps; warp w takes rows w, w+8, ...
+// of the CTA's R rows, so a row's histogram key is warp-uniform. The rows'
+// bytes arrive in shared memory by one TMA bulk copy (cp.async.bulk, mbarrier
+// transaction count). A row whose bytes all equal its first (road rows, the
+// sky) is one warp-level aggregate: a single shared atomic of W. Other rows go
+// 16-byte chunk by chunk: a uniform chunk extends the lane's (d, count) run, a
+// mixed one is merged per byte, and the lanes' runs are added with one shared
+// atomic per distinct d (all lanes equal: one add of the warp sum; else
+// __match_any_sync groups and their leaders). Only the transposed histogram
+// [D1][H] is written (the v-path DP's layout; the VDISPARITY hook transposes
+// it back on the host).
 // =====================================================================
 
-// One pixel of build_vdisparity: run-length merged into (key, run) so a road
-// row (one disparity almost everywhere) costs one shared atomic per run.
-__device__ __forceinline__ void vd_pixel(int dv, int row, int D1, int d_max, int32_t* hist,
-                                         int& key, int& run, unsigned long long& valid,
-                                         unsigned long long& counted) {
-    valid += dv != 0;
-    const bool in = dv >= 1 && dv <= d_max;  // road_profile.hpp:42
-    counted += in;
-    const int k = in ? row * D1 + dv : -1;
-    if (k != key) {
-        if (run) atomicAdd(&hist[key], run);
-        key = k;
-        run = 0;
-    }
-    run += in;
+constexpr int K1_UNROLL = 3;  // 3 x 32 x 16 B covers a 1242-px row in one round
+
+// Byte b (0..15) of a 16-byte chunk, without a local-memory array.
+__device__ __forceinline__ int chunk_byte(const uint4& q, int b) {
+    const int k = b >> 2;
+    const uint32_t w = k == 0 ? q.x : k == 1 ? q.y : k == 2 ? q.z : q.w;
+    return (w >> (8 * (b & 3))) & 0xff;
 }
 
-__global__ void __launch_bounds__(256) k_vdisparity(Dev d, int32_t* vhistT) {
-    extern __shared__ int32_t sh_hist[];  // [K1_ROWS][D1]
-    const int f = blockIdx.y;
-    const int v0 = blockIdx.x * K1_ROWS;
-    const int rows = min(K1_ROWS, d.H - v0);
-    const int D1 = d.D1, W = d.W, d_max = d.d_max;
-    for (int i = threadIdx.x; i < K1_ROWS * D1; i += blockDim.x) sh_hist[i] = 0;
-    __syncthreads();
-    // the CTA's rows as one byte range, read as aligned 16-byte chunks (each
-    // thread walks its chunk's 16 pixels in order) plus an unaligned head and tail
-    const uint8_t* disp = d.disp + (size_t)f * d.px + (size_t)v0 * W;
-    const int npx = rows * W;
-    const int head = min(npx, (int)((16 - (reinterpret_cast<uintptr_t>(disp) & 15)) & 15));
-    const int nchunk = (npx - head) >> 4, tail0 = head + 16 * nchunk;
-    unsigned long long valid = 0, counted = 0;
-    int key = -1, run = 0;
-    const uint4* chunks = reinterpret_cast<const uint4*>(disp + head);
-    for (int c = threadIdx.x; c < nchunk; c += blockDim.x) {
-        const uint4 q = __ldg(chunks + c);
-        const int i0 = head + 16 * c;
-        int row = i0 / W, col = i0 - row * W;
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int b = 0; b < 16; ++b) {
-            vd_pixel((w[b >> 2] >> (8 * (b & 3))) & 0xff, row, D1, d_max, sh_hist, key, run, valid,
-                     counted);
-            if (++col == W) {
-                col = 0;
-                ++row;
+// Bytes [lo, hi) of a row chunk, per byte (road_profile.hpp:42): valid and
+// counted totals, runs of equal d merged into per-lane shared atomics; the
+// last run is returned in (key, cnt) for the warp-aggregated add. Out of line:
+// it is rare and keeps the hot loop small.
+struct VdRun {
+    int key, cnt, valid, counted;
+};
+
+__device__ __noinline__ VdRun vd_row_chunk(uint4 q, int lo, int hi, int d_max, int32_t* hrow) {
+    VdRun o{-1, 0, 0, 0};
+    for (int b = lo; b < hi; ++b) {
+        const int dv = chunk_byte(q, b);
+        o.valid += dv != 0;
+        const int k = (dv >= 1 && dv <= d_max) ? dv : -1;
+        if (k != o.key) {
+            if (o.cnt) atomicAdd(&hrow[o.key], o.cnt);
+            o.key = k;
+            o.cnt = 0;
+        }
+        o.cnt += k >= 0;
+        o.counted += k >= 0;
+    }
+    return o;
+}
+
+// Warp-aggregated shared atomic of (key, cnt) per lane; cnt == 0 = nothing.
+// Called by whole warps.
+__device__ __forceinline__ void vd_warp_add(int32_t* hrow, int key, int cnt) {
+    const unsigned full = 0xffffffffu;
+    key = cnt ? key : -1;
+    const int k0 = __shfl_sync(full, key, 0);
+    if (__all_sync(full, key == k0)) {
+        const int sum = __reduce_add_sync(full, cnt);
+        if (k0 >= 0 && (threadIdx.x & 31) == 0) atomicAdd(&hrow[k0], sum);
+        return;
+    }
+    const unsigned grp = __match_any_sync(full, key);
+    const int sum = __reduce_add_sync(grp, cnt);
+    if (key >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&hrow[key], sum);
+}
+
+// One full 16-byte chunk's contribution: a uniform chunk extends the lane's
+// run (key, cnt); a mixed one goes through vd_row_chunk. A lane's run is
+// flushed with a per-lane atomic only when its key changes.
+__device__ __forceinline__ void vd_chunk(const uint4& q, int d_max, int32_t* hrow, int& key,
+                                         int& cnt, unsigned& valid, unsigned& counted) {
+    const uint32_t b0 = (q.x & 0xffu) * 0x01010101u;
+    const int dv = q.x & 0xff;
+    if (((q.x ^ b0) | (q.y ^ b0) | (q.z ^ b0) | (q.w ^ b0)) == 0) {
+        valid += dv ? 16 : 0;
+        if (dv >= 1 && dv <= d_max) {  // road_profile.hpp:42
+            counted += 16;
+            if (dv != key) {
+                if (cnt) atomicAdd(&hrow[key], cnt);
+                key = dv;
+                cnt = 0;
             }
+            cnt += 16;
+        }
+    } else {
+        const VdRun o = vd_row_chunk(q, 0, 16, d_max, hrow);
+        valid += o.valid;
+        counted += o.counted;
+        if (o.cnt) {
+            if (o.key != key) {
+                if (cnt) atomicAdd(&hrow[key], cnt);
+                key = o.key;
+                cnt = 0;
+            }
+            cnt += o.cnt;
         }
     }
-    for (int i = threadIdx.x; i < head + (npx - tail0); i += blockDim.x) {
-        const int j = i < head ? i : tail0 + (i - head);
-        vd_pixel(disp[j], j / W, D1, d_max, sh_hist, key, run, valid, counted);
+}
+
+// ---- one-shot TMA bulk staging (cp.async.bulk + mbarrier transaction count)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Arms the barrier with the byte count, then one bulk copy global -> shared
+// (addresses and size multiples of 16) that completes the transaction.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
+                                          uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Row r of the CTA = head bytes [rp, a) + full 16-byte chunks [a, e) + tail
+// bytes [e, rp + W), all in shared memory. One warp round covers the row's first
+// 32*K1_UNROLL chunks plus one head/tail byte per lane (lanes 0-15 head,
+// 16-31 tail).
+__device__ __forceinline__ void vd_row_geometry(const uint8_t* rp, int W, int& head, int& nfull) {
+    head = (int)((16 - (reinterpret_cast<uintptr_t>(rp) & 15)) & 15);
+    if (head > W) head = W;
+    nfull = (W - head) >> 4;
+}
+
+// K1 CTA = (block of R rows, frame). Thread 0 stages the rows' bytes (the
+// 16-byte aligned span around them) into shared memory with one bulk copy
+// while the others zero the histogram; the warps then count rows from shared
+// memory (warp w: rows w, w+8, ...). dynamic smem: barrier, hist [R][D1], span.
+__global__ void __launch_bounds__(256) k_vdisparity(Dev d, int32_t* vhistT, int R) {
+    extern __shared__ __align__(128) unsigned char k1s[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(k1s);
+    int32_t* sh_hist = reinterpret_cast<int32_t*>(k1s + 16);
+    const int D1 = d.D1, W = d.W, d_max = d.d_max;
+    uint8_t* span = k1s + 16 + (((size_t)R * D1 * 4 + 15) & ~(size_t)15);
+    const int f = blockIdx.y;
+    const int v0 = blockIdx.x * R;
+    const int rows = min(R, d.H - v0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint8_t* start = d.disp + (size_t)f * d.px + (size_t)v0 * W;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(start) & ~(uintptr_t)15;
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(start) + (size_t)rows * W + 15) & ~(uintptr_t)15;
+    if (threadIdx.x == 0) {  // (the inputs carry 16 bytes of padding past the last frame)
+        mbar_init(bar, 1);
+        bulk_load(span, reinterpret_cast<const void*>(a), (unsigned)(e - a), bar);
     }
-    if (run) atomicAdd(&sh_hist[key], run);
+    for (int i = threadIdx.x; i < R * D1; i += blockDim.x) sh_hist[i] = 0;
+    unsigned valid = 0, counted = 0;
+    const uint8_t* sbase = span + (reinterpret_cast<uintptr_t>(start) - a);
+    constexpr int RC = 32 * K1_UNROLL;  // chunks per warp round
+    __syncthreads();  // barrier initialised, histogram zeroed
+    mbar_wait(bar, 0);
+    for (int r = warp; r < rows; r += 8) {
+        const uint8_t* rp = sbase + (size_t)r * W;
+        int head, nfull;
+        vd_row_geometry(rp, W, head, nfull);
+        const uint4* a0 = reinterpret_cast<const uint4*>(rp + head);
+        const int tail = W - head - 16 * nfull;  // < 16
+        const int hb = lane < head ? (int)rp[lane]
+                     : (lane >= 16 && lane - 16 < tail) ? (int)rp[head + 16 * nfull + (lane - 16)]
+                                                        : -1;
+        uint4 q[K1_UNROLL];
+#pragma unroll
+        for (int j = 0; j < K1_UNROLL; ++j) {
+            const int c = lane + 32 * j;
+            q[j] = c < nfull ? a0[c] : make_uint4(0, 0, 0, 0);
+        }
+        int32_t* hrow = sh_hist + r * D1;
+        // whole-row test: every byte of the row equal to its first byte
+        const int ref = rp[0];
+        const uint32_t b4 = (uint32_t)ref * 0x01010101u;
+        uint32_t diff = hb >= 0 ? (uint32_t)(hb ^ ref) : 0u;
+#pragma unroll
+        for (int j = 0; j < K1_UNROLL; ++j)
+            if (lane + 32 * j < nfull)
+                diff |= (q[j].x ^ b4) | (q[j].y ^ b4) | (q[j].z ^ b4) | (q[j].w ^ b4);
+        if (nfull <= RC && __all_sync(0xffffffffu, diff == 0)) {
+            if (lane == 0) {  // the warp's whole-row aggregate: one shared atomic
+                valid += ref ? W : 0;
+                if (ref >= 1 && ref <= d_max) {  // road_profile.hpp:42
+                    atomicAdd(&hrow[ref], W);
+                    counted += W;
+                }
+            }
+            continue;
+        }
+        // mixed row: per chunk (uniform chunks merged into lane runs, mixed
+        // chunks per byte), then one warp-aggregated add of the lane runs
+        int key = -1, cnt = 0;
+        for (int c0 = 0; c0 < nfull; c0 += RC) {
+            if (c0) {
+#pragma unroll
+                for (int j = 0; j < K1_UNROLL; ++j) {
+                    const int c = c0 + lane + 32 * j;
+                    q[j] = c < nfull ? a0[c] : make_uint4(0, 0, 0, 0);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < K1_UNROLL; ++j)
+                if (c0 + lane + 32 * j < nfull)
+                    vd_chunk(q[j], d_max, hrow, key, cnt, valid, counted);
+        }
+        vd_warp_add(hrow, key, cnt);
+        int bk = -1, bc = 0;  // head / tail bytes, one per lane
+        if (hb >= 0) {
+            valid += hb != 0;
+            if (hb >= 1 && hb <= d_max) {
+                bk = hb;
+                bc = 1;
+                ++counted;
+            }
+        }
+        vd_warp_add(hrow, bk, bc);
+    }
     for (int o = 16; o; o >>= 1) {
         valid += __shfl_xor_sync(0xffffffffu, valid, o);
         counted += __shfl_xor_sync(0xffffffffu, counted, o);
     }
-    if ((threadIdx.x & 31) == 0) {
-        if (valid) atomicAdd((unsigned long long*)&d.rep[f].valid_disparities, valid);
-        if (counted) atomicAdd(&d.aux[f].hist_total, counted);
+    if (lane == 0) {
+        if (valid) atomicAdd((unsigned long long*)&d.rep[f].valid_disparities,
+                             (unsigned long long)valid);
+        if (counted) atomicAdd(&d.aux[f].hist_total, (unsigned long long)counted);
     }
     __syncthreads();
-    int32_t* out = d.vhist + ((size_t)f * d.H + v0) * D1;
-    int32_t* outT = vhistT + (size_t)f * D1 * d.H;
-    for (int i = threadIdx.x; i < rows * D1; i += blockDim.x) {
-        out[i] = sh_hist[i];
-        const int r = i / D1, c = i - r * D1;
-        outT[(size_t)c * d.H + v0 + r] = sh_hist[i];
-    }
+    // transposed store [D1][H]: warp per column, lane = row (R <= 32: runs of R ints)
+    int32_t* outT = vhistT + (size_t)f * D1 * d.H + v0;
+    for (int c = warp; c < D1; c += 8)
+        if (lane < rows) outT[(size_t)c * d.H + lane] = sh_hist[lane * D1 + c];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         lk_frame_report& rep = d.rep[f];
         rep.width = d.W;
         rep.height = d.H;
     }
+}
+
+// Rows per K1 CTA: as many as keep the CTA's shared memory (histogram rows +
+// staged bytes) within ~56 KB (4 CTAs per SM), at most one per lane.
+int vdisparity_rows(int W, int D1) {
+    const int r = (56 * 1024 - 160) / (W + 4 * D1 + 1);
+    return r < 1 ? 1 : r > K1_ROWS ? K1_ROWS : r;
+}
+
+size_t vdisparity_smem(int W, int D1) {
+    const int R = vdisparity_rows(W, D1);
+    return 16 + (((size_t)R * D1 * 4 + 15) & ~(size_t)15) + (size_t)R * W + 32;
 }
 
 // Block-wide (value, index) argmin, first index among equal minima (the
@@ -1885,8 +2066,11 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
             cudaEventRecord(stage_ev[stage], s);
     };
     if (mark_start) mark(0);
-    k_vdisparity<<<dim3((d.H + K1_ROWS - 1) / K1_ROWS, n), 256, K1_ROWS * d.D1 * 4, s>>>(
-        d, lp.vhistT);
+    {
+        const int R = vdisparity_rows(d.W, d.D1);
+        k_vdisparity<<<dim3((d.H + R - 1) / R, n), 256, vdisparity_smem(d.W, d.D1), s>>>(
+            d, lp.vhistT, R);
+    }
     mark(5);
     k_vpath<<<n, 512, lp.vpath_smem, s>>>(d, lp.vhistT, lp.vpath_choice_smem);
     mark(6);
@@ -1977,6 +2161,9 @@ int launches_per_batch(const Dev& d, const LaunchPlan& lp) {
 
 cudaError_t configure_kernels(const LaunchPlan& lp) {
     cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_vdisparity, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lp.vdisp_smem)))
+        return e;
     if ((e = cudaFuncSetAttribute(k_vpath, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lp.vpath_smem)))
         return e;

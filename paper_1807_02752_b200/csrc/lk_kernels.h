@@ -46,6 +46,7 @@ struct LaunchPlan {
     int fast_tpc;             // fast-bilateral tiles per CTA (LK_BF_TPC)
     int refine_ctas, decide_ctas;  // per-frame grids of k_refine_exact / k_sobel_decide
     int32_t* vhistT;          // [B][D1][H] transposed v-disparity for the v-path DP
+    size_t vdisp_smem;        // k_vdisparity: barrier + histogram rows + staged bytes
     size_t vpath_smem;
     int vpath_choice_smem;    // choices of the v-path DP kept in shared memory
     size_t road_smem;
@@ -73,6 +74,8 @@ cudaError_t configure_stereo(const Dev& d);
 size_t stereo_smem(const Dev& d);
 int stereo_launches();
 cudaError_t configure_kernels(const LaunchPlan& lp);
+int vdisparity_rows(int W, int D1);
+size_t vdisparity_smem(int W, int D1);
 cudaError_t configure_fastpath();
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all = 0);
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);

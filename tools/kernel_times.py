@@ -1,6 +1,7 @@
 """Device-resident replays only (no e2e, no CPU baseline): a clean target for
 an ncu launch list. usage: python tools/kernel_times.py [kitti|hires] [steps] [stereo]"""
 import ctypes as C
+import os
 import sys
 from pathlib import Path
 
@@ -10,6 +11,9 @@ from paper_1807_02752_b200 import abi, lanekit  # noqa: E402
 
 
 def main():
+    # one range per launch: every kernel launch covers the whole batch
+    os.environ.setdefault("LK_BRANCHES", "1")
+    os.environ.setdefault("LK_H2D_CHUNKS", "1")
     cfg_name = sys.argv[1] if len(sys.argv) > 1 else "kitti"
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     stereo = len(sys.argv) > 3 and sys.argv[3] == "stereo"

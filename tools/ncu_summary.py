@@ -13,6 +13,12 @@ METRICS = [
     ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1/LSU data-pipe wavefronts %"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("smsp__inst_executed_op_shared_atom.sum", "smem atomic instructions (warp)"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", "smem atomic wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum", "smem atomic bank conflicts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum.pct_of_peak_sustained_elapsed",
+     "smem atomic wavefronts % of peak"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active %"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
