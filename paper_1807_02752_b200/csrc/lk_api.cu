@@ -356,6 +356,8 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     };
     double *d_ws, *d_wr, *d_val;
     float* d_ft = nullptr;
+    float2* d_nt = nullptr;
+    std::vector<float2> need_tab;
     std::vector<float> fast_tab;
     uint64_t* d_rng;
     A(&d_ws, ws.size());
@@ -496,8 +498,41 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         d.need_cap = d.n_stile * (lkg::SB_TW + 2) * (lkg::SB_TH + 2);  // every ring pixel of every tile
         lp.refine_ctas = 8;
         lp.decide_ctas = 32;
+        // certified pre-screen constants (lk_fastpath.cu), each
+        // rounded toward the safe side
+        auto up = [](double x) {
+            float y = (float)x;
+            return (double)y < x ? std::nextafter(y, INFINITY) : y;
+        };
+        double wmin = 1.0;
+        for (double w : ws) wmin = std::min(wmin, w);
+        const double iw = 1.0 / wmin * (1.0 + 1e-12);
+        lp.ps.kappa = up(inv_r2);
+        lp.ps.inv_wmin = up(iw);
+        lp.ps.ew = up(iw - 1.0);
+        {  // sup over 0 < x <= 1 of (1 - exp(-kappa x^2)) / x; |f'| <= 2 kappa bounds the gap
+            const double h = 1e-5;
+            double fm = 0.0;
+            for (double x = h; x <= 1.0 + h / 2; x += h)
+                fm = std::max(fm, (1.0 - std::exp(-inv_r2 * x * x)) / x);
+            lp.ps.fmax = up(fm + 2.0 * inv_r2 * h + 1e-9);
+        }
+        lp.ps.c1 = up(1.0 / (121.0 * 255.0));
+        lp.ps.c2 = up(1.0 / (121.0 * 255.0 * 255.0));
+        lp.ps.s_star_lo = d.sobel_s_star_lo;
+        for (int j = 0; j < 11; ++j)
+            for (int i = 0; i < 11; ++i)
+                lp.nbf.S[j * 11 + i] = (float)(win == 11 ? ws[(size_t)j * 11 + i] : 0.0);
+        need_tab.resize(511);
+        for (int i = 0; i < 511; ++i) {
+            const double dl = i - 255, r = std::exp(-(dl / 255.0) * (dl / 255.0) * inv_r2);
+            need_tab[i] = make_float2((float)r, (float)(r * dl));
+        }
         if (lp.fast_front) {
             A(&d.smoothed_f, (size_t)B * d.px);
+            A(&d.pbits, (size_t)B * H * d.words_per_row);
+            A(&d.fneed, (size_t)B * d.px);
+            A(&d_nt, need_tab.size());
             A(&d.bf_flag, (size_t)B * d.bf_ntiles);
             A(&d.need, (size_t)B * d.need_cap);
             A(&d.need_cnt, (size_t)B);
@@ -545,6 +580,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         return s;
     }
     cudaError_t e = lkg::configure_kernels(lp);
+    lp.need_ctas = lkg::need_bilateral_ctas(prop.multiProcessorCount);
     if (e == cudaSuccess && d.stereo) {
         if (lkg::stereo_smem(d) > smem_cap) {
             lk_destroy(c);
@@ -570,6 +606,9 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     if (e == cudaSuccess) e = cudaMemcpy(d_rng, rng.data(), rng.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d_ft, fast_tab.data(), fast_tab.size() * 4, cudaMemcpyHostToDevice);
     d.fast_tab = d_ft;
+    if (e == cudaSuccess && d_nt)
+        e = cudaMemcpy(d_nt, need_tab.data(), need_tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
+    d.need_tab = d_nt;
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     for (int i = 0; i < 13 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     {
@@ -683,6 +722,8 @@ static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     sh(v.vpx, H);
     sh(v.smoothed, px);
     sh(v.smoothed_f, px);
+    sh(v.pbits, H * d.words_per_row);
+    sh(v.fneed, px);
     sh(v.bf_flag, (size_t)d.bf_ntiles);
     sh(v.need, (size_t)d.need_cap);
     sh(v.need_cnt, 1);

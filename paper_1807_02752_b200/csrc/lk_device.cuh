@@ -25,7 +25,7 @@ struct FrameAux {
     unsigned int p99_bucket2;      // next 12 bits inside the exponent bucket
     unsigned int p99_done;         // the percentile is exactly +0 (rank among the zeros)
     unsigned int p99_level2;       // bucket too large: narrowed by a second histogram
-    unsigned int pad3;
+    unsigned int fneed;             // need-list length of the FP32 bilateral (k_prescreen)
     unsigned long long p99_zeros;  // |m1| values that are exactly zero
     unsigned long long p99_rank;    // rank of the percentile inside the bucket
     double tr;                      // tr_lpv used
@@ -93,6 +93,9 @@ struct Dev {
     uint32_t* ctile_cnt;    // [B]
     int need_cap, n_stile;
     const float* fast_tab;  // [256] k/255 as float, then [512] range factor of dr = (i-255)/255
+    const float2* need_tab; // [511] (R(delta), R(delta) * delta), delta = i - 255 (k_bilateral_need)
+    uint32_t* pbits;        // [B][H][words_per_row] pre-screen survivors ("possibly an edge")
+    uint32_t* fneed;        // [B][px] pixels (v << 16 | u) whose s~ the Sobel screen needs
     uint32_t* ebits;        // [B][H][words_per_row]
     int n_seg;              // edge-list segments per row (ceil(W / SB_TW))
     int32_t* seg_cnt;       // [B][H][n_seg]

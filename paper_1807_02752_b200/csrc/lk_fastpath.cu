@@ -390,7 +390,8 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
     __shared__ __align__(8) float s_f[FH * FWP];
     __shared__ unsigned s_cw[SB_TH][TWORD];
     __shared__ unsigned s_need[FH][NWORD];
-    __shared__ int s_nneed, s_base, s_lo[SB_TH], s_hi[SB_TH];
+    __shared__ int s_nneed, s_base;
+    __shared__ unsigned s_pw[SB_TH][TWORD];  // pre-screen survivors (k_prescreen)
     const int f = blockIdx.z;
     if (frame_failed(d, f)) return;
     if (d.W < 3 || d.H < 3) {  // preprocess.hpp:68-69
@@ -410,19 +411,20 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
     // owned pixels: rows pr0 * SB_PPT + k (consecutive, so the 3x3 window slides
     // down one row per pixel), column pc
     const int pc = tid & (SB_TW - 1), pr0 = (tid >> 7) * SB_PPT;
-    // independent loads first: disparity and profile of the owned pixels, s~ tile
-    int dv[SB_PPT];
-#pragma unroll
-    for (int k = 0; k < SB_PPT; ++k) {
-        const int v = v0 + pr0 + k, u = u0 + pc;
-        dv[k] = v < H && u < W ? d.disp[(size_t)f * d.px + (size_t)v * W + u] : 0;
+    // only pre-screen survivors (masked pixels that can still be edges) are
+    // screened; a tile without survivors has no edge
+    bool anyp = false;
+    if (tid < SB_TH * TWORD) {
+        const int r = tid / TWORD, w = (u0 >> 5) + tid % TWORD;
+        const unsigned x = v0 + r < H && w < d.words_per_row
+                               ? d.pbits[((size_t)f * H + v0 + r) * d.words_per_row + w] : 0u;
+        s_pw[r][tid % TWORD] = x;
+        anyp = x != 0;
     }
-    // road_mask as per-row disparity intervals (k_road_fit, mask_interval): each
-    // pixel's test is two integer compares
-    if (tid < SB_TH) {
-        const int2 m = v0 + tid < H ? d.mrange[(size_t)f * H + v0 + tid] : make_int2(256, 0);
-        s_lo[tid] = m.x;
-        s_hi[tid] = m.y;
+    if (!__syncthreads_or(anyp)) {
+        if (tid < SB_TH && v0 + tid < H)
+            d.seg_cnt[((size_t)f * H + v0 + tid) * d.n_seg + blockIdx.x] = 0;
+        return;
     }
     // s~ tile + ring: s_f[r][j] holds column u0 - 2 + j (j = c + 1 for ring column c),
     // so interior tiles stage aligned 8-byte pairs (row starts are 8-byte aligned)
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
     if (tid == 0) s_nneed = 0;
     __syncthreads();
     const float D = (float)(8.0 * kEpsSmooth + 1e-6);
-    int n_mask = 0, any_cand = 0;
+    int any_cand = 0;
     // window rows v-1, v, v+1 at columns u-1, u, u+1 (ring row r holds image row v0 - 1 + r)
     float a[3], b[3], cc[3];
     {
@@ -479,8 +481,7 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
 #pragma unroll
             for (int x = 0; x < 3; ++x) cc[x] = p[x];
         }
-        const bool m = dv[k] >= s_lo[r] && dv[k] <= s_hi[r];  // road_mask, preprocess.hpp:14-25
-        n_mask += m;
+        const bool m = (s_pw[r][pc >> 5] >> (pc & 31)) & 1;  // survivor => road_mask pixel
         bool cand = false;
         if (m) {
             const float gx = ((a[2] - a[0]) + 2.f * (b[2] - b[0])) + (cc[2] - cc[0]);
@@ -499,8 +500,6 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
             b[x] = cc[x];
         }
     }
-    for (int o = 16; o; o >>= 1) n_mask += __shfl_xor_sync(0xffffffffu, n_mask, o);
-    if (lane == 0 && n_mask) atomicAdd(&d.aux[f].mask_px, (unsigned long long)n_mask);
     if (!__syncthreads_or(any_cand)) {  // no edge can exist in this tile (most tiles)
         if (tid < SB_TH && v0 + tid < H)
             d.seg_cnt[((size_t)f * H + v0 + tid) * d.n_seg + blockIdx.x] = 0;
@@ -650,6 +649,333 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, WsParam ws) {
     }
 }
 
+// ---- 0. certified pre-screen (k_prescreen) and the need-list bilateral
+//
+// Which masked pixels can possibly be edges, decided from integer box sums
+// of the raw grey bytes, before any bilateral arithmetic. With
+// delta_q = v_q - v_p, beta the normalised spatial weights of p's window,
+// r_q = exp(-kappa delta_q^2) the range factors (kappa = 1/sigma_r^2) and
+// e_q = 1 - r_q in [0, min(1, kappa delta_q^2)]:
+//   s(p) - g(p) = (ebar * m1 - sum beta e delta) / (1 - ebar),
+// g the beta-weighted mean, m1 = g - v_p, ebar = sum beta e <= kappa m2,
+// m2 = sum beta delta^2, |e delta| <= fmax delta^2 (fmax = sup (1 - exp(-kappa
+// x^2)) / x). The spatial weights lie in [w_min, 1] (w_min = 0.99944 at the
+// default sigma_s = 300), so beta-moments are bounded by box moments: m2 <=
+// m2b / w_min, |m1| <= |m1b| + ew sqrt(m2b), |g - b| <= ew sqrt(m2b), ew =
+// 1/w_min - 1, with b the 11x11 box mean (mirrored window) and m1b, m2b the
+// box moments of delta. Hence |s - b| <= E with
+//   E = (kappa A2 A1 + fmax A2) / (1 - kappa A2) + ew sqrt(m2b),
+//   A2 = m2b / w_min, A1 = |m1b| + ew sqrt(m2b)      (E = inf if kappa A2 >= 0.95).
+// The box sums S1 = sum k, S2 = sum k^2 (k the u8 grey) are integers below
+// 2^24, exact in FP32, and so are M1 = S1 - 121 k_p and M2 = S2 - 2 k_p S1 +
+// 121 k_p^2 (m1b = M1 / (121*255), m2b = M2 / (121*255^2)). E is evaluated in
+// FP32 (relative error < 1e-5 including the 1 - kappa A2 >= 0.05 division)
+// and inflated by 1.0001, + 1e-9 for the reference's own double rounding.
+// The exact Sobel of s then satisfies |gx - gx_b| <= Ex = sum |c_k| E(p + k)
+// (gx_b = Sobel(S1) / (121*255), an exact integer Sobel), and a masked pixel
+// is a *survivor* unless (|gx_b| + Ex)^2 + (|gy_b| + Ey)^2 (x 1.00001) < s*_lo:
+// a non-survivor has s_g < s*, so it is provably not an edge. On the KITTI
+// batch ~6 % of the masked pixels survive; only the 3x3 neighbourhoods of the
+// survivors (~9 %) need s~ (the FP32 bilateral below), instead of every tile
+// near the road.
+//
+// CTA = (strip of 128 columns, frame), 160 threads walking down the strip
+// from the horizon in blocks of PS_RB rows. Thread t owns image column
+// x = x0 - 2 + t (t < 132: the strip and the two ring columns the E grid
+// needs on each side). For its column a thread keeps the vertical running
+// sums S1, S2 (exact int) of the horizontal 11-sums H1 = sum k, H2 = sum k^2
+// of each input row (two dp4a chains over the row's 11 window bytes, read as
+// four words and funnel-shifted), the H ring of the last 16 input rows, and a
+// byte shift register of the column's centre values; per E row it writes
+// (S1, E) to shared memory. E columns outside the image evaluate at their
+// mirror column, so the Sobel of a border pixel reads its mirrored neighbours
+// (preprocess.hpp:71-72). Per block: E rows -> barrier -> Sobel test of P
+// rows (x0 - 1 .. x0 + 128; warp ballots, aligned to the strip's words by a
+// funnel shift of 2) -> barrier -> need rows (3x3 dilation, one row behind)
+// appended to the frame's list.
+constexpr int PS_RB = 16;   // rows per block
+constexpr int PS_NT = 160;  // threads (5 warps)
+constexpr int PS_NW = PS_NT / 32;
+
+__device__ __forceinline__ void ps_window(const uint8_t* row, int x, int W, bool fast,
+                                          uint32_t& a0, uint32_t& a1, uint32_t& a2) {
+    // bytes row[x - 5 .. x + 5] (mirrored), packed little-endian into a0, a1, a2 (3 bytes)
+    if (fast) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(row + x - 5);
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+        const unsigned sh = 8u * (unsigned)(a & 3);
+        const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2), w3 = __ldg(w + 3);
+        a0 = __funnelshift_r(w0, w1, sh);
+        a1 = __funnelshift_r(w1, w2, sh);
+        a2 = __funnelshift_r(w2, w3, sh) & 0x00ffffffu;
+    } else {
+        uint32_t b[11];
+#pragma unroll
+        for (int i = 0; i < 11; ++i) b[i] = __ldg(row + mirror(x - 5 + i, W));
+        a0 = b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24;
+        a1 = b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24;
+        a2 = b[8] | b[9] << 8 | b[10] << 16;
+    }
+}
+
+__global__ void __launch_bounds__(PS_NT) k_prescreen(Dev d, PrescreenParam p) {
+    __shared__ float2 sE[PS_RB + 2][PS_NT];     // (S1, E) of E rows R0 - 1 .. R0 + 16
+    __shared__ int2 sH[16][PS_NT];              // (H1, H2) of the last 16 input rows
+    __shared__ uint32_t sP[PS_RB + 2][PS_NW];   // survivor ballots of P rows R0 - 2 .. R0 + 15
+    const int f = blockIdx.y, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int x0 = blockIdx.x * 128, W = d.W, H = d.H;
+    if (blockIdx.x == 0 && t == 0) {  // the Sobel screen appends to these
+        d.need_cnt[f] = 0;
+        d.ctile_cnt[f] = 0;
+    }
+    if (frame_failed(d, f)) return;
+    const int horizon = (int)d.rep[f].horizon;
+    const int P0 = max(horizon, 0);  // first row that can hold road-mask pixels
+    const int wpr = d.words_per_row;
+    // survivor words of the rows a Sobel tile reads but the walk does not reach
+    for (int i = t; i < 4 * (P0 - (P0 & ~(SB_TH - 1))); i += PS_NT) {
+        const int r = (P0 & ~(SB_TH - 1)) + i / 4, w = (x0 >> 5) + i % 4;
+        if (r < H && w < wpr) d.pbits[((size_t)f * H + r) * wpr + w] = 0;
+    }
+    if (P0 >= H) return;
+    const int x = x0 - 2 + t;
+    const bool ecol = t < 132;  // E column (evaluated at its mirror)
+    const int xm = mirror(x, W);
+    const bool fast = xm >= 8 && xm + 8 < W;  // window words stay inside the row
+    const bool bigH = H >= 16;  // one reflection covers every row overhang
+    const uint8_t* g = d.grey + (size_t)f * d.px;
+    const uint8_t* dp = d.disp + (size_t)f * d.px;
+    const bool pcol = t >= 1 && t <= 130 && x >= 0 && x < W;  // a P pixel of the image
+    const bool tcol = t >= 2 && t <= 129;                     // a strip pixel
+    const int e0 = max(P0 - 1, 0);  // first E row
+    int S1 = 0, S2 = 0;
+    uint32_t cl = 0, ch = 0;  // centre bytes of the last 8 input rows (newest in the low byte)
+    auto hrow = [&](int rin, int& h1, int& h2) {
+        const int rr = bigH ? (rin < 0 ? -rin - 1 : rin >= H ? 2 * H - 1 - rin : rin) : mirror(rin, H);
+        uint32_t a0, a1, a2;
+        ps_window(g + (size_t)rr * W, xm, W, fast, a0, a1, a2);
+        h1 = (int)__dp4a(a0, 0x01010101u, __dp4a(a1, 0x01010101u, __dp4a(a2, 0x01010101u, 0u)));
+        h2 = (int)__dp4a(a0, a0, __dp4a(a1, a1, __dp4a(a2, a2, 0u)));
+        ch = __funnelshift_l(cl, ch, 8);
+        cl = cl << 8 | ((a1 >> 8) & 0xffu);  // byte 5 of the window = column xm
+    };
+    auto eval = [&]() {  // E of the running sums with the centre byte of 5 rows ago
+        const int k = (int)((ch >> 8) & 0xffu);
+        const int M1 = S1 - 121 * k;
+        const int M2 = S2 - 2 * k * S1 + 121 * k * k;
+        const float m1 = fabsf((float)M1) * p.c1, m2 = (float)M2 * p.c2;
+        const float A2 = m2 * p.inv_wmin, km = p.kappa * A2;
+        const float sq = fmaf(10.f, m2, 0.025f);  // >= sqrt(m2) (AM-GM at 0.05)
+        const float A1 = fmaf(p.ew, sq, m1);
+        const float e = fmaf(km, A1, p.fmax * A2) * fmaf(2.f, km, 1.f);
+        // 1 / (1 - km) <= 1 + 2 km needs km <= 1/2
+        return km >= 0.5f ? 1e30f : fmaf(fmaf(p.ew, sq, e), 1.0001f, 1e-9f);
+    };
+    if (ecol) {
+        for (int i = -5; i <= 5; ++i) {
+            int h1, h2;
+            hrow(e0 + i, h1, h2);
+            S1 += h1;
+            S2 += h2;
+            sH[(e0 + i) & 15][t] = make_int2(h1, h2);
+        }
+        sE[e0 - (P0 - 1)][t] = make_float2((float)S1, eval());
+    }
+    if (t < 2 * PS_NW) sP[t / PS_NW][t % PS_NW] = 0;
+    int nmask = 0;
+    int e_done = e0;  // last E row computed
+    __syncthreads();
+    for (int R0 = P0; R0 < H; R0 += PS_RB) {
+        // sE[k] holds E row R0 - 1 + k; sP[k] P row R0 - 2 + k
+        if (R0 > P0) {
+            if (ecol) {
+                sE[0][t] = sE[PS_RB][t];
+                sE[1][t] = sE[PS_RB + 1][t];
+            }
+            if (t < 2 * PS_NW) sP[t / PS_NW][t % PS_NW] = sP[PS_RB + t / PS_NW][t % PS_NW];
+        }
+        const int e_end = min(R0 + PS_RB, H - 1);  // E rows up to R0 + 16
+        if (ecol)
+#pragma unroll 4
+            for (int e = e_done + 1; e <= e_end; ++e) {
+                int h1, h2;
+                hrow(e + 5, h1, h2);
+                const int2 o = sH[(e - 6) & 15][t];
+                S1 += h1 - o.x;
+                S2 += h2 - o.y;
+                sH[(e + 5) & 15][t] = make_int2(h1, h2);
+                sE[e - (R0 - 1)][t] = make_float2((float)S1, eval());
+            }
+        e_done = e_end;
+        __syncthreads();
+        // Sobel test of P rows R0 .. R0 + 15 (E rows mirrored at the top / bottom)
+        {
+            const int kmax = min(PS_RB, H - R0);
+            int2 mr = make_int2(256, 0);
+            int dv = 0;
+            if (pcol) {
+                mr = d.mrange[(size_t)f * H + R0];
+                dv = dp[(size_t)R0 * W + x];
+            }
+            float2 a0, a1, a2, b0, b1, b2;
+            {
+                const int ka = R0 == 0 ? 1 : 0;  // E row mirror(R0 - 1)
+                a0 = sE[ka][t - 1 >= 0 ? t - 1 : 0];
+                a1 = sE[ka][t];
+                a2 = sE[ka][t + 1 < PS_NT ? t + 1 : t];
+                b0 = sE[1][t - 1 >= 0 ? t - 1 : 0];
+                b1 = sE[1][t];
+                b2 = sE[1][t + 1 < PS_NT ? t + 1 : t];
+            }
+            for (int k = 0; k < PS_RB; ++k) {
+                const int r = R0 + k;
+                bool ps = false;
+                int2 mrn = make_int2(256, 0);
+                int dvn = 0;
+                if (pcol && k + 1 < kmax) {  // next row's mask inputs in flight
+                    mrn = d.mrange[(size_t)f * H + r + 1];
+                    dvn = dp[(size_t)(r + 1) * W + x];
+                }
+                const int kc = r + 1 >= H ? k + 1 : k + 2;  // E row mirror(r + 1)
+                const float2 c0 = sE[kc][t - 1 >= 0 ? t - 1 : 0], c1 = sE[kc][t],
+                             c2 = sE[kc][t + 1 < PS_NT ? t + 1 : t];
+                if (k < kmax && pcol && dv >= mr.x && dv <= mr.y) {
+                    nmask += tcol;
+                    const float gx = ((a2.x - a0.x) + 2.f * (b2.x - b0.x)) + (c2.x - c0.x);
+                    const float gy = ((c0.x - a0.x) + 2.f * (c1.x - a1.x)) + (c2.x - a2.x);
+                    const float ex = ((a2.y + a0.y) + 2.f * (b2.y + b0.y)) + (c2.y + c0.y);
+                    const float ey = ((c0.y + a0.y) + 2.f * (c1.y + a1.y)) + (c2.y + a2.y);
+                    const float tx = fmaf(fabsf(gx), p.c1, ex), ty = fmaf(fabsf(gy), p.c1, ey);
+                    ps = fmaf(tx, tx, ty * ty) * 1.00001f >= p.s_star_lo;
+                }
+                const uint32_t bb = __ballot_sync(0xffffffffu, ps);
+                if (lane == 0) sP[k + 2][warp] = bb;
+                a0 = b0; a1 = b1; a2 = b2;
+                b0 = c0; b1 = c1; b2 = c2;
+                mr = mrn;
+                dv = dvn;
+            }
+        }
+        __syncthreads();
+        // need rows R0 - 1 .. R0 + 14 (row R0 + 15 waits for the next block's
+        // first survivors); task (row k, strip word i), 4 + 64 tasks in the last block
+        const bool last = R0 + PS_RB >= H;
+        if (t < 64 + (last ? 4 : 0)) {
+            const int k = t < 64 ? t >> 2 : 16, i = t & 3;
+            const int r = R0 - 1 + k;  // need(r) = survivors of P rows r - 1 .. r + 1 (sP k .. k + 2)
+            uint32_t nw = 0;
+            if (r >= 0 && r < H) {
+                auto orw = [&](int w) -> uint32_t {  // ballot word w of rows k .. k + 2
+                    if (w < 0 || w >= PS_NW) return 0u;
+                    return sP[k][w] | sP[k + 1][w] | (k + 2 <= PS_RB + 1 ? sP[k + 2][w] : 0u);
+                };
+                auto dil = [&](int w) {  // horizontal 3-dilation in thread (t) space
+                    const uint32_t X = orw(w);
+                    return X | (X << 1 | orw(w - 1) >> 31) | (X >> 1 | orw(w + 1) << 31);
+                };
+                nw = __funnelshift_r(dil(i), dil(i + 1), 2);  // strip columns 32 i .. 32 i + 31
+                uint32_t pw = __funnelshift_r(sP[k + 1][i], i + 1 < PS_NW ? sP[k + 1][i + 1] : 0u, 2);
+                const int ub = x0 + 32 * i;
+                const uint32_t valid = ub >= W ? 0u : W - ub >= 32 ? 0xffffffffu : (1u << (W - ub)) - 1u;
+                nw &= valid;
+                pw &= valid;
+                if ((ub >> 5) < wpr && r >= P0) d.pbits[((size_t)f * H + r) * wpr + (ub >> 5)] = pw;
+            }
+            const unsigned am = t < 64 ? 0xffffffffu : 0xfu;  // warp 2: the 4 tasks of row R0 + 15
+            const int cnt = __popc(nw);
+            int pre = cnt;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int q = __shfl_up_sync(am, pre, o);
+                if (lane >= o) pre += q;
+            }
+            const int tot = __shfl_sync(am, pre, 31 - __clz(am));
+            unsigned base = 0;
+            if (lane == 0 && tot) base = atomicAdd(&d.aux[f].fneed, (unsigned)tot);
+            base = __shfl_sync(am, base, 0) + (unsigned)(pre - cnt);
+            uint32_t* out = d.fneed + (size_t)f * d.px;
+            const int ub = x0 + 32 * i;
+            while (nw) {
+                const int bb = __ffs(nw) - 1;
+                nw &= nw - 1;
+                out[base++] = ((uint32_t)r << 16) | (uint32_t)(ub + bb);
+            }
+        }
+        __syncthreads();
+    }
+    for (int o = 16; o; o >>= 1) nmask += __shfl_xor_sync(0xffffffffu, nmask, o);
+    if (lane == 0 && nmask) atomicAdd(&d.aux[f].mask_px, (unsigned long long)nmask);
+}
+
+// FP32 bilateral of the need pixels (k_prescreen's list), one thread per
+// pixel, the frames' lists flattened over a persistent grid. Each tap
+// reads (R(delta), R(delta) * delta) from a shared table (delta = k_q - k_p,
+// 16 lane copies entry-major: a half-warp's 8-byte loads hit 32 distinct
+// banks) and adds S_t * R to den and S_t * R * delta to num (two FMAs, S_t
+// an immediate constant-bank operand); s~ = (k_p + num / den) / 255. The sums
+// of a pixel run in j-major / i-minor order. Error: the weights are exact to
+// 3 ulp, each FMA chain of 121 terms adds <= 121 ulp of sum |S R delta| <=
+// 255 den (num) or of den, so |num/den - q| <= ~246 * 255 * 2^-24 and
+// |s~ - s| <= ~248 * 2^-24 < 1.5e-5 < kEpsSmooth.
+// all = 1: every pixel of every frame (lk_fast_path_error).
+__global__ void __launch_bounds__(256) k_bilateral_need(Dev d, NeedBfParam p, int n, int all) {
+    extern __shared__ float2 s_T[];  // [511][16]
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int i = tid; i < 511 * 16; i += 256) s_T[i] = d.need_tab[i >> 4];
+    __syncthreads();
+    const unsigned T = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + tid;
+    const unsigned tb = (unsigned)__cvta_generic_to_shared(s_T) + 8u * (lane & 15);
+    const int W = d.W, H = d.H;
+    unsigned base = 0;  // first flattened index of frame f
+    for (int f = 0; f < n; ++f) {
+        const unsigned cnt = all ? (frame_failed(d, f) ? 0u : (unsigned)d.px)
+                                 : (frame_failed(d, f) ? 0u : d.aux[f].fneed);
+        const uint8_t* g = d.grey + (size_t)f * d.px;
+        const uint32_t* list = d.fneed + (size_t)f * d.px;
+        for (unsigned i = (t + T - base % T) % T; i < cnt; i += T) {
+            int u, v;
+            if (all) {
+                v = (int)(i / (unsigned)W);
+                u = (int)i - v * W;
+            } else {
+                const uint32_t e = list[i];
+                v = (int)(e >> 16);
+                u = (int)(e & 0xffffu);
+            }
+            const int kp = g[(size_t)v * W + u];
+            const unsigned C = tb + 128u * (unsigned)(255 - kp);
+            const bool inner = u >= 5 && v >= 5 && u + 5 < W && v + 5 < H;
+            int col[11];
+#pragma unroll
+            for (int k = 0; k < 11; ++k) col[k] = inner ? u - 5 + k : mirror(u - 5 + k, W);
+            float num = 0.f, den = 0.f;
+            uint8_t kc[11];
+            refine_row<5>(g, (size_t)(inner ? v - 5 : mirror(v - 5, H)) * W, col, inner, u, kc);
+#pragma unroll
+            for (int j = 0; j < 11; ++j) {
+                uint8_t kn[11];
+                if (j < 10)
+                    refine_row<5>(g, (size_t)(inner ? v - 4 + j : mirror(v - 4 + j, H)) * W, col,
+                                  inner, u, kn);
+#pragma unroll
+                for (int k = 0; k < 11; ++k) {
+                    float2 rt;
+                    asm("ld.shared.v2.f32 {%0, %1}, [%2];"
+                        : "=f"(rt.x), "=f"(rt.y)
+                        : "r"(C + 128u * kc[k]));
+                    den = fmaf(p.S[j * 11 + k], rt.x, den);
+                    num = fmaf(p.S[j * 11 + k], rt.y, num);
+                }
+                if (j < 10)
+#pragma unroll
+                    for (int k = 0; k < 11; ++k) kc[k] = kn[k];
+            }
+            d.smoothed_f[(size_t)f * d.px + (size_t)v * W + u] =
+                ((float)kp + __fdiv_rn(num, den)) * (1.f / 255.f);
+        }
+        base += cnt;
+    }
+}
+
 // Exact Sobel (preprocess.hpp:76-81) of the candidates of each candidate
 // tile, on the exact smoothed values k_refine_exact wrote for their 3x3
 // neighbourhoods: edge bits replace the candidate bits, then the segment and
@@ -710,8 +1036,11 @@ __global__ void __launch_bounds__(128) k_sobel_decide(Dev d) {
     }
 }
 
+constexpr size_t kNeedTabSmem = 511 * 16 * sizeof(float2);
+
 cudaError_t configure_fastpath() {
-    cudaError_t e = cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_bilateral_need, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kNeedTabSmem);
     for (auto fn : {k_bilateral_fast<5, 0>, k_bilateral_fast<5, 10>, k_bilateral_fast<5, 21>,
                     k_bilateral_fast<5, 27>, k_bilateral_fast<5, 31>, k_bilateral_fast<5, 63>})
         if (e == cudaSuccess)
@@ -719,20 +1048,20 @@ cudaError_t configure_fastpath() {
     return e;
 }
 
+int need_bilateral_ctas(int sm_count) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_need, 256, kNeedTabSmem) !=
+            cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return sm_count * per_sm;
+}
+
+// Stage 9 of the throughput path: the certified pre-screen, then the FP32
+// bilateral of its need pixels (all = 1: every pixel, for lk_fast_path_error).
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all) {
-    const dim3 g((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n);
-    const int tpc = std::min(32, std::max(1, lp.fast_tpc));
-    const int pg = (int)((g.x * g.y * g.z + tpc - 1) / tpc);
     if (!all)
-        k_bf_flags<<<dim3((d.H + BT_H - 1) / BT_H, n), 256, 0, s>>>(d);
-    constexpr size_t kTableSmem = 511 * 32 * 4;
-    switch (lp.fast_table) {
-#define LK_BF(M) \
-    case M: k_bilateral_fast<5, M><<<pg, 256, kTableSmem, s>>>(d, lp.fbf, n, tpc, all); break;
-        LK_BF(0) LK_BF(10) LK_BF(21) LK_BF(27) LK_BF(31) LK_BF(63)
-#undef LK_BF
-        default: k_bilateral_fast<5, 63><<<pg, 256, kTableSmem, s>>>(d, lp.fbf, n, tpc, all); break;
-    }
+        k_prescreen<<<dim3((d.W + 127) / 128, n), PS_NT, 0, s>>>(d, lp.ps);
+    k_bilateral_need<<<lp.need_ctas, 256, kNeedTabSmem, s>>>(d, lp.nbf, n, all);
 }
 
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s) {

@@ -38,9 +38,31 @@ struct FastBfParam {
     float c2;      // -inv_r2 * log2(e)
 };
 
+// Certified pre-screen (k_prescreen): constants of the bound |s - b| <= E on
+// the gap between the bilateral s and the 11x11 box mean b,
+// each rounded so the bound stays an upper bound.
+struct PrescreenParam {
+    float kappa;     // inv_r2 = 1 / sigma_r^2 (range exponent per unit dr^2), rounded up
+    float inv_wmin;  // 1 / (smallest spatial weight of the window), rounded up
+    float ew;        // inv_wmin - 1, rounded up
+    float fmax;      // sup over 0 < x <= 1 of (1 - exp(-kappa x^2)) / x, rounded up
+    float c1;        // 1 / (121 * 255), rounded up
+    float c2;        // 1 / (121 * 255^2), rounded up
+    float s_star_lo; // largest float <= the exact Sobel threshold s*
+};
+
+// Need-list bilateral (k_bilateral_need): the spatial factor of every tap
+// (j-major) as float; the range factors come from a shared (R, R*delta) table.
+struct NeedBfParam {
+    float S[121];
+};
+
 struct LaunchPlan {
     WsParam ws;
     FastBfParam fbf;
+    PrescreenParam ps;
+    NeedBfParam nbf;
+    int need_ctas;            // persistent k_bilateral_need CTAs
     int fast_front;           // certified fast bilateral + exact refinement (lk_fastpath.cu)
     int fast_table;           // mask of tap pairs whose range factor comes from the smem table
     int fast_tpc;             // fast-bilateral tiles per CTA (LK_BF_TPC)
@@ -77,6 +99,7 @@ cudaError_t configure_kernels(const LaunchPlan& lp);
 int vdisparity_rows(int W, int D1);
 size_t vdisparity_smem(int W, int D1);
 cudaError_t configure_fastpath();
+int need_bilateral_ctas(int sm_count);
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all = 0);
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
 void launch_exact_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);

@@ -9,9 +9,10 @@ def main(path):
     hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     hdr = rows[hdr_i]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
     agg = collections.defaultdict(list)
     for r in rows[hdr_i + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
             continue
         name = r[ki].split("(")[0].replace("void lkg::", "").replace("lkg::", "")
         v = float(r[vi].replace(",", ""))
