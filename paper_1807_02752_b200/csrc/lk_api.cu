@@ -460,7 +460,9 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     // budget holds (exponent of the smallest weight <= 20; default 11.1).
     {
         const double xmax = 50.0 * inv_s2 + inv_r2;
-        lp.fast_front = win == 11 && !d.hooks && !(flags & LK_FLAG_EXACT) && xmax <= 20.0;
+        lp.fast_front = win == 11 && !d.hooks && !(flags & LK_FLAG_EXACT) && xmax <= 20.0 &&
+                        lkg::prescreen_threads(W) <= 768 &&
+                        lkg::prescreen_smem(W, lkg::prescreen_threads(W)) <= 200 * 1024;
         const double log2e = 1.4426950408889634;
         for (int dj = -5; dj <= 5; ++dj)
             for (int di = -5; di <= 5; ++di)
@@ -520,6 +522,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         lp.ps.c1 = up(1.0 / (121.0 * 255.0));
         lp.ps.c2 = up(1.0 / (121.0 * 255.0 * 255.0));
         lp.ps.s_star_lo = d.sobel_s_star_lo;
+        lp.fast_width = W;
         for (int j = 0; j < 11; ++j)
             for (int i = 0; i < 11; ++i)
                 lp.nbf.S[j * 11 + i] = (float)(win == 11 ? ws[(size_t)j * 11 + i] : 0.0);

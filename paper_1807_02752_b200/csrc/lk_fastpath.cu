@@ -679,90 +679,127 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, WsParam ws) {
 // survivors (~9 %) need s~ (the FP32 bilateral below), instead of every tile
 // near the road.
 //
-// CTA = (strip of 128 columns, frame), 160 threads walking down the strip
-// from the horizon in blocks of PS_RB rows. Thread t owns image column
-// x = x0 - 2 + t (t < 132: the strip and the two ring columns the E grid
-// needs on each side). For its column a thread keeps the vertical running
-// sums S1, S2 (exact int) of the horizontal 11-sums H1 = sum k, H2 = sum k^2
-// of each input row (two dp4a chains over the row's 11 window bytes, read as
-// four words and funnel-shifted), the H ring of the last 16 input rows, and a
-// byte shift register of the column's centre values; per E row it writes
-// (S1, E) to shared memory. E columns outside the image evaluate at their
-// mirror column, so the Sobel of a border pixel reads its mirrored neighbours
-// (preprocess.hpp:71-72). Per block: E rows -> barrier -> Sobel test of P
-// rows (x0 - 1 .. x0 + 128; warp ballots, aligned to the strip's words by a
-// funnel shift of 2) -> barrier -> need rows (3x3 dilation, one row behind)
-// appended to the frame's list.
-constexpr int PS_RB = 16;   // rows per block
-constexpr int PS_NT = 160;  // threads (5 warps)
-constexpr int PS_NW = PS_NT / 32;
+// CTA = one frame, walking down its rows from the horizon. Lane l of warp w
+// owns the quad q = 30 w - 1 + l (image columns 4q .. 4q + 3, evaluated at
+// their mirror columns outside the image); lanes 1-30 are the warp's output
+// quads, lanes 0 and 31 the neighbours its Sobels read, so warps never wait
+// for each other inside a row. Per input row a lane loads the 14 window bytes
+// of its quad as five words, forms H1 = sum k and H2 = sum k^2 of the first
+// column's 11 bytes with dp4a and slides them across the quad; the vertical
+// running sums S1, S2 (exact int) subtract the row that left the window (a
+// shared ring of packed H1 | H2 << 12 of the last 16 input rows). E rows are
+// kept in registers (rows r - 1, r, r + 1), the neighbour columns come by
+// shuffle, and the Sobel test of P row r runs as soon as E row r + 1 exists.
+// Survivor nibbles go to a shared row bitmap (one match/reduce OR per word
+// group); every PQ_RB rows the need rows (3x3 dilation, one row behind) are
+// appended to the frame's list and the survivor words written to pbits.
+constexpr int PQ_RB = 16;  // rows per need block
+constexpr int PQ_RING = 11;  // H ring: the 11 input rows of the current window
+constexpr int PQ_SR = 20;  // survivor bitmap ring rows (>= PQ_RB + 3)
+constexpr uint32_t kOnes = 0x01010101u;
 
-__device__ __forceinline__ void ps_window(const uint8_t* row, int x, int W, bool fast,
-                                          uint32_t& a0, uint32_t& a1, uint32_t& a2) {
-    // bytes row[x - 5 .. x + 5] (mirrored), packed little-endian into a0, a1, a2 (3 bytes)
+__device__ __forceinline__ uint32_t pq_byte(uint32_t w, int i) { return (w >> (8 * i)) & 0xffu; }
+
+// the 14 window bytes 4q - 5 .. 4q + 8 of a (mirrored) row as t0..t3 (bytes 0-13)
+__device__ __forceinline__ void pq_bytes(const uint8_t* row, int q, int W, bool fast, uint32_t& t0,
+                                         uint32_t& t1, uint32_t& t2, uint32_t& t3) {
     if (fast) {
-        const uintptr_t a = reinterpret_cast<uintptr_t>(row + x - 5);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(row + 4 * q - 5);
         const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
         const unsigned sh = 8u * (unsigned)(a & 3);
-        const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2), w3 = __ldg(w + 3);
-        a0 = __funnelshift_r(w0, w1, sh);
-        a1 = __funnelshift_r(w1, w2, sh);
-        a2 = __funnelshift_r(w2, w3, sh) & 0x00ffffffu;
+        const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2), w3 = __ldg(w + 3),
+                       w4 = __ldg(w + 4);
+        t0 = __funnelshift_r(w0, w1, sh);
+        t1 = __funnelshift_r(w1, w2, sh);
+        t2 = __funnelshift_r(w2, w3, sh);
+        t3 = __funnelshift_r(w3, w4, sh);
     } else {
-        uint32_t b[11];
+        uint32_t b[14];
 #pragma unroll
-        for (int i = 0; i < 11; ++i) b[i] = __ldg(row + mirror(x - 5 + i, W));
-        a0 = b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24;
-        a1 = b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24;
-        a2 = b[8] | b[9] << 8 | b[10] << 16;
+        for (int i = 0; i < 14; ++i) b[i] = __ldg(row + mirror(4 * q - 5 + i, W));
+        t0 = b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24;
+        t1 = b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24;
+        t2 = b[8] | b[9] << 8 | b[10] << 16 | b[11] << 24;
+        t3 = b[12] | b[13] << 8;
     }
 }
 
-__global__ void __launch_bounds__(PS_NT) k_prescreen(Dev d, PrescreenParam p) {
-    __shared__ float2 sE[PS_RB + 2][PS_NT];     // (S1, E) of E rows R0 - 1 .. R0 + 16
-    __shared__ int2 sH[16][PS_NT];              // (H1, H2) of the last 16 input rows
-    __shared__ uint32_t sP[PS_RB + 2][PS_NW];   // survivor ballots of P rows R0 - 2 .. R0 + 15
-    const int f = blockIdx.y, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int x0 = blockIdx.x * 128, W = d.W, H = d.H;
-    if (blockIdx.x == 0 && t == 0) {  // the Sobel screen appends to these
+__global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
+    extern __shared__ __align__(16) uint32_t pq_sm[];
+    const int f = blockIdx.x, seg = blockIdx.y, nseg = gridDim.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nt = blockDim.x, W = d.W, H = d.H, wpr = d.words_per_row;
+    uint4* ring = reinterpret_cast<uint4*>(pq_sm);                 // [PQ_RING][nt]
+    uint32_t* sbits = pq_sm + PQ_RING * 4 * nt;                     // [PQ_SR][wpr + 1]
+    const int sbw = wpr + 1;
+    if (tid == 0 && seg == 0) {  // the Sobel screen appends to these
         d.need_cnt[f] = 0;
         d.ctile_cnt[f] = 0;
     }
     if (frame_failed(d, f)) return;
     const int horizon = (int)d.rep[f].horizon;
-    const int P0 = max(horizon, 0);  // first row that can hold road-mask pixels
-    const int wpr = d.words_per_row;
+    const int P0 = max(horizon, 0);
     // survivor words of the rows a Sobel tile reads but the walk does not reach
-    for (int i = t; i < 4 * (P0 - (P0 & ~(SB_TH - 1))); i += PS_NT) {
-        const int r = (P0 & ~(SB_TH - 1)) + i / 4, w = (x0 >> 5) + i % 4;
-        if (r < H && w < wpr) d.pbits[((size_t)f * H + r) * wpr + w] = 0;
-    }
+    if (seg == 0)
+        for (int i = tid; i < wpr * (P0 - (P0 & ~(SB_TH - 1))); i += nt) {
+            const int r = (P0 & ~(SB_TH - 1)) + i / wpr;
+            if (r < H) d.pbits[((size_t)f * H + r) * wpr + i % wpr] = 0;
+        }
     if (P0 >= H) return;
-    const int x = x0 - 2 + t;
-    const bool ecol = t < 132;  // E column (evaluated at its mirror)
-    const int xm = mirror(x, W);
-    const bool fast = xm >= 8 && xm + 8 < W;  // window words stay inside the row
-    const bool bigH = H >= 16;  // one reflection covers every row overhang
+    // this segment's rows [pa, pb) of P0 .. H - 1: it emits their need rows
+    // (segment 0 also row P0 - 1) and survivor words, and tests P rows
+    // [t_lo, t_hi] (one more on each side for the dilation)
+    const int L = (H - P0 + nseg - 1) / nseg;
+    const int pa = P0 + seg * L, pb = min(pa + L, H);
+    if (pa >= pb) return;
+    const int t_lo = max(pa - 1, P0), t_hi = min(pb, H - 1);
+    const int n_lo = seg == 0 ? max(P0 - 1, 0) : pa;
+    for (int i = tid; i < PQ_SR * sbw; i += nt) sbits[i] = 0;
+    const int q = 30 * warp - 1 + lane;
+    const int qlast = (W - 1) >> 2;
+    const bool outq = lane >= 1 && lane <= 30 && q <= qlast;  // an output quad
+    const bool fast = 4 * q - 5 >= 0 && 4 * q + 11 < W;       // window words inside the row
+    const bool bigH = H >= 16;
     const uint8_t* g = d.grey + (size_t)f * d.px;
     const uint8_t* dp = d.disp + (size_t)f * d.px;
-    const bool pcol = t >= 1 && t <= 130 && x >= 0 && x < W;  // a P pixel of the image
-    const bool tcol = t >= 2 && t <= 129;                     // a strip pixel
-    const int e0 = max(P0 - 1, 0);  // first E row
-    int S1 = 0, S2 = 0;
-    uint32_t cl = 0, ch = 0;  // centre bytes of the last 8 input rows (newest in the low byte)
-    auto hrow = [&](int rin, int& h1, int& h2) {
+    int S1[4] = {0, 0, 0, 0}, S2[4] = {0, 0, 0, 0};  // box sums of k, k^2 (exact) per column
+    uint32_t cen[6] = {0, 0, 0, 0, 0, 0};  // centre bytes (columns 4q..4q+3) of input rows, newest first
+    // H1, H2 of the quad's 4 columns for input row rin (mirrored), packed H1 | H2 << 12
+    auto hrow = [&](int rin, uint4& hp) {
         const int rr = bigH ? (rin < 0 ? -rin - 1 : rin >= H ? 2 * H - 1 - rin : rin) : mirror(rin, H);
-        uint32_t a0, a1, a2;
-        ps_window(g + (size_t)rr * W, xm, W, fast, a0, a1, a2);
-        h1 = (int)__dp4a(a0, 0x01010101u, __dp4a(a1, 0x01010101u, __dp4a(a2, 0x01010101u, 0u)));
-        h2 = (int)__dp4a(a0, a0, __dp4a(a1, a1, __dp4a(a2, a2, 0u)));
-        ch = __funnelshift_l(cl, ch, 8);
-        cl = cl << 8 | ((a1 >> 8) & 0xffu);  // byte 5 of the window = column xm
+        uint32_t t0, t1, t2, t3;
+        pq_bytes(g + (size_t)rr * W, q, W, fast, t0, t1, t2, t3);
+        const uint32_t t2m = t2 & 0x00ffffffu;
+        int h1 = (int)__dp4a(t0, kOnes, __dp4a(t1, kOnes, __dp4a(t2m, kOnes, 0u)));
+        int h2 = (int)__dp4a(t0, t0, __dp4a(t1, t1, __dp4a(t2m, t2m, 0u)));
+        const int o0 = pq_byte(t0, 0), o1 = pq_byte(t0, 1), o2 = pq_byte(t0, 2);
+        const int n0 = pq_byte(t2, 3), n1 = pq_byte(t3, 0), n2 = pq_byte(t3, 1);
+        hp.x = (uint32_t)h1 | (uint32_t)h2 << 12;
+        h1 += n0 - o0;
+        h2 += n0 * n0 - o0 * o0;
+        hp.y = (uint32_t)h1 | (uint32_t)h2 << 12;
+        h1 += n1 - o1;
+        h2 += n1 * n1 - o1 * o1;
+        hp.z = (uint32_t)h1 | (uint32_t)h2 << 12;
+        h1 += n2 - o2;
+        h2 += n2 * n2 - o2 * o2;
+        hp.w = (uint32_t)h1 | (uint32_t)h2 << 12;
+#pragma unroll
+        for (int i = 5; i > 0; --i) cen[i] = cen[i - 1];
+        cen[0] = __funnelshift_r(t1, t2, 8);  // bytes 5 .. 8 = columns 4q .. 4q + 3
     };
-    auto eval = [&]() {  // E of the running sums with the centre byte of 5 rows ago
-        const int k = (int)((ch >> 8) & 0xffu);
-        const int M1 = S1 - 121 * k;
-        const int M2 = S2 - 2 * k * S1 + 121 * k * k;
+    auto addrow = [&](const uint4& hp, int sg) {
+        const uint32_t h[4] = {hp.x, hp.y, hp.z, hp.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            S1[j] += sg * (int)(h[j] & 0xfffu);
+            S2[j] += sg * (int)(h[j] >> 12);
+        }
+    };
+    auto evalE = [&](int j) {  // E of column j with the centre byte of 5 rows ago
+        const int k = (int)pq_byte(cen[5], j);
+        const int M1 = S1[j] - 121 * k;
+        const int M2 = S2[j] - 2 * k * S1[j] + 121 * k * k;
         const float m1 = fabsf((float)M1) * p.c1, m2 = (float)M2 * p.c2;
         const float A2 = m2 * p.inv_wmin, km = p.kappa * A2;
         const float sq = fmaf(10.f, m2, 0.025f);  // >= sqrt(m2) (AM-GM at 0.05)
@@ -771,139 +808,165 @@ __global__ void __launch_bounds__(PS_NT) k_prescreen(Dev d, PrescreenParam p) {
         // 1 / (1 - km) <= 1 + 2 km needs km <= 1/2
         return km >= 0.5f ? 1e30f : fmaf(fmaf(p.ew, sq, e), 1.0001f, 1e-9f);
     };
-    if (ecol) {
-        for (int i = -5; i <= 5; ++i) {
-            int h1, h2;
-            hrow(e0 + i, h1, h2);
-            S1 += h1;
-            S2 += h2;
-            sH[(e0 + i) & 15][t] = make_int2(h1, h2);
-        }
-        sE[e0 - (P0 - 1)][t] = make_float2((float)S1, eval());
+    const int e0 = max(t_lo - 1, 0);  // first E row
+    for (int i = -5; i <= 5; ++i) {
+        uint4 hp;
+        hrow(e0 + i, hp);
+        addrow(hp, 1);
+        ring[(i + 5) * nt + tid] = hp;  // slot k <-> input row e0 - 5 + k (mod PQ_RING)
     }
-    if (t < 2 * PS_NW) sP[t / PS_NW][t % PS_NW] = 0;
+    // E rows of the quad, (S1, E) per column, plus the left neighbour's column 3
+    // (l) and the right neighbour's column 0 (r); three rotate without copies
+    struct RowE {
+        float2 v[4], l, r;
+    };
+    auto make_row = [&](RowE& C) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) C.v[j] = make_float2((float)S1[j], evalE(j));
+        C.l = make_float2(__shfl_up_sync(0xffffffffu, C.v[3].x, 1), __shfl_up_sync(0xffffffffu, C.v[3].y, 1));
+        C.r = make_float2(__shfl_down_sync(0xffffffffu, C.v[0].x, 1), __shfl_down_sync(0xffffffffu, C.v[0].y, 1));
+    };
     int nmask = 0;
-    int e_done = e0;  // last E row computed
-    __syncthreads();
-    for (int R0 = P0; R0 < H; R0 += PS_RB) {
-        // sE[k] holds E row R0 - 1 + k; sP[k] P row R0 - 2 + k
-        if (R0 > P0) {
-            if (ecol) {
-                sE[0][t] = sE[PS_RB][t];
-                sE[1][t] = sE[PS_RB + 1][t];
-            }
-            if (t < 2 * PS_NW) sP[t / PS_NW][t % PS_NW] = sP[PS_RB + t / PS_NW][t % PS_NW];
-        }
-        const int e_end = min(R0 + PS_RB, H - 1);  // E rows up to R0 + 16
-        if (ecol)
-#pragma unroll 4
-            for (int e = e_done + 1; e <= e_end; ++e) {
-                int h1, h2;
-                hrow(e + 5, h1, h2);
-                const int2 o = sH[(e - 6) & 15][t];
-                S1 += h1 - o.x;
-                S2 += h2 - o.y;
-                sH[(e + 5) & 15][t] = make_int2(h1, h2);
-                sE[e - (R0 - 1)][t] = make_float2((float)S1, eval());
-            }
-        e_done = e_end;
-        __syncthreads();
-        // Sobel test of P rows R0 .. R0 + 15 (E rows mirrored at the top / bottom)
-        {
-            const int kmax = min(PS_RB, H - R0);
-            int2 mr = make_int2(256, 0);
-            int dv = 0;
-            if (pcol) {
-                mr = d.mrange[(size_t)f * H + R0];
-                dv = dp[(size_t)R0 * W + x];
-            }
-            float2 a0, a1, a2, b0, b1, b2;
-            {
-                const int ka = R0 == 0 ? 1 : 0;  // E row mirror(R0 - 1)
-                a0 = sE[ka][t - 1 >= 0 ? t - 1 : 0];
-                a1 = sE[ka][t];
-                a2 = sE[ka][t + 1 < PS_NT ? t + 1 : t];
-                b0 = sE[1][t - 1 >= 0 ? t - 1 : 0];
-                b1 = sE[1][t];
-                b2 = sE[1][t + 1 < PS_NT ? t + 1 : t];
-            }
-            for (int k = 0; k < PS_RB; ++k) {
-                const int r = R0 + k;
-                bool ps = false;
-                int2 mrn = make_int2(256, 0);
-                int dvn = 0;
-                if (pcol && k + 1 < kmax) {  // next row's mask inputs in flight
-                    mrn = d.mrange[(size_t)f * H + r + 1];
-                    dvn = dp[(size_t)(r + 1) * W + x];
-                }
-                const int kc = r + 1 >= H ? k + 1 : k + 2;  // E row mirror(r + 1)
-                const float2 c0 = sE[kc][t - 1 >= 0 ? t - 1 : 0], c1 = sE[kc][t],
-                             c2 = sE[kc][t + 1 < PS_NT ? t + 1 : t];
-                if (k < kmax && pcol && dv >= mr.x && dv <= mr.y) {
-                    nmask += tcol;
-                    const float gx = ((a2.x - a0.x) + 2.f * (b2.x - b0.x)) + (c2.x - c0.x);
-                    const float gy = ((c0.x - a0.x) + 2.f * (c1.x - a1.x)) + (c2.x - a2.x);
-                    const float ex = ((a2.y + a0.y) + 2.f * (b2.y + b0.y)) + (c2.y + c0.y);
-                    const float ey = ((c0.y + a0.y) + 2.f * (c1.y + a1.y)) + (c2.y + a2.y);
-                    const float tx = fmaf(fabsf(gx), p.c1, ex), ty = fmaf(fabsf(gy), p.c1, ey);
-                    ps = fmaf(tx, tx, ty * ty) * 1.00001f >= p.s_star_lo;
-                }
-                const uint32_t bb = __ballot_sync(0xffffffffu, ps);
-                if (lane == 0) sP[k + 2][warp] = bb;
-                a0 = b0; a1 = b1; a2 = b2;
-                b0 = c0; b1 = c1; b2 = c2;
-                mr = mrn;
-                dv = dvn;
+    // P row r from E rows A = E(r - 1), B = E(r), C = E(r + 1): exact integer
+    // Sobel of S1 and |c|-weighted Sobel of E as packed (S1, E) pairs
+    const float2 np = make_float2(-1.f, 1.f), two = make_float2(2.f, 2.f);
+    auto test_row = [&](int r, const RowE& A, const RowE& B, const RowE& C) {
+        // mask inputs of the quad: disparity bytes 4q .. 4q + 3 and the row interval
+        uint32_t dw = 0;
+        int2 mr = make_int2(256, 0);
+        if (outq) {
+            mr = d.mrange[(size_t)f * H + r];
+            const uint8_t* dr = dp + (size_t)r * W + 4 * q;
+            if (4 * q + 4 <= W) {
+                const uintptr_t a = reinterpret_cast<uintptr_t>(dr);
+                const uint32_t* wp = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+                dw = __funnelshift_r(__ldg(wp), __ldg(wp + 1), 8u * (unsigned)(a & 3));
+            } else {
+                for (int j = 0; j < 4 && 4 * q + j < W; ++j) dw |= (uint32_t)dr[j] << (8 * j);
             }
         }
+        uint32_t nib = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int dv = (int)pq_byte(dw, j);
+            if (outq && 4 * q + j < W && dv >= mr.x && dv <= mr.y) {
+                nmask += r >= pa && r < pb;
+                const float2 a0 = j ? A.v[j - 1] : A.l, a1 = A.v[j], a2 = j < 3 ? A.v[j + 1] : A.r;
+                const float2 b0 = j ? B.v[j - 1] : B.l, b2 = j < 3 ? B.v[j + 1] : B.r;
+                const float2 c0 = j ? C.v[j - 1] : C.l, c1 = C.v[j], c2 = j < 3 ? C.v[j + 1] : C.r;
+                // (gx, ex): x = right - left, y = right + left; rows weighted 1, 2, 1
+                const float2 hx = __fadd2_rn(__ffma2_rn(__ffma2_rn(b0, np, b2), two, __ffma2_rn(a0, np, a2)),
+                                             __ffma2_rn(c0, np, c2));
+                // (gy, ey): x = bottom - top, y = bottom + top; columns weighted 1, 2, 1
+                const float2 hy = __fadd2_rn(__ffma2_rn(__ffma2_rn(a1, np, c1), two, __ffma2_rn(a0, np, c0)),
+                                             __ffma2_rn(a2, np, c2));
+                const float tx = fmaf(fabsf(hx.x), p.c1, hx.y), ty = fmaf(fabsf(hy.x), p.c1, hy.y);
+                if (fmaf(tx, tx, ty * ty) * 1.00001f >= p.s_star_lo) nib |= 1u << j;
+            }
+        }
+        // OR the nibbles of each 32-column word into the shared row bitmap
+        const int wd = outq ? (4 * q) >> 5 : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, wd);
+        const uint32_t word = __reduce_or_sync(grp, nib << ((4 * q) & 31));
+        if (wd >= 0 && lane == __ffs(grp) - 1 && word) atomicOr(&sbits[(r % PQ_SR) * sbw + wd], word);
+    };
+    // need rows rb .. re - 1 from the survivor rows around them (ring), then pbits
+    auto need_rows = [&](int rb, int re) {
         __syncthreads();
-        // need rows R0 - 1 .. R0 + 14 (row R0 + 15 waits for the next block's
-        // first survivors); task (row k, strip word i), 4 + 64 tasks in the last block
-        const bool last = R0 + PS_RB >= H;
-        if (t < 64 + (last ? 4 : 0)) {
-            const int k = t < 64 ? t >> 2 : 16, i = t & 3;
-            const int r = R0 - 1 + k;  // need(r) = survivors of P rows r - 1 .. r + 1 (sP k .. k + 2)
+        const int ntask = (re - rb) * wpr;
+        for (int base0 = 0; base0 < ntask; base0 += nt) {
+            const int ti = base0 + tid;
             uint32_t nw = 0;
-            if (r >= 0 && r < H) {
-                auto orw = [&](int w) -> uint32_t {  // ballot word w of rows k .. k + 2
-                    if (w < 0 || w >= PS_NW) return 0u;
-                    return sP[k][w] | sP[k + 1][w] | (k + 2 <= PS_RB + 1 ? sP[k + 2][w] : 0u);
+            int r = 0, w = 0;
+            if (ti < ntask) {
+                r = rb + ti / wpr;
+                w = ti % wpr;
+                auto orw = [&](int ww) -> uint32_t {
+                    if (ww < 0 || ww >= wpr) return 0u;
+                    uint32_t x = r >= t_lo ? sbits[(r % PQ_SR) * sbw + ww] : 0u;
+                    if (r - 1 >= t_lo) x |= sbits[((r - 1) % PQ_SR) * sbw + ww];
+                    if (r + 1 <= t_hi) x |= sbits[((r + 1) % PQ_SR) * sbw + ww];
+                    return x;
                 };
-                auto dil = [&](int w) {  // horizontal 3-dilation in thread (t) space
-                    const uint32_t X = orw(w);
-                    return X | (X << 1 | orw(w - 1) >> 31) | (X >> 1 | orw(w + 1) << 31);
-                };
-                nw = __funnelshift_r(dil(i), dil(i + 1), 2);  // strip columns 32 i .. 32 i + 31
-                uint32_t pw = __funnelshift_r(sP[k + 1][i], i + 1 < PS_NW ? sP[k + 1][i + 1] : 0u, 2);
-                const int ub = x0 + 32 * i;
-                const uint32_t valid = ub >= W ? 0u : W - ub >= 32 ? 0xffffffffu : (1u << (W - ub)) - 1u;
-                nw &= valid;
-                pw &= valid;
-                if ((ub >> 5) < wpr && r >= P0) d.pbits[((size_t)f * H + r) * wpr + (ub >> 5)] = pw;
+                const uint32_t X = orw(w);
+                nw = X | (X << 1 | orw(w - 1) >> 31) | (X >> 1 | orw(w + 1) << 31);
+                const int ub = 32 * w;
+                if (W - ub < 32) nw &= (1u << (W - ub)) - 1u;
+                if (r >= pa) d.pbits[((size_t)f * H + r) * wpr + w] = sbits[(r % PQ_SR) * sbw + w];
             }
-            const unsigned am = t < 64 ? 0xffffffffu : 0xfu;  // warp 2: the 4 tasks of row R0 + 15
             const int cnt = __popc(nw);
             int pre = cnt;
             for (int o = 1; o < 32; o <<= 1) {
-                const int q = __shfl_up_sync(am, pre, o);
-                if (lane >= o) pre += q;
+                const int x = __shfl_up_sync(0xffffffffu, pre, o);
+                if (lane >= o) pre += x;
             }
-            const int tot = __shfl_sync(am, pre, 31 - __clz(am));
-            unsigned base = 0;
-            if (lane == 0 && tot) base = atomicAdd(&d.aux[f].fneed, (unsigned)tot);
-            base = __shfl_sync(am, base, 0) + (unsigned)(pre - cnt);
+            const int tot = __shfl_sync(0xffffffffu, pre, 31);
+            unsigned bo = 0;
+            if (lane == 0 && tot) bo = atomicAdd(&d.aux[f].fneed, (unsigned)tot);
+            bo = __shfl_sync(0xffffffffu, bo, 0) + (unsigned)(pre - cnt);
             uint32_t* out = d.fneed + (size_t)f * d.px;
-            const int ub = x0 + 32 * i;
             while (nw) {
                 const int bb = __ffs(nw) - 1;
                 nw &= nw - 1;
-                out[base++] = ((uint32_t)r << 16) | (uint32_t)(ub + bb);
+                out[bo++] = ((uint32_t)r << 16) | (uint32_t)(32 * w + bb);
             }
         }
         __syncthreads();
+        // survivor rows older than re - 2 are no longer read: clear them for reuse
+        for (int i = tid; i < (re - rb) * sbw; i += nt) {
+            const int r = rb - 1 + i / sbw;
+            if (r >= t_lo && r < re - 1) sbits[(r % PQ_SR) * sbw + i % sbw] = 0;
+        }
+        __syncthreads();
+    };
+    int need_from = n_lo;  // next need row to emit
+    int slot = 0;          // ring slot of input row e - 6 (e the next E row); e + 5 reuses it
+    // one row step: E row e into N (its storage held E(e - 3)), then P row e - 1
+    // with M = E(e - 2) (O = E(e - 1)); at e == H, N = E(H - 1) (the mirror of row H)
+    auto step = [&](int e, RowE& M, RowE& O, RowE& N) {
+        if (e < H) {
+            uint4 hp;
+            hrow(e + 5, hp);
+            addrow(ring[slot * nt + tid], -1);
+            addrow(hp, 1);
+            ring[slot * nt + tid] = hp;  // (PQ_RING = 11: row e + 5 takes row e - 6's slot)
+            slot = slot + 1 == PQ_RING ? 0 : slot + 1;
+            make_row(N);
+        } else {
+            N = O;
+        }
+        const int r = e - 1;
+        if (r >= t_lo) test_row(r, r == 0 ? O : M, O, N);  // mirror(-1) = 0
+        // rows up to r are tested: need rows up to r - 1 are final
+        if ((r - need_from + 1 >= PQ_RB && r >= t_lo) || r == t_hi) {
+            const int re = r == t_hi ? pb : r;
+            if (re > need_from) need_rows(need_from, re);
+            need_from = re;
+        }
+    };
+    RowE X, Y, Z;
+    make_row(Z);  // E row e0
+    Y = Z;        // (rolls into the A slot of the first test, which only happens for r >= P0)
+    __syncthreads();  // sbits cleared
+    const int e_last = t_hi + 1;  // == H: the last step mirrors E row H
+    for (int e = e0 + 1; e <= e_last; e += 3) {
+        step(e, Y, Z, X);
+        if (e + 1 <= e_last) step(e + 1, Z, X, Y);
+        if (e + 2 <= e_last) step(e + 2, X, Y, Z);
     }
     for (int o = 16; o; o >>= 1) nmask += __shfl_xor_sync(0xffffffffu, nmask, o);
     if (lane == 0 && nmask) atomicAdd(&d.aux[f].mask_px, (unsigned long long)nmask);
+}
+
+size_t prescreen_smem(int W, int nt) {
+    return (size_t)PQ_RING * nt * 16 + (size_t)PQ_SR * ((W + 31) / 32 + 1) * 4;
+}
+
+int prescreen_segments(int H) { return H >= 128 ? 2 : 1; }
+
+int prescreen_threads(int W) {
+    const int qlast = (W - 1) >> 2;
+    return 32 * ((qlast + 1 + 29) / 30);
 }
 
 // FP32 bilateral of the need pixels (k_prescreen's list), one thread per
@@ -1038,9 +1101,12 @@ __global__ void __launch_bounds__(128) k_sobel_decide(Dev d) {
 
 constexpr size_t kNeedTabSmem = 511 * 16 * sizeof(float2);
 
-cudaError_t configure_fastpath() {
+cudaError_t configure_fastpath(int W) {
     cudaError_t e = cudaFuncSetAttribute(k_bilateral_need, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kNeedTabSmem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_prescreen, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 prescreen_smem(W, prescreen_threads(W)));
     for (auto fn : {k_bilateral_fast<5, 0>, k_bilateral_fast<5, 10>, k_bilateral_fast<5, 21>,
                     k_bilateral_fast<5, 27>, k_bilateral_fast<5, 31>, k_bilateral_fast<5, 63>})
         if (e == cudaSuccess)
@@ -1060,7 +1126,8 @@ int need_bilateral_ctas(int sm_count) {
 // bilateral of its need pixels (all = 1: every pixel, for lk_fast_path_error).
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all) {
     if (!all)
-        k_prescreen<<<dim3((d.W + 127) / 128, n), PS_NT, 0, s>>>(d, lp.ps);
+        k_prescreen<<<dim3(n, prescreen_segments(d.H)), prescreen_threads(d.W),
+                      prescreen_smem(d.W, prescreen_threads(d.W)), s>>>(d, lp.ps);
     k_bilateral_need<<<lp.need_ctas, 256, kNeedTabSmem, s>>>(d, lp.nbf, n, all);
 }
 

@@ -2192,7 +2192,7 @@ cudaError_t configure_kernels(const LaunchPlan& lp) {
     if ((e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lp.select_smem)))
         return e;
-    return configure_fastpath();
+    return configure_fastpath(lp.fast_width);
 }
 
 }  // namespace lkg

@@ -63,6 +63,7 @@ struct LaunchPlan {
     PrescreenParam ps;
     NeedBfParam nbf;
     int need_ctas;            // persistent k_bilateral_need CTAs
+    int fast_width;           // frame width (k_prescreen's block shape)
     int fast_front;           // certified fast bilateral + exact refinement (lk_fastpath.cu)
     int fast_table;           // mask of tap pairs whose range factor comes from the smem table
     int fast_tpc;             // fast-bilateral tiles per CTA (LK_BF_TPC)
@@ -98,7 +99,9 @@ int stereo_launches();
 cudaError_t configure_kernels(const LaunchPlan& lp);
 int vdisparity_rows(int W, int D1);
 size_t vdisparity_smem(int W, int D1);
-cudaError_t configure_fastpath();
+cudaError_t configure_fastpath(int W);
+size_t prescreen_smem(int W, int nt);
+int prescreen_threads(int W);
 int need_bilateral_ctas(int sm_count);
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all = 0);
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
