@@ -401,9 +401,12 @@ def run_ours(args):
     achieved = bytes_per_frame * tf / (dom_ms * 1e-3) / 1e9
     win = 2 * ((cfg.bf_window - 1) // 2) + 1
     taps = win * win * px * tf  # nominal range-weight evaluations of one launch
-    sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
-    xu_ex2_peak = 16 * torch.cuda.get_device_properties(local).multi_processor_count * sm_mhz * 1e6
     pipe_fps_hbm = fps / world / (hbm_peak * 1e9 / bytes_per_frame)
+    # stage 5 is one kernel, k_vdisparity (K1): the path's HBM-bound kernel.
+    # Algorithmic bytes: the u8 disparity read + the transposed i32 histogram written.
+    k1_ms = float(solo_ms[5])
+    k1_bytes = px + 4 * H * (cfg.d_max + 1)
+    k1_gbs = k1_bytes * tf / (k1_ms * 1e-3) / 1e9 if k1_ms > 0 else None
 
     line = {
         "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -437,16 +440,22 @@ def run_ours(args):
                       f"region runs {B // tf_dev} overlapping ranges of {tf_dev} frames",
             "pipeline_frac_of_hbm_roofline": pipe_fps_hbm,
             "compute": {
-                "kernel": "k_bilateral_fast (certified FP32 approximation, DESIGN.md §3)"
+                "kernel": ("k_prescreen (certified box-moment pre-screen) + k_bilateral_need "
+                           "(FP32 bilateral of the survivors' 3x3 neighbourhoods), DESIGN.md §3")
                           if dom == 9 else f"stage {dom} kernels (see stage_ms)",
-                "taps_per_s": taps / (dom_ms * 1e-3) if dom == 9 else None,
-                "mufu_ex2_only_ceiling_per_s": xu_ex2_peak,
-                "note": "range weights from a conflict-free shared-memory table "
-                        "(LK_BF_TABLE tap-pair mask, default 63: all five pairs and the 11th "
-                        "column from the table; MUFU ex2 is the per-pair alternative); FMA-pipe- and "
-                        "LSU-bound (profiles/r01_k_bilateral_fast_ncu.txt). taps are nominal: "
-                        "tiles with no road-mask pixel within one pixel are skipped"},
+                "nominal_taps_per_s": taps / (dom_ms * 1e-3) if dom == 9 else None,
+                "note": "compute-bound stage (integer dp4a box sums, FP32 bound arithmetic, "
+                        "shared-memory range-table gathers); the nominal taps count every pixel's "
+                        "121-tap window although only the pre-screen survivors' neighbourhoods "
+                        "are filtered (profiles/r02_*_ncu.txt)"},
         },
+        "roofline_k1": {
+            "bound": "hbm", "kernel": "k_vdisparity (stage 5, TMA bulk-staged rows)",
+            "achieved": k1_gbs, "peak": hbm_peak, "unit": "GB/s",
+            "frac": k1_gbs / hbm_peak if k1_gbs else None, "kernel_ms": k1_ms,
+            "algorithmic_bytes": f"{k1_bytes} B/frame (u8 disparity in, i32 [D1][H] histogram "
+                                 f"out) x {tf}",
+            "timing": "stage 5 of the same single-range replay (CUDA events)"},
         "notes": f"paper: {PAPER_FPS} fps on GTX 970M + i7 (different hardware, context only)",
     }
     traffic = ROOT / "profiles" / "traffic.json"

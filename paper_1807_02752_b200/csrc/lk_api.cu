@@ -83,7 +83,6 @@ constexpr int kMaxBranches = 16;      // concurrent frame ranges (streams) per b
 constexpr int kMinBranchFrames = 16;  // smallest range worth a branch
 constexpr int kH2dChunksDefault = 12; // host-fed batches: copy/compute pipeline depth
 constexpr int kBranchesDefault = 8;   // device-resident batches: concurrent frame ranges
-constexpr int kFastTableDefault = 63;  // tap pairs of the fast bilateral served by the range table
 
 }  // namespace
 
@@ -355,10 +354,8 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         if (s == LK_OK) s = c->alloc(p, n);
     };
     double *d_ws, *d_wr, *d_val;
-    float* d_ft = nullptr;
     float2* d_nt = nullptr;
     std::vector<float2> need_tab;
-    std::vector<float> fast_tab;
     uint64_t* d_rng;
     A(&d_ws, ws.size());
     A(&d_wr, wr.size());
@@ -463,39 +460,6 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         lp.fast_front = win == 11 && !d.hooks && !(flags & LK_FLAG_EXACT) && xmax <= 20.0 &&
                         lkg::prescreen_threads(W) <= 768 &&
                         lkg::prescreen_smem(W, lkg::prescreen_threads(W)) <= 200 * 1024;
-        const double log2e = 1.4426950408889634;
-        for (int dj = -5; dj <= 5; ++dj)
-            for (int di = -5; di <= 5; ++di)
-                lp.fbf.c[(dj + 5) * 11 + (di + 5)] =
-                    (float)(-(double)(di * di + dj * dj) * inv_s2 * log2e);
-        for (int dj = 0; dj < 11; ++dj)
-            for (int q = 0; q < 5; ++q)
-                lp.fbf.cp[dj][q] = make_float2(lp.fbf.c[dj * 11 + 2 * q], lp.fbf.c[dj * 11 + 2 * q + 1]);
-        for (int k = 0; k < 12; ++k) {
-            auto c10 = [&](int dj) { return dj < 0 || dj > 10 ? -INFINITY : lp.fbf.c[dj * 11 + 10]; };
-            lp.fbf.c10[k] = make_float2(c10(k), c10(k - 1));
-            auto s10 = [&](int dj) {
-                return dj < 0 || dj > 10 ? 0.f : (float)std::exp(-(double)(25 + (dj - 5) * (dj - 5)) * inv_s2);
-            };
-            lp.fbf.s10[k] = make_float2(s10(k), s10(k - 1));
-        }
-        lp.fbf.c2 = (float)(-inv_r2 * log2e);
-        for (int dj = -5; dj <= 5; ++dj)
-            for (int q = 0; q < 5; ++q) {
-                auto sf = [&](int di) { return (float)std::exp(-(double)(di * di + dj * dj) * inv_s2); };
-                lp.fbf.sp[dj + 5][q] = make_float2(sf(2 * q - 5), sf(2 * q - 4));
-            }
-        fast_tab.resize(256 + 512);
-        for (int k = 0; k < 256; ++k) fast_tab[k] = (float)(k / 255.0);
-        for (int i = 0; i < 512; ++i) {
-            const double dr = (i - 255) / 255.0;
-            fast_tab[256 + i] = i < 511 ? (float)std::exp(-dr * dr * inv_r2) : 0.f;
-        }
-        const char* m = std::getenv("LK_BF_TABLE");
-        lp.fast_table = m ? std::atoi(m) & 63 : kFastTableDefault;
-        const char* tpc = std::getenv("LK_BF_TPC");  // tiles per CTA
-        lp.fast_tpc = tpc ? std::atoi(tpc) : 24;
-        d.bf_ntiles = ((W + lkg::BT_W - 1) / lkg::BT_W) * ((H + lkg::BT_H - 1) / lkg::BT_H);
         d.n_stile = ((W + lkg::SB_TW - 1) / lkg::SB_TW) * ((H + lkg::SB_TH - 1) / lkg::SB_TH);
         d.need_cap = d.n_stile * (lkg::SB_TW + 2) * (lkg::SB_TH + 2);  // every ring pixel of every tile
         lp.refine_ctas = 8;
@@ -536,13 +500,11 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
             A(&d.pbits, (size_t)B * H * d.words_per_row);
             A(&d.fneed, (size_t)B * d.px);
             A(&d_nt, need_tab.size());
-            A(&d.bf_flag, (size_t)B * d.bf_ntiles);
             A(&d.need, (size_t)B * d.need_cap);
             A(&d.need_cnt, (size_t)B);
             A(&d.ctile, (size_t)B * d.n_stile);
             A(&d.ctile_cnt, (size_t)B);
         }
-        A(&d_ft, fast_tab.size());
     }
     lp.vanish_smem = (size_t)(2 * C + 32) * 8 + (size_t)2 * C * 4 + (size_t)2 * H * 4 +
                      (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 8 + (size_t)(H + 1) * 4 +
@@ -607,8 +569,6 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     if (e == cudaSuccess) e = cudaMemcpy(d_wr, wr.data(), wr.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d_val, val.data(), val.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d_rng, rng.data(), rng.size() * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d_ft, fast_tab.data(), fast_tab.size() * 4, cudaMemcpyHostToDevice);
-    d.fast_tab = d_ft;
     if (e == cudaSuccess && d_nt)
         e = cudaMemcpy(d_nt, need_tab.data(), need_tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
     d.need_tab = d_nt;
@@ -727,7 +687,6 @@ static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     sh(v.smoothed_f, px);
     sh(v.pbits, H * d.words_per_row);
     sh(v.fneed, px);
-    sh(v.bf_flag, (size_t)d.bf_ntiles);
     sh(v.need, (size_t)d.need_cap);
     sh(v.need_cnt, 1);
     sh(v.ctile, (size_t)d.n_stile);

@@ -84,15 +84,12 @@ struct Dev {
     double* vpx;            // [B][H]
     double* smoothed;       // [B][H][W] (fast path: exact only around edge candidates)
     float* smoothed_f;      // [B][H][W] certified approximation (fast path)
-    uint8_t* bf_flag;       // [B][bf_ntiles] fast-bilateral tiles the Sobel screen needs
-    int bf_ntiles;          // fast-bilateral tiles per frame
     uint32_t* need;         // [B][need_cap] pixels (v << 16 | u) whose exact smoothed value the
                             // fast path needs (3x3 neighbourhoods of Sobel candidates)
     uint32_t* need_cnt;     // [B]
     uint32_t* ctile;        // [B][n_stile] Sobel tiles holding candidates
     uint32_t* ctile_cnt;    // [B]
     int need_cap, n_stile;
-    const float* fast_tab;  // [256] k/255 as float, then [512] range factor of dr = (i-255)/255
     const float2* need_tab; // [511] (R(delta), R(delta) * delta), delta = i - 255 (k_bilateral_need)
     uint32_t* pbits;        // [B][H][words_per_row] pre-screen survivors ("possibly an edge")
     uint32_t* fneed;        // [B][px] pixels (v << 16 | u) whose s~ the Sobel screen needs

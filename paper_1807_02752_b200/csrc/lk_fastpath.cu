@@ -6,15 +6,19 @@
 // come from the edge list, preprocess.hpp:103-113), and the only integer
 // decision taken on non-edge pixels is "not an edge". So:
 //
-//  1. k_bilateral_fast computes every needed pixel approximately: weights
-//     2^(c_t + c2*dr^2) (MUFU ex2 or an exact-index shared table) and FP32
-//     sums. A rigorous bound |s~ - s| <= kEpsSmooth holds against the exact
-//     double result (derivation in DESIGN.md §3; the worst error measured is
-//     checked by tests/test_gpu_fastpath.py).
-//  2. k_sobel_screen evaluates Sobel on s~ and propagates the bound to
-//     s = gx^2 + gy^2. A masked pixel whose s can still reach the threshold is
-//     a candidate; its 3x3 neighbourhood goes to the frame's need list.
-//  3. k_refine_exact gives every need pixel its EXACT bilateral (the LUT
+//  0. k_prescreen certifies, from integer box sums of the raw grey bytes,
+//     which road-mask pixels cannot be edges (most of them): only the
+//     survivors and their 3x3 neighbourhoods go on.
+//  1. k_bilateral_need computes the neighbourhood ("need") pixels
+//     approximately in FP32 from an exact-index shared range table. A
+//     rigorous bound |s~ - s| <= kEpsSmooth holds against the exact double
+//     result (derivation in DESIGN.md §3; the worst error measured is checked
+//     by tests/test_gpu_fastpath.py).
+//  2. k_sobel_screen evaluates Sobel on s~ at the survivors and propagates the
+//     bound to s = gx^2 + gy^2. A survivor whose s can still reach the
+//     threshold is a candidate; its 3x3 neighbourhood goes to the frame's
+//     exact need list.
+//  3. k_refine_exact gives every exact need pixel its EXACT bilateral (the LUT
 //     arithmetic of k_bilateral_tile), and k_sobel_decide takes each
 //     candidate's edge decision from those exact values.
 //
@@ -33,285 +37,6 @@ namespace lkg {
 
 constexpr double kEpsSmooth = 2.5e-5;  // bound on |s~ - s| (absolute, values in [0, 1])
 
-__device__ __forceinline__ float ex2_approx(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-// ---- 1. approximate bilateral: tile BT_W x BT_H, BT_R outputs per thread
-//
-// Issue-slot budget per (output, window row): 5 packed tap pairs + the 11th
-// column, where every instruction counts (the kernel is issue-, LSU- and
-// MUFU-bound at once; the FMA pipe binds first):
-//  - window values come in as 8-byte pairs (LDS.64). The tile is staged twice,
-//    the second copy shifted by one pixel, so an odd column's pair is aligned too;
-//  - MUFU pairs: dr = v_q - v_p (FADD2), c2*dr^2 + c_t (FMUL2, FFMA2), 2x ex2;
-//  - table pairs: one FFMA2 turns v_q into the shared-memory byte ADDRESS of
-//    R[k_q - k_p] in this lane's copy. The FMA lands in the subnormal range,
-//    where a float's bit pattern is the integer multiple of 2^-149, so
-//    RN(v_q*32640*2^-149 + C_p) has bits A_lane + 128(k_q - k_p + 255) exactly
-//    (v_q*32640 is within 6e-3 of 128 k_q; C_p = RN((A_lane + 32640 -
-//    v_p*32640) * 2^-149) is an exact integer). The LDS takes that register as
-//    its address: no differences, no integer adds, no keys;
-//  - sums go straight into float2 accumulators (no per-row combine);
-//  - the 11th column of outputs r and r+1 runs as one packed pair (the window
-//    row offsets differ by one; a -inf exponent zeroes a row outside a window).
-// The FP32 error of the longer sum chains is budgeted in DESIGN.md §3.
-//
-// all = 0 (the pipeline): s~ is consumed only by the Sobel of road-mask pixels
-// (k_sobel_screen), i.e. within one pixel of a masked pixel (mirroring at the
-// border stays within that pixel). Tiles whose one-pixel ring holds no masked
-// pixel are skipped (k_bf_flags, the exact road_mask test of preprocess.hpp:14-25).
-// all = 1 computes every tile (lk_fast_path_error).
-__device__ __forceinline__ float lds_f32(unsigned addr) {
-    float v;
-    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-    return v;
-}
-
-//
-// Range table: R[k_q - k_p] (511 entries) replicated 32 times entry-major
-// (word 32 i + lane) in 64 KB of dynamic shared memory, 2 CTAs per SM: lane L
-// always reads bank L, so a warp's lookup is one wavefront whatever the
-// differences (a single copy averaged ~3.1 wavefronts per lookup). The index
-// FFMA2 takes v_q itself with a per-output constant (the address formula is
-// above), so a table pair costs 4 packed FMA-pipe ops (index, S_t * R, num,
-// den) against 5 for a MUFU pair; a 256-entry R[|k_q - k_p|] table that fits
-// 3 CTAs in 48 KB needs |dr| for its index and measured 2.39 vs 2.30 ms.
-// The table is staged once per CTA, which walks TPC consecutive tiles.
-//
-// Staging is software-pipelined: the grey bytes of the CTA's next needed tile
-// are loaded into registers before the current tile's taps run, so their
-// global latency hides behind ~10^4 cycles of arithmetic (the old per-tile
-// load -> barrier -> compute sequence left ~30 % of the stall samples on the
-// staging loads). Which tiles are needed comes from k_bf_flags.
-constexpr int BF_PF = (BT_W + 10) * (BT_H + 10) / 256 + 1;  // prefetched bytes per thread
-
-template <int RHO>
-__device__ __forceinline__ void bf_issue(const Dev& d, int nbx, int nb, int t, uint32_t (&pb)[BF_PF]) {
-    constexpr int TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO, NPX = TWh * THh;
-    const int f = t / nb, tr = t - f * nb, by = tr / nbx, bx = tr - by * nbx;
-    const int u0 = bx * BT_W - RHO, v0 = by * BT_H - RHO;
-    const uint8_t* g = d.grey + (size_t)f * d.px;
-    const bool inner = u0 >= 0 && v0 >= 0 && u0 + TWh <= d.W && v0 + THh <= d.H;
-#pragma unroll
-    for (int k = 0; k < BF_PF; ++k) {
-        const int i = threadIdx.x + 256 * k;
-        if (i < NPX) {
-            const int ry = i / TWh, rx = i - ry * TWh;
-            int v = v0 + ry, u = u0 + rx;
-            if (!inner) {
-                v = mirror(v, d.H);
-                u = mirror(u, d.W);
-            }
-            pb[k] = __ldg(g + (size_t)v * d.W + u);
-        }
-    }
-}
-
-template <int RHO, int TB>
-__global__ void __launch_bounds__(256, 2) k_bilateral_fast(Dev d, FastBfParam p, int n, int tpc, int all) {
-    constexpr int WIN = 2 * RHO + 1, TWh = BT_W + 2 * RHO, THh = BT_H + 2 * RHO;
-    constexpr int NPX = TWh * THh;
-    static_assert(WIN == 11 && BT_R % 2 == 0 && TWh % 2 == 0, "packed pairs assume an 11-wide window");
-    // copy 1 starts 14 banks after copy 0 (mod 32): a half-warp's float2 row
-    // loads (even lanes from copy 0, odd lanes from copy 1) then hit 32
-    // distinct banks; NPX + 2 (bank offset 6) cost two wavefronts per
-    // half-warp, ~25 % of the kernel's shared-memory wavefronts
-    constexpr int SV = NPX + ((14 - NPX % 32) + 32) % 32;
-    static_assert(SV >= NPX + 1 && SV % 2 == 0 && SV % 32 == 14, "copy-1 bank offset");
-    __shared__ __align__(16) float s_v[2][SV];
-    extern __shared__ __align__(16) float s_R[];  // [511][32]: R[k_q - k_p + 255], lane-replicated
-    const int nbx = (d.W + BT_W - 1) / BT_W, nb = nbx * ((d.H + BT_H - 1) / BT_H);
-    const int tile0 = blockIdx.x * tpc, tile1 = min(tile0 + tpc, n * nb);
-    // needed tiles of this chunk (tpc <= 32): one ballot, the same in every warp
-    unsigned need;
-    {
-        const int t = tile0 + (threadIdx.x & 31);
-        bool nd = false;
-        if (t < tile1) nd = all ? !frame_failed(d, t / nb) : d.bf_flag[t] != 0;
-        need = __ballot_sync(0xffffffffu, nd);
-    }
-    if (!need) return;
-    const int tx = threadIdx.x % BT_W, ty = threadIdx.x / BT_W;
-    const int r0 = ty * BT_R;
-    // aligned base of this thread's window rows: element (row, tx + k) is
-    // base[row * TWh + k] in both cases (copy 1 holds element i at i + 1)
-    const float* base = (tx & 1) ? &s_v[1][tx + 1] : &s_v[0][tx];
-    const float kA = __int_as_float(128 * 255);  // |dr| * 32640 * 2^-149 = 128 |delta| (subnormal)
-    // RN(v_q kA + cidx_r) = A_lane + 128 (k_q - k_p + 255) with cidx_r = A_lane + 32640 - v_p kA
-    const float cb = __int_as_float((int)((unsigned)__cvta_generic_to_shared(s_R) + 4u * (threadIdx.x % 32) +
-                                          128u * 255u));
-    const float2 c2 = make_float2(p.c2, p.c2), kA2 = make_float2(kA, kA);
-    uint32_t pb[BF_PF];
-    int cur = tile0 + __ffs(need) - 1;
-    need &= need - 1;
-    bf_issue<RHO>(d, nbx, nb, cur, pb);
-    if (TB) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = threadIdx.x + 256 * h;  // entry e <-> delta = e - 255
-            if (e < 511) {
-                const float r = __ldg(d.fast_tab + 256 + e);
-#pragma unroll
-                for (int k = 0; k < 32; k += 4)
-                    *reinterpret_cast<float4*>(&s_R[e * 32 + k]) = make_float4(r, r, r, r);
-            }
-        }
-    }
-    while (true) {
-        __syncthreads();  // the previous tile's taps are done with s_v
-#pragma unroll
-        for (int k = 0; k < BF_PF; ++k) {
-            const int i = threadIdx.x + 256 * k;
-            if (i < NPX) {
-                const float v = __ldg(d.fast_tab + pb[k]);  // (float)(k / 255.0), an L1 hit
-                s_v[0][i] = v;
-                s_v[1][i + 1] = v;  // copy 1 is shifted: s_v[1][i] = s_v[0][i - 1]
-            }
-        }
-        __syncthreads();
-        const int f = cur / nb, tr = cur - f * nb, by = tr / nbx, bx = tr - by * nbx;
-        const int u0 = bx * BT_W, v0 = by * BT_H;
-        const int nxt = need ? tile0 + __ffs(need) - 1 : -1;
-        need &= need - 1;
-        if (nxt >= 0) bf_issue<RHO>(d, nbx, nb, nxt, pb);  // in flight during the taps below
-        // the Sobel screen reads s~ only on rows >= horizon - 1 (3x3 of masked
-        // pixels, which lie at rows >= horizon): warps whose BT_R rows are all
-        // above that, or below the image, skip their taps (warp-uniform rows)
-        const int row_lo = all ? 0 : (int)d.rep[f].horizon - 1;
-        if (v0 + r0 + BT_R - 1 >= row_lo && v0 + r0 < d.H) {
-            float va[BT_R];
-            float2 nva[BT_R], num[BT_R], den[BT_R], cidx[BT_R];
-#pragma unroll
-            for (int r = 0; r < BT_R; ++r) {
-                va[r] = base[(r0 + r + RHO) * TWh + RHO];
-                nva[r] = make_float2(-va[r], -va[r]);
-                num[r] = den[r] = make_float2(0.f, 0.f);
-                const float c = fmaf(-va[r], kA, cb);  // exact integer (x 2^-149)
-                cidx[r] = make_float2(c, c);
-            }
-            float2 n11[BT_R / 2], d11[BT_R / 2], nv11[BT_R / 2], cidx11[BT_R / 2];
-#pragma unroll
-            for (int m = 0; m < BT_R / 2; ++m) {
-                n11[m] = d11[m] = make_float2(0.f, 0.f);
-                nv11[m] = make_float2(-va[2 * m], -va[2 * m + 1]);
-                cidx11[m] = make_float2(cidx[2 * m].x, cidx[2 * m + 1].x);
-            }
-#pragma unroll
-            for (int jj = 0; jj < BT_R + 2 * RHO; ++jj) {
-                const float* row = base + (r0 + jj) * TWh;
-                float2 vp[5];
-#pragma unroll
-                for (int q = 0; q < 5; ++q) vp[q] = *reinterpret_cast<const float2*>(row + 2 * q);
-                const float vl = row[10];
-#pragma unroll
-                for (int r = 0; r < BT_R; ++r) {
-                    const int dj = jj - r;
-                    if (dj < 0 || dj >= WIN) continue;
-#pragma unroll
-                    for (int q = 0; q < 5; ++q) {
-                        float2 w;
-                        if ((TB >> q) & 1) {
-                            const float2 t = __ffma2_rn(vp[q], kA2, cidx[r]);
-                            w = __fmul2_rn(p.sp[dj][q], make_float2(lds_f32(__float_as_uint(t.x)),
-                                                                    lds_f32(__float_as_uint(t.y))));
-                        } else {
-                            const float2 dr = __fadd2_rn(vp[q], nva[r]);
-                            const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.cp[dj][q]);
-                            w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-                        }
-                        num[r] = __ffma2_rn(w, vp[q], num[r]);
-                        den[r] = __fadd2_rn(w, den[r]);
-                    }
-                }
-                // 11th column: outputs (2m, 2m + 1) use window rows (jj - 2m, jj - 2m - 1)
-#pragma unroll
-                for (int m = 0; m < BT_R / 2; ++m) {
-                    const int k = jj - 2 * m;
-                    if (k < 0 || k > WIN) continue;
-                    const float2 vl2 = make_float2(vl, vl);
-                    float2 w;
-                    if ((TB >> 5) & 1) {  // table: index pair from outputs 2m, 2m + 1
-                        const float2 t = __ffma2_rn(vl2, kA2, cidx11[m]);
-                        w = __fmul2_rn(p.s10[k], make_float2(lds_f32(__float_as_uint(t.x)),
-                                                             lds_f32(__float_as_uint(t.y))));
-                    } else {
-                        const float2 dr = __fadd2_rn(vl2, nv11[m]);
-                        const float2 x = __ffma2_rn(c2, __fmul2_rn(dr, dr), p.c10[k]);
-                        w = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-                    }
-                    n11[m] = __ffma2_rn(w, vl2, n11[m]);
-                    d11[m] = __fadd2_rn(w, d11[m]);
-                }
-            }
-            const int u = u0 + tx;
-#pragma unroll
-            for (int r = 0; r < BT_R; ++r) {
-                const int v = v0 + r0 + r;
-                const float a = (r & 1) ? n11[r / 2].y : n11[r / 2].x;
-                const float b = (r & 1) ? d11[r / 2].y : d11[r / 2].x;
-                if (u < d.W && v < d.H)
-                    d.smoothed_f[(size_t)f * d.px + (size_t)v * d.W + u] =
-                        __fdiv_rn((num[r].x + num[r].y) + a, (den[r].x + den[r].y) + b);
-            }
-        }
-        if (nxt < 0) break;
-        cur = nxt;
-    }
-}
-
-// Which fast-bilateral tiles the pipeline needs: s~ is read only by the Sobel
-// of road-mask pixels (k_sobel_screen), i.e. within one pixel of a masked
-// pixel (mirroring at the border stays within that pixel). Flag = some pixel
-// of the tile's one-pixel ring is in road_mask (preprocess.hpp:14-25, the exact
-// test k_sobel_screen applies). One CTA per (tile row, frame); failed frames
-// and bands above the horizon get 0.
-__global__ void __launch_bounds__(256) k_bf_flags(Dev d) {
-    __shared__ unsigned s_bits[(65536 + 31) / 32];
-    const int f = blockIdx.y, by = blockIdx.x, v0 = by * BT_H;
-    const int nbx = (d.W + BT_W - 1) / BT_W;
-    uint8_t* out = d.bf_flag + (size_t)f * nbx * gridDim.x + (size_t)by * nbx;
-    if (by == 0 && threadIdx.x == 0) {  // the Sobel screen appends to these lists
-        d.need_cnt[f] = 0;
-        d.ctile_cnt[f] = 0;
-    }
-    const int horizon = frame_failed(d, f) ? INT_MAX : (int)d.rep[f].horizon;
-    if (v0 + BT_H < horizon) {
-        for (int bx = threadIdx.x; bx < nbx; bx += blockDim.x) out[bx] = 0;
-        return;
-    }
-    const uint8_t* dp = d.disp + (size_t)f * d.px;
-    const int ra = max(max(v0 - 1, horizon), 0), rb = min(v0 + BT_H, d.H - 1);
-    __shared__ int2 s_mr[BT_H + 2];  // road_mask intervals of rows ra .. rb (k_road_fit)
-    if (threadIdx.x <= rb - ra) s_mr[threadIdx.x] = d.mrange[(size_t)f * d.H + ra + threadIdx.x];
-    __syncthreads();
-    const int nw = (d.W + 31) / 32;
-    for (int c0 = threadIdx.x & ~31; c0 < nw * 32; c0 += blockDim.x) {
-        const int c = c0 + (threadIdx.x & 31);
-        bool any = false;
-        if (c < d.W)
-            for (int r = ra; r <= rb && !any; ++r) {
-                const int dv = dp[(size_t)r * d.W + c];
-                any = dv >= s_mr[r - ra].x && dv <= s_mr[r - ra].y;  // road_mask, preprocess.hpp:14-25
-            }
-        const unsigned b = __ballot_sync(0xffffffffu, any);
-        if ((threadIdx.x & 31) == 0) s_bits[c0 >> 5] = b;
-    }
-    __syncthreads();
-    for (int bx = threadIdx.x; bx < nbx; bx += blockDim.x) {
-        const int lo = max(bx * BT_W - 1, 0), hi = min(bx * BT_W + BT_W, d.W - 1);
-        bool any = false;
-        for (int w = lo >> 5; w <= (hi >> 5) && !any; ++w) {
-            unsigned m = s_bits[w];
-            if (w == (lo >> 5)) m &= ~0u << (lo & 31);
-            if (w == (hi >> 5)) m &= (hi & 31) == 31 ? ~0u : (1u << ((hi & 31) + 1)) - 1u;
-            any = m != 0;
-        }
-        out[bx] = any;
-    }
-}
 
 // Exact bilateral at in-image pixel (u, v) from the staged mirrored grey tile
 // (origin gx0, gy0): the arithmetic of k_bilateral_tile / preprocess.hpp:38-56,
@@ -380,18 +105,14 @@ __device__ __forceinline__ double exact_bilateral(const Dev& d, const WsParam& w
 // Thread t of a tile owns pixels (row (t>>7) * SB_TH / 2 + k, col t & 127), k < SB_TH / 2, so
 // each warp covers 32 consecutive pixels of a row and its ballot is a
 // candidate / edge word directly.
-__global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
+__global__ void __launch_bounds__(128) k_sobel_screen(Dev d) {
     constexpr int FW = SB_TW + 2, FH = SB_TH + 2;  // tile + 1-px ring
     constexpr int NWORD = (FW + 31) / 32;          // ring row bitmap words
     constexpr int TWORD = SB_TW / 32;              // tile row bitmap words
-    constexpr int NF = (FH * FW + 255) / 256;
-    static_assert(SB_TW == 128 && SB_TH % 2 == 0, "pixel ownership assumes 128-wide tiles");
-    constexpr int FWP = FW + 2;  // staged row pitch (even: 8-byte pairs)
-    __shared__ __align__(8) float s_f[FH * FWP];
+    static_assert(SB_TW == 128 && SB_TH * TWORD <= 128, "one thread per survivor word");
     __shared__ unsigned s_cw[SB_TH][TWORD];
     __shared__ unsigned s_need[FH][NWORD];
     __shared__ int s_nneed, s_base;
-    __shared__ unsigned s_pw[SB_TH][TWORD];  // pre-screen survivors (k_prescreen)
     const int f = blockIdx.z;
     if (frame_failed(d, f)) return;
     if (d.W < 3 || d.H < 3) {  // preprocess.hpp:68-69
@@ -399,7 +120,7 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
             fail_frame(d, f, 10, LK_MSG_SOBEL_TOO_SMALL);
         return;
     }
-    const int W = d.W, H = d.H, tid = threadIdx.x, lane = tid & 31;
+    const int W = d.W, H = d.H, tid = threadIdx.x;
     const int u0 = blockIdx.x * SB_TW, v0 = blockIdx.y * SB_TH;
     const int horizon = (int)d.rep[f].horizon;
     if (v0 + SB_TH <= horizon) {  // the mask is empty above the horizon
@@ -408,99 +129,38 @@ __global__ void __launch_bounds__(256, 4) k_sobel_screen(Dev d) {
         return;
     }
     const float* sf = d.smoothed_f + (size_t)f * d.px;
-    // owned pixels: rows pr0 * SB_PPT + k (consecutive, so the 3x3 window slides
-    // down one row per pixel), column pc
-    const int pc = tid & (SB_TW - 1), pr0 = (tid >> 7) * SB_PPT;
     // only pre-screen survivors (masked pixels that can still be edges) are
-    // screened; a tile without survivors has no edge
-    bool anyp = false;
+    // screened, one thread per 32-pixel survivor word: each survivor reads the
+    // s~ of its 3x3 neighbourhood (need pixels of k_bilateral_need, mirrored at
+    // the border, preprocess.hpp:71-72)
+    const float D = (float)(8.0 * kEpsSmooth + 1e-6);
+    unsigned cw = 0;
     if (tid < SB_TH * TWORD) {
-        const int r = tid / TWORD, w = (u0 >> 5) + tid % TWORD;
-        const unsigned x = v0 + r < H && w < d.words_per_row
-                               ? d.pbits[((size_t)f * H + v0 + r) * d.words_per_row + w] : 0u;
-        s_pw[r][tid % TWORD] = x;
-        anyp = x != 0;
-    }
-    if (!__syncthreads_or(anyp)) {
-        if (tid < SB_TH && v0 + tid < H)
-            d.seg_cnt[((size_t)f * H + v0 + tid) * d.n_seg + blockIdx.x] = 0;
-        return;
-    }
-    // s~ tile + ring: s_f[r][j] holds column u0 - 2 + j (j = c + 1 for ring column c),
-    // so interior tiles stage aligned 8-byte pairs (row starts are 8-byte aligned)
-    if (u0 >= 2 && v0 >= 1 && u0 + FWP - 2 <= W && v0 + FH - 1 <= H && (W & 1) == 0) {
-        constexpr int NP = FWP / 2, NF2 = (FH * NP + 255) / 256;
-        float2 t[NF2];
-#pragma unroll
-        for (int q = 0; q < NF2; ++q) {
-            const int i = tid + q * 256;
-            if (i < FH * NP) {
-                const int r = i / NP, m = i - r * NP;
-                t[q] = *reinterpret_cast<const float2*>(sf + (size_t)(v0 - 1 + r) * W + u0 - 2 + 2 * m);
-            }
+        const int r = tid / TWORD, wt = tid % TWORD, w = (u0 >> 5) + wt;
+        const int v = v0 + r;
+        unsigned x = v < H && w < d.words_per_row
+                         ? d.pbits[((size_t)f * H + v) * d.words_per_row + w] : 0u;
+        const float* ra = sf + (size_t)mirror(v - 1, H) * W;
+        const float* rb = sf + (size_t)v * W;
+        const float* rc = sf + (size_t)mirror(v + 1, H) * W;
+        while (x) {
+            const int bit = __ffs(x) - 1;
+            x &= x - 1;
+            const int u = 32 * w + bit, ul = mirror(u - 1, W), ur = mirror(u + 1, W);
+            const float a0 = ra[ul], a1 = ra[u], a2 = ra[ur];
+            const float b0 = rb[ul], b2 = rb[ur];
+            const float c0 = rc[ul], c1 = rc[u], c2 = rc[ur];
+            const float gx = ((a2 - a0) + 2.f * (b2 - b0)) + (c2 - c0);
+            const float gy = ((c0 - a0) + 2.f * (c1 - a1)) + (c2 - a2);
+            const float sg = gx * gx + gy * gy;
+            const float ds = 1.001f * (D * (2.f * fabsf(gx) + D) + D * (2.f * fabsf(gy) + D)) +
+                             4e-7f * sg + 1e-9f;
+            if (sg + ds >= d.sobel_s_star_lo) cw |= 1u << bit;
         }
-#pragma unroll
-        for (int q = 0; q < NF2; ++q)
-            if (tid + q * 256 < FH * NP) reinterpret_cast<float2*>(s_f)[tid + q * 256] = t[q];
-    } else {
-        float t[NF];
-#pragma unroll
-        for (int q = 0; q < NF; ++q) {
-            const int i = tid + q * 256;
-            t[q] = 0.f;
-            if (i < FH * FW) {
-                const int r = i / FW, c = i - r * FW;
-                t[q] = sf[(size_t)mirror(v0 - 1 + r, H) * W + mirror(u0 - 1 + c, W)];
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < NF; ++q) {
-            const int i = tid + q * 256;
-            if (i < FH * FW) s_f[(i / FW) * FWP + i % FW + 1] = t[q];
-        }
+        s_cw[r][wt] = cw;
     }
     if (tid == 0) s_nneed = 0;
-    __syncthreads();
-    const float D = (float)(8.0 * kEpsSmooth + 1e-6);
-    int any_cand = 0;
-    // window rows v-1, v, v+1 at columns u-1, u, u+1 (ring row r holds image row v0 - 1 + r)
-    float a[3], b[3], cc[3];
-    {
-        const float* p = s_f + pr0 * FWP + pc + 1;
-#pragma unroll
-        for (int x = 0; x < 3; ++x) {
-            a[x] = p[x];
-            b[x] = p[FWP + x];
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < SB_PPT; ++k) {
-        const int r = pr0 + k;
-        {
-            const float* p = s_f + (r + 2) * FWP + pc + 1;
-#pragma unroll
-            for (int x = 0; x < 3; ++x) cc[x] = p[x];
-        }
-        const bool m = (s_pw[r][pc >> 5] >> (pc & 31)) & 1;  // survivor => road_mask pixel
-        bool cand = false;
-        if (m) {
-            const float gx = ((a[2] - a[0]) + 2.f * (b[2] - b[0])) + (cc[2] - cc[0]);
-            const float gy = ((cc[0] - a[0]) + 2.f * (cc[1] - a[1])) + (cc[2] - a[2]);
-            const float s = gx * gx + gy * gy;
-            const float ds = 1.001f * (D * (2.f * fabsf(gx) + D) + D * (2.f * fabsf(gy) + D)) +
-                             4e-7f * s + 1e-9f;
-            cand = s + ds >= d.sobel_s_star_lo;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, cand);
-        if (lane == 0) s_cw[r][pc >> 5] = bal;
-        any_cand |= cand;
-#pragma unroll
-        for (int x = 0; x < 3; ++x) {
-            a[x] = b[x];
-            b[x] = cc[x];
-        }
-    }
-    if (!__syncthreads_or(any_cand)) {  // no edge can exist in this tile (most tiles)
+    if (!__syncthreads_or(cw != 0)) {  // no edge can exist in this tile (most tiles)
         if (tid < SB_TH && v0 + tid < H)
             d.seg_cnt[((size_t)f * H + v0 + tid) * d.n_seg + blockIdx.x] = 0;
         return;
@@ -1107,10 +767,6 @@ cudaError_t configure_fastpath(int W) {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_prescreen, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  prescreen_smem(W, prescreen_threads(W)));
-    for (auto fn : {k_bilateral_fast<5, 0>, k_bilateral_fast<5, 10>, k_bilateral_fast<5, 21>,
-                    k_bilateral_fast<5, 27>, k_bilateral_fast<5, 31>, k_bilateral_fast<5, 63>})
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 511 * 32 * 4);
     return e;
 }
 
@@ -1133,7 +789,7 @@ void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream
 
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s) {
     const dim3 g((d.W + SB_TW - 1) / SB_TW, (d.H + SB_TH - 1) / SB_TH, n);
-    k_sobel_screen<<<g, 256, 0, s>>>(d);
+    k_sobel_screen<<<g, 128, 0, s>>>(d);
     k_refine_exact<5><<<dim3(lp.refine_ctas, n), 256, 0, s>>>(d, lp.ws);
     k_sobel_decide<<<dim3(lp.decide_ctas, n), 128, 0, s>>>(d);
 }

@@ -2153,7 +2153,7 @@ void launch_exact_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
 }
 
 // Kernels per frame range: the exact path (k_bilateral_tile, k_sobel_edges) or
-// the certified fast path (k_bf_flags, k_bilateral_fast, k_sobel_screen,
+// the certified fast path (k_prescreen, k_bilateral_need, k_sobel_screen,
 // k_refine_exact, k_sobel_decide: 3 more), 5 more with the auto threshold.
 int launches_per_batch(const Dev& d, const LaunchPlan& lp) {
     return (isnan(d.tr_lpv) ? 19 : 14) + (lp.fast_front ? 3 : 0);

@@ -27,17 +27,6 @@ struct WsParam {
     double w[121];
 };
 
-// Approximate bilateral (lk_fastpath.cu): log2-domain spatial terms, range
-// coefficient, and the 8-bit values as floats; passed by value.
-struct FastBfParam {
-    float2 cp[11][5];  // c of taps (2q, 2q+1) of window row dj: packed f32x2 operands
-    float2 sp[11][5];  // the same taps' spatial factors 2^c (range-table taps)
-    float c[121];  // -ds * inv_s2 * log2(e) per tap
-    float2 c10[12];  // 11th-column pair (c[k][10], c[k-1][10]), -inf outside the window
-    float2 s10[12];  // the same pair's spatial factors 2^c (0 outside the window; table taps)
-    float c2;      // -inv_r2 * log2(e)
-};
-
 // Certified pre-screen (k_prescreen): constants of the bound |s - b| <= E on
 // the gap between the bilateral s and the 11x11 box mean b,
 // each rounded so the bound stays an upper bound.
@@ -59,14 +48,11 @@ struct NeedBfParam {
 
 struct LaunchPlan {
     WsParam ws;
-    FastBfParam fbf;
     PrescreenParam ps;
     NeedBfParam nbf;
     int need_ctas;            // persistent k_bilateral_need CTAs
     int fast_width;           // frame width (k_prescreen's block shape)
     int fast_front;           // certified fast bilateral + exact refinement (lk_fastpath.cu)
-    int fast_table;           // mask of tap pairs whose range factor comes from the smem table
-    int fast_tpc;             // fast-bilateral tiles per CTA (LK_BF_TPC)
     int refine_ctas, decide_ctas;  // per-frame grids of k_refine_exact / k_sobel_decide
     int32_t* vhistT;          // [B][D1][H] transposed v-disparity for the v-path DP
     size_t vdisp_smem;        // k_vdisparity: barrier + histogram rows + staged bytes

@@ -2,10 +2,11 @@
 # Regenerates the measurement artefacts of a round on a B200 (run under gpurun):
 #   bench lines (KITTI batch, hires, stereo pairs, the reference arm), the
 #   per-kernel launch list of device-resident replays in the product
-#   configuration (gpu__time_duration; cold and serialised by ncu), and ncu
-#   --set full captures of the two largest kernels. Outputs land in
-#   gpurun_out/; summaries are copied to profiles/ (tools/launch_summary.py,
-#   tools/ncu_summary.py, tools/ncu_lines.py).
+#   configuration (gpu__time_duration; cold and serialised by ncu), a single-
+#   range launch list with DRAM bytes (tools/traffic_json.py -> profiles/
+#   traffic.json), and ncu --set full captures of the front-end kernels, K1 and
+#   the vote accumulation. Outputs land in gpurun_out/; summaries are copied to
+#   profiles/ (tools/launch_summary.py, tools/ncu_summary.py, tools/ncu_lines.py).
 set -u
 OUT=${OUT:-gpurun_out}
 mkdir -p "$OUT"
@@ -18,11 +19,14 @@ python bench.py --impl reference --steps 3 --warmup 1 > "$OUT/bench_ref.json" 2>
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
     --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
     > "$OUT/ncu_launches.log" 2>&1
-LK_BRANCHES=1 LK_H2D_CHUNKS=1 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
-    --log-file "$OUT/launches_single_range.csv" python tools/kernel_times.py kitti 3 \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -c 200 --csv --log-file "$OUT/launches_single_range.csv" python tools/kernel_times.py kitti 3 \
     > "$OUT/ncu_launches_sr.log" 2>&1
-for k in k_bilateral_fast k_refine_exact k_sobel_screen; do
-    LK_BRANCHES=1 LK_H2D_CHUNKS=1 ncu --set full --clock-control none --import-source on -k "regex:$k" -s 2 -c 1 \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -c 200 --csv --log-file "$OUT/launches_hires_single_range.csv" python tools/kernel_times.py hires 3 \
+    > "$OUT/ncu_launches_hires.log" 2>&1
+for k in ${KERNELS:-k_prescreen k_bilateral_need k_sobel_screen k_refine_exact k_vdisparity k_vanish k_edge_emit_tiles}; do
+    ncu --set full --clock-control none --import-source on -k "regex:$k" -s 2 -c 1 \
         -o "$OUT/${k}_full" -f python tools/kernel_times.py kitti 2 \
         > "$OUT/ncu_${k}.log" 2>&1
 done
