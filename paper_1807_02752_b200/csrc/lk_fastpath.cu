@@ -376,7 +376,10 @@ __device__ __forceinline__ void pq_bytes(const uint8_t* row, int q, int W, bool 
     } else {
         uint32_t b[14];
 #pragma unroll
-        for (int i = 0; i < 14; ++i) b[i] = __ldg(row + mirror(4 * q - 5 + i, W));
+        for (int i = 0; i < 14; ++i) {  // one reflection suffices: overhang < 160 <= W
+            const int x = 4 * q - 5 + i;
+            b[i] = __ldg(row + (W >= 160 ? (x < 0 ? -x - 1 : x >= W ? 2 * W - 1 - x : x) : mirror(x, W)));
+        }
         t0 = b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24;
         t1 = b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24;
         t2 = b[8] | b[9] << 8 | b[10] << 16 | b[11] << 24;
@@ -456,18 +459,10 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
             S2[j] += sg * (int)(h[j] >> 12);
         }
     };
-    auto evalE = [&](int j) {  // E of column j with the centre byte of 5 rows ago
-        const int k = (int)pq_byte(cen[5], j);
-        const int M1 = S1[j] - 121 * k;
-        const int M2 = S2[j] - 2 * k * S1[j] + 121 * k * k;
-        const float m1 = fabsf((float)M1) * p.c1, m2 = (float)M2 * p.c2;
-        const float A2 = m2 * p.inv_wmin, km = p.kappa * A2;
-        const float sq = fmaf(10.f, m2, 0.025f);  // >= sqrt(m2) (AM-GM at 0.05)
-        const float A1 = fmaf(p.ew, sq, m1);
-        const float e = fmaf(km, A1, p.fmax * A2) * fmaf(2.f, km, 1.f);
-        // 1 / (1 - km) <= 1 + 2 km needs km <= 1/2
-        return km >= 0.5f ? 1e30f : fmaf(fmaf(p.ew, sq, e), 1.0001f, 1e-9f);
-    };
+    // E of column j (centre byte of 5 rows ago) is
+    //   ((kappa A2 A1 + fmax A2)(1 + 2 kappa A2) + ew sq) * 1.0001 + 1e-9,
+    //   A2 = m2 / w_min, A1 = m1 + ew sq, sq = 10 m2 + 0.025 >= sqrt(m2) (AM-GM at 0.05),
+    // infinite when kappa A2 >= 1/2 (1 / (1 - km) <= 1 + 2 km needs km <= 1/2)
     const int e0 = max(t_lo - 1, 0);  // first E row
     for (int i = -5; i <= 5; ++i) {
         uint4 hp;
@@ -480,9 +475,31 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
     struct RowE {
         float2 v[4], l, r;
     };
+    // E of columns j0, j0 + 1 as one packed f32x2 evaluation (evalE's formula)
+    auto evalE2 = [&](int j0) {
+        const int k0 = (int)pq_byte(cen[5], j0), k1 = (int)pq_byte(cen[5], j0 + 1);
+        const float2 m1 = __fmul2_rn(make_float2((float)abs(S1[j0] - 121 * k0), (float)abs(S1[j0 + 1] - 121 * k1)),
+                                     make_float2(p.c1, p.c1));
+        const float2 m2 = __fmul2_rn(make_float2((float)(S2[j0] - 2 * k0 * S1[j0] + 121 * k0 * k0),
+                                                 (float)(S2[j0 + 1] - 2 * k1 * S1[j0 + 1] + 121 * k1 * k1)),
+                                     make_float2(p.c2, p.c2));
+        const float2 A2 = __fmul2_rn(m2, make_float2(p.inv_wmin, p.inv_wmin));
+        const float2 km = __fmul2_rn(A2, make_float2(p.kappa, p.kappa));
+        const float2 sq = __ffma2_rn(m2, make_float2(10.f, 10.f), make_float2(0.025f, 0.025f));
+        const float2 ew = make_float2(p.ew, p.ew);
+        const float2 A1 = __ffma2_rn(ew, sq, m1);
+        const float2 e = __fmul2_rn(__ffma2_rn(km, A1, __fmul2_rn(make_float2(p.fmax, p.fmax), A2)),
+                                    __ffma2_rn(make_float2(2.f, 2.f), km, make_float2(1.f, 1.f)));
+        const float2 r = __ffma2_rn(__ffma2_rn(ew, sq, e), make_float2(1.0001f, 1.0001f),
+                                    make_float2(1e-9f, 1e-9f));
+        return make_float2(km.x >= 0.5f ? 1e30f : r.x, km.y >= 0.5f ? 1e30f : r.y);
+    };
     auto make_row = [&](RowE& C) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) C.v[j] = make_float2((float)S1[j], evalE(j));
+        const float2 e01 = evalE2(0), e23 = evalE2(2);
+        C.v[0] = make_float2((float)S1[0], e01.x);
+        C.v[1] = make_float2((float)S1[1], e01.y);
+        C.v[2] = make_float2((float)S1[2], e23.x);
+        C.v[3] = make_float2((float)S1[3], e23.y);
         C.l = make_float2(__shfl_up_sync(0xffffffffu, C.v[3].x, 1), __shfl_up_sync(0xffffffffu, C.v[3].y, 1));
         C.r = make_float2(__shfl_down_sync(0xffffffffu, C.v[0].x, 1), __shfl_down_sync(0xffffffffu, C.v[0].y, 1));
     };
@@ -505,25 +522,27 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
                 for (int j = 0; j < 4 && 4 * q + j < W; ++j) dw |= (uint32_t)dr[j] << (8 * j);
             }
         }
-        uint32_t nib = 0;
+        // every pixel of the quad is evaluated (no divergence); the road mask
+        // and the image edge gate the survivor bits
+        uint32_t nib = 0, mnib = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int dv = (int)pq_byte(dw, j);
-            if (outq && 4 * q + j < W && dv >= mr.x && dv <= mr.y) {
-                nmask += r >= pa && r < pb;
-                const float2 a0 = j ? A.v[j - 1] : A.l, a1 = A.v[j], a2 = j < 3 ? A.v[j + 1] : A.r;
-                const float2 b0 = j ? B.v[j - 1] : B.l, b2 = j < 3 ? B.v[j + 1] : B.r;
-                const float2 c0 = j ? C.v[j - 1] : C.l, c1 = C.v[j], c2 = j < 3 ? C.v[j + 1] : C.r;
-                // (gx, ex): x = right - left, y = right + left; rows weighted 1, 2, 1
-                const float2 hx = __fadd2_rn(__ffma2_rn(__ffma2_rn(b0, np, b2), two, __ffma2_rn(a0, np, a2)),
-                                             __ffma2_rn(c0, np, c2));
-                // (gy, ey): x = bottom - top, y = bottom + top; columns weighted 1, 2, 1
-                const float2 hy = __fadd2_rn(__ffma2_rn(__ffma2_rn(a1, np, c1), two, __ffma2_rn(a0, np, c0)),
-                                             __ffma2_rn(a2, np, c2));
-                const float tx = fmaf(fabsf(hx.x), p.c1, hx.y), ty = fmaf(fabsf(hy.x), p.c1, hy.y);
-                if (fmaf(tx, tx, ty * ty) * 1.00001f >= p.s_star_lo) nib |= 1u << j;
-            }
+            const bool m = outq && 4 * q + j < W && dv >= mr.x && dv <= mr.y;
+            const float2 a0 = j ? A.v[j - 1] : A.l, a1 = A.v[j], a2 = j < 3 ? A.v[j + 1] : A.r;
+            const float2 b0 = j ? B.v[j - 1] : B.l, b2 = j < 3 ? B.v[j + 1] : B.r;
+            const float2 c0 = j ? C.v[j - 1] : C.l, c1 = C.v[j], c2 = j < 3 ? C.v[j + 1] : C.r;
+            // (gx, ex): x = right - left, y = right + left; rows weighted 1, 2, 1
+            const float2 hx = __fadd2_rn(__ffma2_rn(__ffma2_rn(b0, np, b2), two, __ffma2_rn(a0, np, a2)),
+                                         __ffma2_rn(c0, np, c2));
+            // (gy, ey): x = bottom - top, y = bottom + top; columns weighted 1, 2, 1
+            const float2 hy = __fadd2_rn(__ffma2_rn(__ffma2_rn(a1, np, c1), two, __ffma2_rn(a0, np, c0)),
+                                         __ffma2_rn(a2, np, c2));
+            const float tx = fmaf(fabsf(hx.x), p.c1, hx.y), ty = fmaf(fabsf(hy.x), p.c1, hy.y);
+            mnib |= (uint32_t)m << j;
+            nib |= (uint32_t)(m && fmaf(tx, tx, ty * ty) * 1.00001f >= p.s_star_lo) << j;
         }
+        if (r >= pa && r < pb) nmask += __popc(mnib);
         // OR the nibbles of each 32-column word into the shared row bitmap
         const int wd = outq ? (4 * q) >> 5 : -1;
         const unsigned grp = __match_any_sync(0xffffffffu, wd);
@@ -648,13 +667,40 @@ __global__ void __launch_bounds__(256) k_bilateral_need(Dev d, NeedBfParam p, in
     const unsigned T = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + tid;
     const unsigned tb = (unsigned)__cvta_generic_to_shared(s_T) + 8u * (lane & 15);
     const int W = d.W, H = d.H;
-    unsigned base = 0;  // first flattened index of frame f
-    for (int f = 0; f < n; ++f) {
-        const unsigned cnt = all ? (frame_failed(d, f) ? 0u : (unsigned)d.px)
-                                 : (frame_failed(d, f) ? 0u : d.aux[f].fneed);
-        const uint8_t* g = d.grey + (size_t)f * d.px;
-        const uint32_t* list = d.fneed + (size_t)f * d.px;
-        for (unsigned i = (t + T - base % T) % T; i < cnt; i += T) {
+    // the frames' lists flattened: prefix sums of their lengths, NC frames at a time
+    constexpr int NC = 1024;
+    __shared__ unsigned s_pre[NC + 1];
+    for (int f0 = 0; f0 < n; f0 += NC) {
+        const int nc = min(NC, n - f0);
+        __syncthreads();  // the previous chunk's prefix array is no longer read
+        if (tid < 32) {   // one warp scans the chunk's counts
+            unsigned carry = 0;
+            for (int c0 = 0; c0 < nc; c0 += 32) {
+                const int f = f0 + c0 + lane;
+                unsigned x = 0;
+                if (c0 + lane < nc)
+                    x = frame_failed(d, f) ? 0u : all ? (unsigned)d.px : d.aux[f].fneed;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (c0 + lane < nc) s_pre[c0 + lane + 1] = carry + x;
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+            if (lane == 0) s_pre[0] = 0;
+        }
+        __syncthreads();
+        const unsigned total = s_pre[nc];
+        for (unsigned gi = t; gi < total; gi += T) {
+            int lo = 0, hi = nc;  // frame: s_pre[lo] <= gi < s_pre[lo + 1]
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= gi) lo = mid; else hi = mid;
+            }
+            const int f = f0 + lo;
+            const unsigned i = gi - s_pre[lo];
+            const uint8_t* g = d.grey + (size_t)f * d.px;
+            const uint32_t* list = d.fneed + (size_t)f * d.px;
             int u, v;
             if (all) {
                 v = (int)(i / (unsigned)W);
@@ -695,7 +741,6 @@ __global__ void __launch_bounds__(256) k_bilateral_need(Dev d, NeedBfParam p, in
             d.smoothed_f[(size_t)f * d.px + (size_t)v * W + u] =
                 ((float)kp + __fdiv_rn(num, den)) * (1.f / 255.f);
         }
-        base += cnt;
     }
 }
 
