@@ -546,6 +546,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     }
     cudaError_t e = lkg::configure_kernels(lp);
     lp.need_ctas = lkg::need_bilateral_ctas(prop.multiProcessorCount);
+    if (const char* nc = std::getenv("LK_NEED_CTAS")) lp.need_ctas = std::max(1, std::atoi(nc));
     if (e == cudaSuccess && d.stereo) {
         if (lkg::stereo_smem(d) > smem_cap) {
             lk_destroy(c);

@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(256) k_bilateral_need(Dev d, NeedBfParam p, in
     const unsigned tb = (unsigned)__cvta_generic_to_shared(s_T) + 8u * (lane & 15);
     const int W = d.W, H = d.H;
     // the frames' lists flattened: prefix sums of their lengths, NC frames at a time
-    constexpr int NC = 1024;
+    constexpr int NC = 64;
     __shared__ unsigned s_pre[NC + 1];
     for (int f0 = 0; f0 < n; f0 += NC) {
         const int nc = min(NC, n - f0);
