@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--config", default="kitti", choices=["kitti", "hires"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stream", type=int, default=0, metavar="N",
+                    help="BASELINE config 5: a stream of N KITTI-size frames sharded over the "
+                         "ranks (each cycles a resident 256-frame pool over its shard); lane "
+                         "records gathered on rank 0 inside the timed region")
     ap.add_argument("--stereo", action="store_true",
                     help="stereo pairs in: stages 1-12 (the reference's run_pipeline) instead "
                          "of the north-star path (stages 5-12 on a given disparity)")
@@ -260,7 +264,12 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("gloo")
+    local = local % max(1, torch.cuda.device_count())  # ranks may share a GPU (tests)
     torch.cuda.set_device(local)
+    from paper_1807_02752_b200 import shard as _shard
+
+    all_cpus = os.sched_getaffinity(0)
+    _shard.bind_local_cpus(local)  # pinned host buffers below NUMA-local to the GPU
     scene_fn, cfg, W, H, B, desc = workload(args.config, args.batch)
     pool = args.pool or B
     stereo = args.stereo
@@ -468,6 +477,7 @@ def run_ours(args):
         except Exception:
             pass
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.sched_setaffinity(0, all_cpus)  # the CPU baseline gets every host core
         cb, ref_reps = cpu_baseline(grey, disp, cfg, frames=2 * (os.cpu_count() or 8),
                                     stereo=stereo)
         line["cpu_baseline"] = cb
@@ -490,10 +500,146 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+class GpuStreamEngine:
+    """Config-5 engine on one GPU: a resident pool of B distinct frames, batches
+    queued with lk_submit_resident (kernels + asynchronous report read-back),
+    two pinned report buffers so batch k's records are consumed while batch
+    k+1 runs."""
+
+    def __init__(self, B: int, device: int, seed0: int):
+        import torch
+
+        from paper_1807_02752_b200 import abi, lanekit, scenes
+
+        self.torch, self.abi = torch, abi
+        self.B = B
+        grey, disp = make_frames(scenes.batch_scene, B, B, seed0)
+        H, W = grey.shape[1:]
+        self.pipe = lanekit.GpuPipeline(W, H, abi.default_config(), max_batch=B, device=device)
+        self.L = lanekit.library()
+        h = self.h = self.pipe._h
+        reps = (abi.LkFrameReport * B)()
+        st = self.L.lk_run_batch(h, grey.ctypes.data, disp.ctypes.data, B, abi.LK_MEM_HOST, reps)
+        if st not in (abi.LK_OK, abi.LK_ERR_FRAME):  # the pool is now resident in HBM
+            raise RuntimeError(self.L.lk_last_error().decode())
+        self.rbufs = []
+        for _ in range(2):
+            rp = C.c_void_p()
+            self.L.lk_host_alloc(C.byref(rp), B * C.sizeof(abi.LkFrameReport))
+            self.rbufs.append(C.cast(rp, C.POINTER(abi.LkFrameReport * B)).contents)
+        self.stream = torch.cuda.ExternalStream(self.L.lk_stream(h), device=device)
+        self.pending = []
+
+    def submit(self, k: int, n: int):
+        if self.L.lk_submit_resident(self.h, n, self.rbufs[k % 2]) != self.abi.LK_OK:
+            raise RuntimeError(self.L.lk_last_error().decode())
+        self.pending.append((k, n))
+
+    def wait(self, frame0: int):
+        from paper_1807_02752_b200 import shard
+
+        k, n = self.pending.pop(0)
+        if self.L.lk_wait_batch(self.h) not in (self.abi.LK_OK, self.abi.LK_ERR_FRAME):
+            raise RuntimeError(self.L.lk_last_error().decode())
+        return shard.compact_records(self.rbufs[k % 2], frame0, n)
+
+    def event(self):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        return e
+
+    def elapsed_ms(self, e0, e1) -> float:
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
+    def close(self):
+        for rb in self.rbufs:
+            self.L.lk_host_free(C.cast(C.pointer(rb), C.c_void_p))
+        self.pipe.close()
+
+
+def run_stream(args, engine_factory=None, emit=print):
+    """BASELINE config 5: N frames sharded over the ranks (contiguous frame
+    ranges, shard.shard_range); each rank streams its shard through its own
+    engine in batches of B (a resident pool of B distinct frames cycled) and
+    the compact lane records are host-gathered on rank 0 (gloo). Timed per rank
+    from a barrier to the end of the gather on the engine's device clock; the
+    slowest rank sets the time. Returns rank 0's JSON line (None elsewhere)."""
+    from paper_1807_02752_b200 import shard
+
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            dist.init_process_group("gloo")
+    N, B = args.stream, args.batch or 256
+    lo, hi = shard.shard_range(N, rank, world)
+    if engine_factory is None:
+        import torch
+
+        device = local % max(1, torch.cuda.device_count())  # ranks may share a GPU
+        torch.cuda.set_device(device)
+        cpus = shard.bind_local_cpus(device)  # NUMA-local pinned buffers
+        engine = GpuStreamEngine(B, device, 1 + lo)
+    else:
+        cpus, engine = None, engine_factory(B, 1 + lo)
+    batches = [(f0, min(B, hi - f0)) for f0 in range(lo, hi, B)]
+    for k in range(min(3, len(batches))):  # warm-up (graphs of the batch sizes captured)
+        engine.submit(k, batches[k][1])
+        engine.wait(0)
+    if dist:
+        dist.barrier()
+    e0 = engine.event()
+    recs = []
+    for k, (f0, n) in enumerate(batches):
+        engine.submit(k, n)
+        if k >= 1:
+            recs.append(engine.wait(batches[k - 1][0]))
+    if batches:
+        recs.append(engine.wait(batches[-1][0]))
+    local_recs = np.concatenate(recs) if recs else np.zeros(0, shard.RECORD_DTYPE)
+    gathered = shard.gather_records(local_recs)
+    e1 = engine.event()
+    ms = engine.elapsed_ms(e0, e1)
+    (ms,) = shard.max_over_ranks([ms])
+    failed = int((local_recs["status"] != 0).sum())
+    (failed,) = shard.sum_over_ranks([failed])
+    engine.close()
+    line = None
+    if rank == 0:
+        ok = gathered is not None and len(gathered) == N and bool(
+            np.array_equal(gathered["frame"], np.arange(N, dtype=np.uint32)))
+        line = {
+            "metric": METRIC, "value": N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": len(batches), "warmup": min(3, len(batches)),
+            "ms_per_step": ms / max(1, len(batches)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config 5: stream of {N} synthetic KITTI-size 1242x375 "
+                                   f"frames sharded over {world} rank(s), batches of {B} from a "
+                                   f"resident pool of {B} distinct frames per rank; compact lane "
+                                   f"records gathered on rank 0 inside the timed region",
+                       "frames": N, "batch": B, "parallelism": f"frame-sharded x{world}",
+                       "numa_cpus_rank0": f"{cpus[0]}-{cpus[-1]}" if cpus else None},
+            "timing": "per rank: device events on the library stream from a barrier to after "
+                      "the gather; max over ranks",
+            "records": {"gathered": None if gathered is None else int(len(gathered)),
+                        "in_frame_order": ok, "bytes_each": shard.RECORD_DTYPE.itemsize},
+            "failed_frames": failed,
+        }
+        emit(json.dumps(line))
+    if dist:
+        dist.barrier()
+    return line
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.stream:
+        run_stream(args)
     else:
         run_ours(args)
 

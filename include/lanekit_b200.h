@@ -255,6 +255,11 @@ lk_status lk_submit_batch(lk_ctx* ctx, const uint8_t* grey, const uint8_t* dispa
  * [n][H][W] in, stages 1-12 (run_pipeline, pipeline.hpp:118-270) per batch. */
 lk_status lk_submit_stereo_batch(lk_ctx* ctx, const uint8_t* left, const uint8_t* right, int n,
                                  lk_frame_report* reports);
+/* Device-resident stream (BASELINE config 5): the pipeline over the frames
+ * already in the input buffers (lk_device_inputs), and the asynchronous
+ * read-back of their n reports into `reports` (pinned; may be NULL), queued
+ * like lk_submit_batch (at most two in flight; lk_wait_batch). */
+lk_status lk_submit_resident(lk_ctx* ctx, int n, lk_frame_report* reports);
 lk_status lk_wait_batch(lk_ctx* ctx);
 lk_status lk_fetch_reports(lk_ctx* ctx, lk_frame_report* reports, int n);
 lk_status lk_synchronize(lk_ctx* ctx);

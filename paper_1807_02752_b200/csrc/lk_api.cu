@@ -906,6 +906,50 @@ lk_status lk_wait_batch(lk_ctx* c) {
     return any ? LK_ERR_FRAME : LK_OK;
 }
 
+// First streaming use: the second input slot, the copy stream, slot events.
+static lk_status ensure_streaming(lk_ctx* c) {
+    if (c->copy_stream) return LK_OK;
+    if (lk_status s = c->alloc(&c->slot_grey[1], (size_t)c->max_batch * c->d.px + 16)) return s;
+    if (lk_status s = c->alloc(&c->slot_disp[1], (size_t)c->max_batch * c->d.px + 16)) return s;
+    c->slot_grey[0] = c->in_grey;
+    c->slot_disp[0] = c->in_disp;
+    CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        CU(cudaEventCreateWithFlags(&c->slot_copied[k], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->slot_free[k], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->slot_done[k], cudaEventDisableTiming));
+        CU(cudaEventRecord(c->slot_free[k], c->stream));
+    }
+    return LK_OK;
+}
+
+// Device-resident stream (BASELINE config 5): the pipeline over the frames
+// already in the input buffers (lk_device_inputs) plus the asynchronous
+// read-back of their reports, queued like lk_submit_batch (lk_wait_batch).
+// Batch k+1's kernels follow batch k's report copy on the context stream, so
+// the host consumes batch k's records while batch k+1 runs.
+lk_status lk_submit_resident(lk_ctx* c, int n, lk_frame_report* reports) {
+    if (!c) return fail(LK_ERR_INVALID_ARGUMENT, "null context");
+    if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
+    CU(cudaSetDevice(c->device));
+    if (lk_status s = ensure_streaming(c)) return s;
+    if (c->n_pending == 2) {  // at most two batches in flight
+        const lk_status s = lk_wait_batch(c);
+        if (s != LK_OK && s != LK_ERR_FRAME) return s;
+    }
+    const int sl = c->next_slot;  // completion-event slot (the inputs stay in slot 0)
+    c->next_slot ^= 1;
+    c->slot = 0;
+    c->run_stereo = false;
+    if (lk_status s = enqueue_mode(c, n)) return s;
+    if (reports)
+        CU(cudaMemcpyAsync(reports, c->d.rep, (size_t)n * sizeof(lk_frame_report),
+                           cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaEventRecord(c->slot_done[sl], c->stream));
+    c->pending[c->n_pending++] = {sl, n, reports};
+    return LK_OK;
+}
+
 // Streaming submit shared by the mono (grey + disparity) and stereo (left +
 // right) entry points: the copy goes to one of two input slots on the copy
 // stream, the kernels wait for it, and the next submit's copy overlaps them.
@@ -916,19 +960,7 @@ static lk_status submit(lk_ctx* c, const uint8_t* a, const uint8_t* b, int n,
         return fail(LK_ERR_INVALID_ARGUMENT, "context was created without LK_FLAG_STEREO");
     if (n < 1 || n > c->max_batch) return fail(LK_ERR_INVALID_ARGUMENT, "batch size out of range");
     CU(cudaSetDevice(c->device));
-    if (!c->copy_stream) {  // first use: the second input slot and the copy stream
-        if (lk_status s = c->alloc(&c->slot_grey[1], (size_t)c->max_batch * c->d.px + 16)) return s;
-        if (lk_status s = c->alloc(&c->slot_disp[1], (size_t)c->max_batch * c->d.px + 16)) return s;
-        c->slot_grey[0] = c->in_grey;
-        c->slot_disp[0] = c->in_disp;
-        CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-        for (int k = 0; k < 2; ++k) {
-            CU(cudaEventCreateWithFlags(&c->slot_copied[k], cudaEventDisableTiming));
-            CU(cudaEventCreateWithFlags(&c->slot_free[k], cudaEventDisableTiming));
-            CU(cudaEventCreateWithFlags(&c->slot_done[k], cudaEventDisableTiming));
-            CU(cudaEventRecord(c->slot_free[k], c->stream));
-        }
-    }
+    if (lk_status s = ensure_streaming(c)) return s;
     if (stereo && !c->slot_right[0]) {
         if (lk_status s = c->alloc(&c->slot_right[1], (size_t)c->max_batch * c->d.px)) return s;
         c->slot_right[0] = c->in_right;

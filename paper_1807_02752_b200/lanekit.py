@@ -51,6 +51,7 @@ def library() -> C.CDLL:
     L.lk_device_inputs.argtypes = [P, C.POINTER(P), C.POINTER(P)]
     L.lk_enqueue.argtypes = [P, I]
     L.lk_submit_batch.argtypes = [P, P, P, I, repp]
+    L.lk_submit_resident.argtypes = [P, I, repp]
     L.lk_submit_stereo_batch.argtypes = [P, P, P, I, repp]
     L.lk_wait_batch.argtypes = [P]
     L.lk_fetch_reports.argtypes = [P, repp, I]

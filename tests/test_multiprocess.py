@@ -72,3 +72,72 @@ def test_two_rank_gloo_shards_match_single_process(tmp_path):
     assert json.loads(json.dumps(want)) == got["records"]
     assert got["t"] == [2.0, 20.0]      # max over ranks
     assert got["f"] == [0, n]           # failures summed, frames summed
+
+
+class _CpuStreamEngine:
+    """bench.run_stream's engine contract on CPU: the oracle (test infrastructure)
+    stands in for the GPU; a pool of B acceptance-size frames cycled."""
+
+    def __init__(self, B, seed0):
+        import time
+
+        from checkers import Checker
+        from paper_1807_02752_b200 import lanekit, scenes
+
+        self.time = time
+        self.grey, self.disp = lanekit.synth_batch(
+            [scenes.acceptance_scene(seed0 + i) for i in range(B)], threads=2)
+        self.chk, self.cfg, self.pending = Checker("oracle"), scenes.acceptance_config(), []
+
+    def submit(self, k, n):
+        self.pending.append(n)
+
+    def wait(self, frame0):
+        import ctypes as C
+
+        from paper_1807_02752_b200 import abi, shard
+
+        n = self.pending.pop(0)
+        reps = self.chk.run_batch(self.grey[:n], self.disp[:n], self.cfg, threads=2)
+        arr = (abi.LkFrameReport * n)(*reps)
+        return shard.compact_records(arr, frame0)
+
+    def event(self):
+        return self.time.perf_counter()
+
+    def elapsed_ms(self, e0, e1):
+        return (e1 - e0) * 1e3
+
+    def close(self):
+        pass
+
+
+def _stream_worker(rank, world, port, out_path):
+    sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import argparse
+    import json
+
+    import bench
+
+    args = argparse.Namespace(stream=10, batch=4)
+    line = bench.run_stream(args, engine_factory=_CpuStreamEngine, emit=lambda s: None)
+    if rank == 0:
+        Path(out_path).write_text(json.dumps(line))
+
+
+def test_bench_stream_two_ranks_gather(tmp_path):
+    """bench.py --stream under two gloo ranks: shards [0, 5) and [5, 10), batches of
+    4 (+1), the compact lane records gathered on rank 0 in frame order, the slowest
+    rank's time, one JSON line on rank 0 only."""
+    import json
+
+    out = tmp_path / "line.json"
+    mp.spawn(_stream_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True)
+    line = json.loads(out.read_text())
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["records"] == {"gathered": 10, "in_frame_order": True,
+                               "bytes_each": line["records"]["bytes_each"]}
+    assert line["failed_frames"] == 0 and line["value"] > 0
+    assert line["config"]["frames"] == 10 and line["steps"] == 2
