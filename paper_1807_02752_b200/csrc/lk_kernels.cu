@@ -452,11 +452,8 @@ __global__ void __launch_bounds__(128) k_road_fit(Dev d) {
     __syncthreads();
     block_ransac<3, NW>(px, pv, n, d.tr_y, d.eps_y, d.max_iter, d.rng, bufs, tbuf, st);
     lk_frame_report& rep = d.rep[f];
-    if (st.msg) {
-        if (threadIdx.x == 0) {
-            rep.beta_iterations = st.iterations;
-            fail_frame(d, f, 7, st.msg);
-        }
+    if (st.msg) {  // ransac_trim threw: the report keeps its defaults (pipeline.hpp:199-207)
+        if (threadIdx.x == 0) fail_frame(d, f, 7, st.msg);
         return;
     }
     const double b0 = st.model[0], b1 = st.model[1], b2 = st.model[2];
@@ -1346,11 +1343,8 @@ __global__ void __launch_bounds__(32 * GAMMA_NW, 2) k_gamma_fit(Dev d) {
 #ifdef LK_GAMMA_PROF
     const long long t1 = clock64();
 #endif
-    if (st.msg) {
-        if (threadIdx.x == 0) {
-            rep.gamma_iterations = st.iterations;
-            fail_frame(d, f, 11, st.msg);
-        }
+    if (st.msg) {  // ransac_trim threw: the report keeps its defaults (pipeline.hpp:245-251)
+        if (threadIdx.x == 0) fail_frame(d, f, 11, st.msg);
         return;
     }
     const double g0 = st.model[0], g1 = st.model[1], g2 = st.model[2], g3 = st.model[3],

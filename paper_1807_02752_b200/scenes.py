@@ -50,12 +50,27 @@ def stress_scene(i: int) -> abi.LkSceneParams:
 
 
 def hires_scene(i: int) -> abi.LkSceneParams:
-    """Config 4: 2560x1024 (SURVEY.md §7 hard part 7: beta below, d_max 248, lambda_g 1)."""
-    return batch_scene(i, HIRES_W, HIRES_H, beta=BETA, d_max=256)
+    """Config 4: 2560x1024 (SURVEY.md §7 hard part 7: beta below, d_max 248). The
+    acceptance pattern's lane bottoms scale with W/320; the lane curvature is
+    scaled to the taller frame (gamma2 by (W/320) / (H/240)^2, gamma1 = 0), so
+    the reference itself finds the painted lanes (batch_scene's KITTI curvature
+    at 1024 rows bends the lanes off the frame and the reference then selects
+    16+ spurious lanes)."""
+    W, H = HIRES_W, HIRES_H
+    s, sv = W / 320.0, H / 240.0
+    nl = 2 + i % 3
+    start = (60.0 + (i % 4) * 8.0) * s
+    span = 250.0 * s - start
+    bottoms = tuple(start + span * k / (nl - 1) for k in range(nl))
+    gamma = (W / 2 + ((i % 5) - 2) * 12.0 * s, 0.0, ((i % 4) - 1.5) * 5e-4 * s / (sv * sv), 0.0, 0.0)
+    return abi.scene_params(width=W, height=H, beta=BETA, gamma=gamma, d_max=256,
+                            lane_bottoms=bottoms, noise_sigma=0.02, rng_seed=1 + i)
 
 
 def hires_config() -> abi.LkConfig:
-    return abi.default_config(d_max=248, lambda_g=1.0)
+    """d_max 248 (f(1023) = 242), lambda_g 1, and a lane separation scaled to the
+    frame width (150 px; the default 20 px lets one painted lane yield several)."""
+    return abi.default_config(d_max=248, lambda_g=1.0, min_lane_sep=150)
 
 
 def acceptance_scene(i: int) -> abi.LkSceneParams:

@@ -26,6 +26,7 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
 
 from checkers import Checker  # noqa: E402
+from golden_util import apply_mutation  # noqa: E402
 
 from paper_1807_02752_b200 import abi, scenes  # noqa: E402
 
@@ -72,11 +73,19 @@ def cases():
     yield ("acceptance_2_window7_rho_vote2", scenes.acceptance_scene(2),
            abi.default_config(d_max=32, bf_window=7, rho_vote=2.0, lambda_x=3.5, varsigma=2,
                               min_lane_sep=8), None)
-    yield "hires_0", scenes.hires_scene(0), scenes.hires_config(), None
+    yield "hires_5", scenes.hires_scene(5), scenes.hires_config(), None
     yield "fail_stage6_no_disparity", scenes.acceptance_scene(3), scenes.acceptance_config(), \
         "zero_disparity"
     yield "fail_stage11_flat_grey", scenes.acceptance_scene(4), scenes.acceptance_config(), \
         "flat_grey"
+    # stage 7 (ransac.hpp:41-42): d_max 1 leaves 2 v-path points for a 3-point sample
+    yield "fail_stage7_few_points", scenes.acceptance_scene(0), \
+        abi.default_config(d_max=1, rho=4, sigma_floor=0.03, tr_lrc=1, nu=2, lambda_g=1.03), \
+        "disparity_one_below_120"
+    # stage 7 (ransac.hpp:90): all road evidence in one row -> every sample's
+    # parabola fit lacks three distinct rows
+    yield "fail_stage7_no_fit", scenes.acceptance_scene(0), scenes.acceptance_config(), \
+        "disparity_row150_d10"
 
 
 def main():
@@ -94,10 +103,7 @@ def main():
         else:
             grey, _, disp, _ = ref.gen_scene(p)
             source = "reference gen_scene"
-        if mutate == "zero_disparity":
-            disp[:] = 0
-        elif mutate == "flat_grey":
-            grey[:] = 128
+        apply_mutation(mutate, grey, disp)
         r = ref.run(grey, disp, cfg)
         case = {"name": name, "scene": params_dict(p), "config": config_dict(cfg),
                 "mutate": mutate, "inputs": source, "grey_sha256": sha(grey.tobytes()),
@@ -107,6 +113,9 @@ def main():
         if r.report.status == 0:
             for hook in abi.STAGES:
                 raw = r.raw(abi.STAGE[hook])
+                if not raw and hook in ("STATS_MU", "STATS_SIGMA", "DISP_LEFT", "DISP_RIGHT",
+                                        "DISPARITY"):
+                    continue  # stage 1-4 hooks: the disparity is injected here
                 arr = r.get(hook)
                 h = {"sha256": sha(raw), "shape": list(arr.shape), "nbytes": len(raw)}
                 if hook in SMALL_HOOKS:

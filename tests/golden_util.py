@@ -62,6 +62,22 @@ def config(case) -> abi.LkConfig:
     return c
 
 
+def apply_mutation(mutate, grey, disp):
+    """The failure cases' input edits (in place), shared with make_golden.py."""
+    if mutate == "zero_disparity":
+        disp[:] = 0
+    elif mutate == "flat_grey":
+        grey[:] = 128
+    elif mutate == "disparity_one_below_120":
+        disp[:] = 0
+        disp[120:] = 1
+    elif mutate == "disparity_row150_d10":
+        disp[:] = 0
+        disp[150, :] = 10
+    elif mutate is not None:
+        raise ValueError(f"unknown mutation {mutate}")
+
+
 def inputs(case):
     """Regenerates the case's grey / disparity with the repo generator and
     checks them against the reference's bytes (SHA-256)."""
@@ -69,10 +85,7 @@ def inputs(case):
 
     p = scene_params(case)
     grey, _, disp, _ = lanekit.synth_scene(p)
-    if case["mutate"] == "zero_disparity":
-        disp[:] = 0
-    elif case["mutate"] == "flat_grey":
-        grey[:] = 128
+    apply_mutation(case["mutate"], grey, disp)
     assert sha(grey.tobytes()) == case["grey_sha256"], "generator drifted (grey)"
     assert sha(disp.tobytes()) == case["disp_sha256"], "generator drifted (disparity)"
     return grey, disp

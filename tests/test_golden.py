@@ -35,8 +35,13 @@ def test_oracle_matches_reference_golden(oracle, name):
 
 def test_golden_covers_failures_and_configs():
     names = set(CASES)
-    assert {"fail_stage6_no_disparity", "fail_stage11_flat_grey", "hires_0",
-            "batch_92_gamma181"} <= names
+    assert {"fail_stage6_no_disparity", "fail_stage11_flat_grey", "hires_5",
+            "batch_92_gamma181", "fail_stage7_few_points", "fail_stage7_no_fit"} <= names
     assert CASES["fail_stage6_no_disparity"]["report"]["failed_stage"] == 6
     assert CASES["fail_stage11_flat_grey"]["report"]["failed_stage"] == 11
+    assert CASES["fail_stage7_few_points"]["report"]["failed_stage"] == 7
+    assert CASES["fail_stage7_no_fit"]["report"]["failed_stage"] == 7
+    assert CASES["fail_stage7_few_points"]["report"]["msg"] != CASES["fail_stage7_no_fit"]["report"]["msg"]
+    # the hi-res case is a lane scene: the reference finds the 4 painted lanes
+    assert CASES["hires_5"]["report"]["lane_count"] == 4
     assert CASES["probe_kitti"]["report"]["lane_bottom_col"] == [767, 370]  # SURVEY.md §6 probe
