@@ -102,6 +102,61 @@ def ref_frames(chk, scene_fn, n: int, seed0: int):
     return np.ascontiguousarray(np.stack(gs)), np.ascontiguousarray(np.stack(ds))
 
 
+def drop_in_measurements(grey, disp, cfg, device: int, hooks_steps: int = 5, calls: int = 200):
+    """The reference is called one frame at a time (pipeline.hpp:118): the
+    drop-in's batch-1 latency with the context reused (frame in from pinned
+    host memory, report out, lk_run_batch n = 1; host wall clock per call), and
+    the hooks-mode throughput (LK_FLAG_HOOKS: the exact path with every
+    PipelineResult member materialised, as the reference always does)."""
+    import torch
+
+    from paper_1807_02752_b200 import abi, lanekit
+
+    B, H, W = grey.shape
+    out = {}
+    with lanekit.GpuPipeline(W, H, cfg, max_batch=1, device=device) as p:
+        L, h = lanekit.library(), p._h
+        hg, hd = C.c_void_p(), C.c_void_p()
+        L.lk_host_alloc(C.byref(hg), H * W)
+        L.lk_host_alloc(C.byref(hd), H * W)
+        rep = abi.LkFrameReport()
+        ts = []
+        for i in range(calls + 10):
+            C.memmove(hg, grey[i % B].ctypes.data, H * W)
+            C.memmove(hd, disp[i % B].ctypes.data, H * W)
+            t0 = time.perf_counter()
+            L.lk_run_batch(h, hg, hd, 1, abi.LK_MEM_HOST, C.byref(rep))
+            t1 = time.perf_counter()
+            if i >= 10:
+                ts.append((t1 - t0) * 1e3)
+        L.lk_host_free(hg)
+        L.lk_host_free(hd)
+        ts.sort()
+        out["batch1_latency_ms"] = {"median": ts[len(ts) // 2], "p99": ts[int(len(ts) * 0.99)],
+                                    "min": ts[0], "calls": calls,
+                                    "api": "lk_run_batch(n=1, LK_MEM_HOST) on a reused context: "
+                                           "H2D, the 22-kernel graph, report D2H, host wall clock"}
+    with lanekit.GpuPipeline(W, H, cfg, max_batch=B, device=device, hooks=True) as p:
+        L, h = lanekit.library(), p._h
+        reps = (abi.LkFrameReport * B)()
+        L.lk_run_batch(h, grey.ctypes.data, disp.ctypes.data, B, abi.LK_MEM_HOST, reps)
+        L.lk_enqueue(h, B)
+        L.lk_synchronize(h)
+        st = torch.cuda.ExternalStream(L.lk_stream(h), device=device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(hooks_steps):
+            L.lk_enqueue(h, B)
+        e1.record(st)
+        e1.synchronize()
+        out["hooks_mode"] = {"value": B * hooks_steps / (e0.elapsed_time(e1) * 1e-3),
+                             "unit": UNIT, "steps": hooks_steps,
+                             "note": "LK_FLAG_HOOKS: exact LUT bilateral on every pixel, MASK / "
+                                     "GX / GY / MAG / THETA / VPX_ACC / M0 / polylines "
+                                     "materialised; device-resident"}
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -233,6 +288,17 @@ def run_reference(args):
         chk.run_batch(grey, disp, cfg, threads=cores)
     dt = time.perf_counter() - t0
     fps = steps * per_step / dt
+    # the reference called one frame at a time (pipeline.hpp:118): latency with
+    # its own intra-frame threading off (threads = 1) and on (threads = nproc)
+    lat = {}
+    for th in (1, cores):
+        c1 = abi_default_copy(cfg, threads=th)
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            chk.run_batch(grey[:1], disp[:1], c1, threads=1)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        lat[f"threads_{th}"] = sorted(ts)[1]
     line = {
         # n_gpus mirrors the launch (--gpus N); the reference arm runs on rank 0's host cores
         "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": max(world, args.gpus),
@@ -248,6 +314,9 @@ def run_reference(args):
         "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": f"{steps} steps x {per_step} frames (one per thread)"},
         "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "single_frame_latency_ms": {**lat, "note": "one frame, median of 3; cfg.threads = the "
+                                                   "reference's intra-frame parallel_for (bilateral "
+                                                   "rows, lane energies)"},
     }
     if kind != "reference":
         line["note"] = "oracle/_ref missing: timed the repo's restatement instead"
@@ -477,6 +546,8 @@ def run_ours(args):
         except Exception:
             pass
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if not stereo and args.config == "kitti":
+            line["drop_in"] = drop_in_measurements(grey, disp, cfg, local)
         os.sched_setaffinity(0, all_cpus)  # the CPU baseline gets every host core
         cb, ref_reps = cpu_baseline(grey, disp, cfg, frames=2 * (os.cpu_count() or 8),
                                     stereo=stereo)
@@ -498,6 +569,16 @@ def run_ours(args):
     L.lk_host_free(hd)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def abi_default_copy(cfg, **overrides):
+    """A copy of an LkConfig with fields overridden."""
+    from paper_1807_02752_b200 import abi
+
+    c = abi.LkConfig.from_buffer_copy(cfg)
+    for k, v in overrides.items():
+        setattr(c, k, v)
+    return c
 
 
 class GpuStreamEngine:

@@ -107,20 +107,20 @@ struct Result {  // PipelineReport + lazily copied PipelineResult members
     std::vector<lk_lane> lanes() const { return stage<lk_lane>(LK_STAGE_LANES); }
 };
 
-// Stages 5-12 on one frame; `left` is a GrayImage-like (width, height,
-// data of k/255.0), `disparity` a DisparityMap-like (ints, 0 = invalid).
-template <typename Gray, typename Disp, typename Cfg>
-Result run_from_disparity(const Gray& left, const Disp& disparity, const Cfg& cfg,
-                          int device = 0) {
+namespace detail {
+template <typename Gray, typename Disp>
+void check_inputs(const Gray& left, const Disp& disparity) {
     if (left.width == 0 || left.height == 0 || disparity.width == 0 || disparity.height == 0)
         throw StageError(1, lk_stage_name(1), "stage 1 (block statistics): empty input image");
     if (left.width != disparity.width || left.height != disparity.height)
         throw StageError(1, lk_stage_name(1),
                          "stage 1 (block statistics): stereo pair dimensions differ");
-    const lk_config c = to_lk_config(cfg);
-    check(lk_validate_config(&c));
+}
+
+// k/255.0 grey -> u8 k (rejecting any other value), int disparity -> u8
+template <typename Gray, typename Disp>
+void to_u8(const Gray& left, const Disp& disparity, uint8_t* g, uint8_t* d) {
     const size_t n = static_cast<size_t>(left.width) * left.height;
-    std::vector<uint8_t> g(n), d(n);
     for (size_t i = 0; i < n; ++i) {
         const double x = left.data[i];
         const long k = std::lround(x * 255.0);
@@ -131,17 +131,72 @@ Result run_from_disparity(const Gray& left, const Disp& disparity, const Cfg& cf
         if (dv < 0 || dv > 255) throw Error("lanekit_gpu: disparity outside 0..255");
         d[i] = static_cast<uint8_t>(dv);
     }
-    Result r;
-    r.ctx = std::make_shared<Context>(left.width, left.height, c, 1, device);
-    const lk_status s = lk_run_batch(r.ctx->get(), g.data(), d.data(), 1, LK_MEM_HOST, &r.report);
-    if (s != LK_OK && s != LK_ERR_FRAME) check(s);
-    if (r.report.status != 0) {
+}
+
+inline void throw_if_failed(const lk_frame_report& rep) {
+    if (rep.status != 0) {
         char buf[256];
-        lk_frame_message(&r.report, buf, sizeof buf);
-        const int st = static_cast<int>(r.report.failed_stage);
+        lk_frame_message(&rep, buf, sizeof buf);
+        const int st = static_cast<int>(rep.failed_stage);
         throw StageError(st, lk_stage_name(st), buf);
     }
-    return r;
+}
+}  // namespace detail
+
+// The drop-in for a caller that runs frame after frame (lanedet detect, a
+// video loop): the context, its device buffers, pinned staging and captured
+// CUDA graph are built once, so a call costs the frame's copies and kernels.
+// A Result's hooks read the context's buffers: they stay valid until the next
+// run() on the same Pipeline.
+class Pipeline {
+  public:
+    template <typename Cfg>
+    Pipeline(int width, int height, const Cfg& cfg, int device = 0,
+             uint32_t flags = LK_FLAG_HOOKS)
+        : w_(width), h_(height) {
+        const lk_config c = to_lk_config(cfg);
+        check(lk_validate_config(&c));
+        ctx_ = std::make_shared<Context>(width, height, c, 1, device, flags);
+        void* g = nullptr;
+        void* d = nullptr;
+        check(lk_host_alloc(&g, static_cast<size_t>(width) * height));
+        check(lk_host_alloc(&d, static_cast<size_t>(width) * height));
+        g_.reset(static_cast<uint8_t*>(g));
+        d_.reset(static_cast<uint8_t*>(d));
+    }
+
+    template <typename Gray, typename Disp>
+    Result run(const Gray& left, const Disp& disparity) {
+        detail::check_inputs(left, disparity);
+        if (left.width != w_ || left.height != h_)
+            throw Error("lanekit_gpu: frame size differs from the Pipeline's");
+        detail::to_u8(left, disparity, g_.get(), d_.get());
+        Result r;
+        r.ctx = ctx_;
+        const lk_status s = lk_run_batch(ctx_->get(), g_.get(), d_.get(), 1, LK_MEM_HOST, &r.report);
+        if (s != LK_OK && s != LK_ERR_FRAME) check(s);
+        detail::throw_if_failed(r.report);
+        return r;
+    }
+
+  private:
+    struct HostDel {
+        void operator()(uint8_t* p) const { lk_host_free(p); }
+    };
+    int w_, h_;
+    std::shared_ptr<Context> ctx_;
+    std::unique_ptr<uint8_t, HostDel> g_, d_;
+};
+
+// Stages 5-12 on one frame; `left` is a GrayImage-like (width, height,
+// data of k/255.0), `disparity` a DisparityMap-like (ints, 0 = invalid).
+// One-shot: builds a context for the call (use Pipeline to reuse one).
+template <typename Gray, typename Disp, typename Cfg>
+Result run_from_disparity(const Gray& left, const Disp& disparity, const Cfg& cfg,
+                          int device = 0) {
+    detail::check_inputs(left, disparity);
+    Pipeline p(left.width, left.height, cfg, device);
+    return p.run(left, disparity);
 }
 
 }  // namespace lanekit_gpu

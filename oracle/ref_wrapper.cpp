@@ -80,7 +80,7 @@ void compute_frame(const uint8_t* grey, const uint8_t* dispu8, int W, int H,
     cfg.min_lane_sep = c.min_lane_sep;
     cfg.rng_seed = c.rng_seed;
     cfg.paper_sign = c.paper_sign != 0;
-    cfg.threads = 1;
+    cfg.threads = c.threads > 0 ? c.threads : 1;  // the reference's own intra-frame threading
 
     int stage = 1;
     auto run_stage = [&](int n, auto&& body) {  // pipeline.hpp:138-150
@@ -162,7 +162,8 @@ void compute_frame(const uint8_t* grey, const uint8_t* dispu8, int W, int H,
             r.mask = mask.data;
         });
         run_stage(9, [&] {
-            smoothed = bilateral_filter(left, cfg.sigma_s, cfg.sigma_r, (cfg.bf_window - 1) / 2, 1);
+            smoothed = bilateral_filter(left, cfg.sigma_s, cfg.sigma_r, (cfg.bf_window - 1) / 2,
+                                        cfg.threads);
             r.smoothed = smoothed.data;
         });
         run_stage(10, [&] {
@@ -218,7 +219,7 @@ void compute_frame(const uint8_t* grey, const uint8_t* dispu8, int W, int H,
             const Real tr = std::isnan(cfg.tr_lpv) ? auto_lane_threshold(m1, vp.v_top, vp.v_max)
                                                    : cfg.tr_lpv;
             rep.tr_lpv_used = tr;
-            energy = aggregate_energy(m1, vp, cfg.xi, cfg.lambda_g, 1);
+            energy = aggregate_energy(m1, vp, cfg.xi, cfg.lambda_g, cfg.threads);
             r.energy = energy.h;
             lanes = select_lanes(energy, tr, cfg.min_lane_sep, vp);
             rep.lane_count = static_cast<int64_t>(lanes.lanes.size());

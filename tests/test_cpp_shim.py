@@ -42,3 +42,18 @@ def test_shim_runs_probe_scene(tmp_path):
     exe = _build(tmp_path, False)
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300).stdout
     assert out.strip() == "lanes: 767 370"
+
+
+@pytest.mark.gpu
+def test_shim_pipeline_reuses_context(tmp_path):
+    """lanekit_gpu::Pipeline: frame after frame on one context (the drop-in for a
+    per-frame caller, pipeline.hpp:118) gives identical lanes every call; prints
+    its batch-1 latency."""
+    import json
+
+    exe = _build(tmp_path, False)
+    out = subprocess.run([str(exe), "--latency", "100"], capture_output=True, text=True,
+                         timeout=300).stdout.strip().splitlines()
+    assert out[0] == "lanes: 767 370"
+    lat = json.loads(out[1])["batch1_latency_ms"]
+    assert lat["lanes_identical"] is True and lat["calls"] == 100 and lat["median"] > 0

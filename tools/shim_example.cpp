@@ -3,7 +3,11 @@
 // lanekit::GrayImage / DisparityMap / PipelineConfig (image.hpp, config.hpp),
 // otherwise structurally identical local stand-ins (the GPU box has no
 // /root/reference). Prints the lanes or the StageError; exit 0 on either.
+#include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "lanekit_gpu.hpp"
@@ -40,7 +44,7 @@ struct PipelineConfig {
 };
 #endif
 
-int main() {
+int main(int argc, char** argv) {
     lk_scene_params p;
     lk_scene_default(&p);
     p.width = 1242;
@@ -75,6 +79,28 @@ int main() {
         std::printf("StageError %d: %s\n", e.stage, e.what());
     } catch (const lanekit_gpu::Error& e) {
         std::printf("Error: %s\n", e.what());
+        return 0;
+    }
+    // --latency N: the drop-in's per-frame latency with the context reused
+    // (lanekit_gpu::Pipeline), host frame in -> lanes out, N calls
+    if (argc == 3 && std::strcmp(argv[1], "--latency") == 0) {
+        const int n = std::atoi(argv[2]);
+        lanekit_gpu::Pipeline pipe(1242, 375, cfg);
+        std::vector<double> ms;
+        bool same = true;
+        for (int i = 0; i < n + 5; ++i) {
+            const auto t0 = std::chrono::steady_clock::now();
+            const lanekit_gpu::Result r = pipe.run(left, disp);
+            const auto t1 = std::chrono::steady_clock::now();
+            same &= r.report.lane_count == 2 && r.report.lane_bottom_col[0] == 767 &&
+                    r.report.lane_bottom_col[1] == 370;
+            if (i >= 5) ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+        }
+        std::sort(ms.begin(), ms.end());
+        std::printf("{\"batch1_latency_ms\": {\"median\": %.4f, \"p99\": %.4f, \"min\": %.4f, "
+                    "\"calls\": %d, \"lanes_identical\": %s}}\n",
+                    ms[ms.size() / 2], ms[std::min(ms.size() - 1, ms.size() * 99 / 100)], ms[0], n,
+                    same ? "true" : "false");
     }
     return 0;
 }
