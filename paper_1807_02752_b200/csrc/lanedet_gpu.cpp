@@ -830,13 +830,100 @@ int cmd_stream(const std::string& list_path, const std::string& out_path, const 
     return 0;
 }
 
+// ---------------------------------------------------------------- bench
+//
+// lanedet bench (lanedet.cpp:111-127, bench.hpp:44-102) on the GPU: the same
+// synthetic scene (lane bottoms at W/3 and 2W/3, d_max and seed from the
+// config, the search range clamped to what the scene can contain), a batch of
+// that stereo pair through stages 1-12 on one LK_FLAG_STEREO context, and the
+// per-stage table from the CUDA events of the batch's first frame range
+// (lk_stage_times; median of --reps runs). The reference's naive-vs-memoised
+// NCC comparison times its two CPU matchers; the GPU matcher is the certified
+// integer NCC, so that part reports the GPU matcher only.
+int cmd_bench(const std::string& cfgp, int width, int height, int reps, int batch,
+              const std::vector<std::string>& overrides) {
+    if (reps < 1) throw Error("bench: need at least one repetition");
+    if (batch < 1) throw Error("bench: need a batch of at least one frame");
+    lk_config cfg = make_config(cfgp, overrides, 0);
+    lk_scene_params sp;  // bench.hpp:51-57
+    lk_scene_default(&sp);
+    sp.width = width;
+    sp.height = height;
+    sp.n_lanes = 2;
+    sp.lane_bottoms[0] = width / 3.0;
+    sp.lane_bottoms[1] = 2.0 * width / 3.0;
+    sp.d_max = cfg.d_max;
+    sp.rng_seed = cfg.rng_seed;
+    // d_scene = min(d_max, llround(road_f(beta, H - 1)) + 4) (bench.hpp:62-64)
+    const double v = height - 1.0;
+    const double f = sp.beta[0] + sp.beta[1] * v + sp.beta[2] * v * v;
+    cfg.d_max = std::min(cfg.d_max, static_cast<int>(std::llround(f)) + 4);
+    if (lk_validate_config(&cfg) != LK_OK) throw Error(lk_last_error());
+    const size_t px = (size_t)width * height;
+    std::vector<uint8_t> l(px), r(px);
+    if (lk_synth_scene(&sp, l.data(), r.data(), nullptr, nullptr)) throw Error(lk_last_error());
+    PinnedBuf L(px * batch), R(px * batch);
+    for (int i = 0; i < batch; ++i) {
+        std::memcpy(static_cast<uint8_t*>(L.p) + i * px, l.data(), px);
+        std::memcpy(static_cast<uint8_t*>(R.p) + i * px, r.data(), px);
+    }
+    lk_ctx* ctx = nullptr;
+    if (lk_create(&ctx, 0, &cfg, width, height, batch, LK_FLAG_STEREO)) throw Error(lk_last_error());
+    std::vector<lk_frame_report> reps_out(batch);
+    std::vector<std::array<float, 13>> runs;
+    std::vector<double> wall;
+    lk_status st = LK_OK;
+    for (int k = 0; k < reps + 1; ++k) {  // the first run captures the graphs
+        const auto t0 = std::chrono::steady_clock::now();
+        st = lk_run_stereo_batch(ctx, static_cast<uint8_t*>(L.p), static_cast<uint8_t*>(R.p), batch,
+                                 LK_MEM_HOST, reps_out.data());
+        const auto t1 = std::chrono::steady_clock::now();
+        if (st != LK_OK && st != LK_ERR_FRAME) {
+            lk_destroy(ctx);
+            throw Error(lk_last_error());
+        }
+        std::array<float, 13> ms{};
+        lk_stage_times(ctx, ms.data());
+        if (k) {
+            runs.push_back(ms);
+            wall.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+        }
+    }
+    const int timed = lk_timed_frames(ctx);
+    lk_destroy(ctx);
+    auto median = [](std::vector<double> x) {
+        std::sort(x.begin(), x.end());
+        return x[x.size() / 2];
+    };
+    std::printf("block matching (GPU certified integer NCC, stages 1-4), %dx%d, batch %d, "
+                "%d rep(s)%s\n", width, height, batch, reps, reps < 3 ? " [low confidence]" : "");
+    std::printf("pipeline stages (GPU, events of the first %d-frame range):\n", timed);
+    for (int s = 1; s <= 12; ++s) {
+        std::vector<double> v;
+        for (const auto& m : runs) v.push_back(m[s]);
+        std::printf("  %2d %-28s %9.3f ms\n", s, lk_stage_name(s), median(v));
+    }
+    std::vector<double> tot;
+    for (const auto& m : runs) tot.push_back(m[0]);
+    std::printf("  total %38.3f ms\n", median(tot));
+    const double w = median(wall);
+    std::printf("batch wall clock (host pairs in, reports out): %.3f ms = %.1f frames/s; "
+                "lanes of frame 0:", w, batch / (w * 1e-3));
+    for (int i = 0; i < (int)reps_out[0].lane_count && i < LK_MAX_INLINE_LANES; ++i)
+        std::printf(" %lld", (long long)reps_out[0].lane_bottom_col[i]);
+    std::printf("%s\n", reps_out[0].status ? " (frame failed)" : "");
+    return 0;
+}
+
 int usage() {
     std::fprintf(stderr,
                  "usage: lanedet_gpu detect --left L --right R --out-dir D [--config F] "
                  "[--set key=value]... [--emit-all] [--threads N]\n"
                  "       lanedet_gpu stream --list PAIRS --out CSV [--batch N] [--config F] "
                  "[--set key=value]... [--threads N]\n"
-                 "       lanedet_gpu synth --out-dir D [--seed S] [--width W] [--height H]\n");
+                 "       lanedet_gpu synth --out-dir D [--seed S] [--width W] [--height H]\n"
+                 "       lanedet_gpu bench [--config F] [--set key=value]... [--width W] "
+                 "[--height H] [--reps N] [--batch N]\n");
     return 2;
 }
 
@@ -847,7 +934,8 @@ int main(int argc, char** argv) {
     const std::string cmd = argv[1];
     std::string left, right, cfg, out_dir, list, out_csv;
     bool emit_all = false;
-    int threads = 0, width = 640, height = 360, batch = 64;
+    int threads = 0, width = 640, height = 360, batch = 64, reps = 3;
+    bool batch_set = false, size_set = false;
     uint64_t seed = 1;
     std::vector<std::string> overrides;
     try {
@@ -864,12 +952,13 @@ int main(int argc, char** argv) {
             else if (a == "--set") overrides.push_back(val());
             else if (a == "--list") list = val();
             else if (a == "--out") out_csv = val();
-            else if (a == "--batch") batch = std::stoi(val());
+            else if (a == "--batch") batch = std::stoi(val()), batch_set = true;
+            else if (a == "--reps") reps = std::stoi(val());
             else if (a == "--threads") threads = std::stoi(val());
             else if (a == "--emit-all") emit_all = true;
             else if (a == "--seed") seed = std::stoull(val());
-            else if (a == "--width") width = std::stoi(val());
-            else if (a == "--height") height = std::stoi(val());
+            else if (a == "--width") width = std::stoi(val()), size_set = true;
+            else if (a == "--height") height = std::stoi(val()), size_set = true;
             else throw Error("unknown option " + a);
         }
         if (cmd == "detect") {
@@ -884,6 +973,9 @@ int main(int argc, char** argv) {
             if (out_dir.empty()) return usage();
             return cmd_synth(out_dir, seed, width, height);
         }
+        if (cmd == "bench")  // the reference's defaults: 320x240 (bench.hpp:44), batch 1
+            return cmd_bench(cfg, size_set ? width : 320, size_set ? height : 240, reps,
+                             batch_set ? batch : 1, overrides);
         return usage();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());

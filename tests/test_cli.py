@@ -177,3 +177,38 @@ def test_cli_stream_matches_reference(tmp_path, oracle):
         cols = [int(x) for x in r["bottom_cols"].split(";")] if r["bottom_cols"] else []
         n = min(rep.lane_count, abi.LK_MAX_INLINE_LANES)
         assert cols == list(ref.get("LANES")["bottom_col"])[:n]
+
+
+def test_cli_bench_rejects_bad_args():
+    out = subprocess.run([str(CLI), "bench", "--reps", "0"], capture_output=True, text=True)
+    assert out.returncode == 1 and "repetition" in out.stderr
+
+
+@pytest.mark.gpu
+def test_cli_bench_stage_table(ref):
+    """lanedet bench (lanedet.cpp:111-127): the reference's synthetic 320x240
+    scene, every stage of run_pipeline timed, and the same lanes as the
+    reference's run_pipeline on that scene (stereo pair in)."""
+    out = subprocess.run([str(CLI), "bench", "--reps", "3", "--batch", "16"], capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    lines = out.stdout.splitlines()
+    stages = [ln for ln in lines if ln[:4].strip().isdigit()]
+    assert [int(ln.split()[0]) for ln in stages] == list(range(1, 13))
+    assert "total" in out.stdout and "frames/s" in out.stdout
+    # lanes of the GPU frame vs the reference's run_pipeline on the same pair
+    p = abi.scene_params(width=320, height=240, lane_bottoms=(320 / 3, 640 / 3), d_max=64,
+                         rng_seed=1)
+    left, right, _, _ = ref.gen_scene(p)
+    cfg = abi.default_config(d_max=min(64, round(-15 + 0.15 * 239 + 1e-4 * 239 ** 2) + 4))
+    import ctypes as C
+
+    rep = (abi.LkFrameReport * 1)()
+    ref.lib.lkref_run_stereo_batch.argtypes = [
+        C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(abi.LkConfig), C.c_int,
+        C.POINTER(abi.LkFrameReport)]
+    ref.lib.lkref_run_stereo_batch(left.ctypes.data, right.ctypes.data, 1, 320, 240,
+                                   C.byref(cfg), 1, rep)
+    want = rep[0].as_dict()["lane_bottom_col"]
+    got = [int(x) for x in lines[-1].split("lanes of frame 0:")[1].split()]
+    assert got == want
