@@ -133,6 +133,13 @@ typedef struct lk_frame_report {
     int64_t lane_count;        /* full count; first LK_MAX_INLINE_LANES inline below */
     int64_t lane_bottom_col[LK_MAX_INLINE_LANES];
     double lane_energy[LK_MAX_INLINE_LANES];
+    /* Certificate of the lane decisions (not a reference field; 0 from the
+     * CPU checkers): the number of integer decisions whose outcome the GPU's
+     * libdevice atan2 / exp (<= 2 ulp from glibc) could have flipped, i.e. the
+     * w_g gates within 1e-12 of pi/6 and the lane-minimum / threshold /
+     * order comparisons within their propagated error bounds. 0 means the
+     * lane columns and polyline lengths equal the reference's exactly. */
+    int64_t uncertain;
 } lk_frame_report;
 
 /* Per-stage hooks: the PipelineResult members (pipeline.hpp:69-99). Layouts:

@@ -112,6 +112,7 @@ class LkFrameReport(C.Structure):
         ("lane_count", C.c_int64),
         ("lane_bottom_col", C.c_int64 * LK_MAX_INLINE_LANES),
         ("lane_energy", C.c_double * LK_MAX_INLINE_LANES),
+        ("uncertain", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -404,6 +404,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     A(&d.energy, (size_t)B * C);
     A(&d.mrange, (size_t)B * H);
     A(&d.track_np, (size_t)B * C);
+    A(&d.e_touch, (size_t)B * C);
     int sort_cap = 1;
     while (sort_cap < C / 2 + 2) sort_cap <<= 1;
     d.lane_cap = sort_cap;
@@ -533,7 +534,7 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     A(&d.wg_nz, (size_t)B * d.m_ntx * d.m_nty);
     lp.collect_blocks = 32;
     lp.sort_cap = sort_cap;
-    lp.select_smem = (size_t)sort_cap * 12 + (size_t)((C + 31) / 32) * 4 + 16;
+    lp.select_smem = (size_t)sort_cap * 12 + (size_t)((C + 31) / 32) * 8 + 16;  // + certificate bits
     const size_t smem_cap = prop.sharedMemPerBlockOptin;
     if (lp.vdisp_smem > smem_cap || lp.vpath_smem > smem_cap || lp.road_smem > smem_cap || lp.bf_smem > smem_cap || lp.bt_smem > smem_cap ||
         lp.vanish_smem > smem_cap || lp.gamma_smem > smem_cap || lp.m_smem > smem_cap || lp.select_smem > smem_cap) {
@@ -714,6 +715,7 @@ static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     sh(v.energy, C);
     sh(v.mrange, H);
     sh(v.track_np, C);
+    sh(v.e_touch, C);
     sh(v.lanes, (size_t)d.lane_cap);
     sh(v.polylines, (size_t)d.lane_cap * H);
     sh(v.mask, px);

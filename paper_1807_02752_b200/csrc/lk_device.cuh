@@ -30,7 +30,8 @@ struct FrameAux {
     unsigned long long p99_rank;    // rank of the percentile inside the bucket
     double tr;                      // tr_lpv used
     int lanes;                      // kept lanes
-    int pad;
+    unsigned int uncertain_gates;   // w_g gates within kGateEps of pi/6 (k_wg)
+    unsigned long long max_wg;      // max |w_g| (IEEE bits of a non-negative double)
 };
 
 // Everything a kernel needs, passed by value. Pointers index frame-major
@@ -116,6 +117,7 @@ struct Dev {
     double* energy;         // [B][ext_cols]
     int2* mrange;           // [B][H] road-mask disparity interval per row (empty above the horizon)
     int32_t* track_np;      // [B][ext_cols] finite points of each column's lane_track
+    uint8_t* e_touch;       // [B][ext_cols] the column's track read a cell within reach of a w_g != 0
     uint8_t* wg_nz;         // [B][m_nty][m_ntx] m0/m1 tiles with a non-zero w_g in reach
     lk_lane* lanes;         // [B][lane_cap]
     double* polylines;      // [B][lane_cap][H] (hooks)

@@ -987,9 +987,15 @@ __global__ void __launch_bounds__(256) k_edge_emit_tiles(Dev d) {
 }
 
 // lanes.hpp:20-25
-__device__ __forceinline__ double piecewise_weight(double te, double tv, double sg) {
+// Gate margin of the certificate (lk_frame_report.uncertain): the two atan2
+// (libdevice, <= 2 ulp; glibc <= 1 ulp) move te - tv, hence dd, by < 1e-14.
+constexpr double kGateEps = 1e-12;
+
+__device__ __forceinline__ double piecewise_weight(double te, double tv, double sg,
+                                                   bool* uncertain = nullptr) {
     double dd = fmod(fabs(te - tv), kPi);
     if (dd > kPi / 2) dd = kPi - dd;
+    if (uncertain) *uncertain = fabs(dd - kPi / 6) <= kGateEps;
     if (dd > kPi / 6) return 0.0;
     return exp(-(dd / (sg * sg)) * (36 / kPi));
 }
@@ -1406,6 +1412,8 @@ __global__ void __launch_bounds__(256) k_wg(Dev d) {
     uint8_t* wnz = d.wg_nz + (size_t)f * d.m_nty * d.m_ntx;
     const int n_edges = d.row_off[(size_t)f * (H + 1) + H];
     const size_t eb = (size_t)f * d.px;
+    unsigned n_unc = 0;
+    double wmax = 0.0;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_edges; e += gridDim.x * blockDim.x) {
         const int uv = d.e_uv[eb + e];
         const int u = uv & 0xffff, v = uv >> 16;
@@ -1421,9 +1429,12 @@ __global__ void __launch_bounds__(256) k_wg(Dev d) {
             if (!(fabs(dx) < 1e-12 && fabs(dy) < 1e-12)) {
                 const double theta_ray = atan2(dy, dx);
                 const double theta_tangent = th + kPi / 2;
-                wg = gx * piecewise_weight(theta_tangent, theta_ray, d.sigma_g);
+                bool unc;
+                wg = gx * piecewise_weight(theta_tangent, theta_ray, d.sigma_g, &unc);
+                n_unc += unc;
             }
         }
+        wmax = fmax(wmax, fabs(wg));
         d.e_wg[eb + e] = wg;
         if (wg != 0.0) {
             const int th = 1 << d.m_tile_shift;
@@ -1433,6 +1444,15 @@ __global__ void __launch_bounds__(256) k_wg(Dev d) {
             for (int ty = ty0; ty <= ty1; ++ty)
                 for (int tx = tx0; tx <= tx1; ++tx) wnz[ty * d.m_ntx + tx] = 1;
         }
+    }
+    // certificate inputs (k_select): uncertain gates and the largest |w_g|
+    for (int o = 16; o; o >>= 1) {
+        n_unc += __shfl_xor_sync(0xffffffffu, n_unc, o);
+        wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (n_unc) atomicAdd(&d.aux[f].uncertain_gates, n_unc);
+        if (wmax > 0.0) atomicMax(&d.aux[f].max_wg, (unsigned long long)__double_as_longlong(wmax));
     }
 }
 
@@ -1858,6 +1878,7 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
     const double u_bottom = (double)(d.ext_lo + ci);
     double u = u_bottom;
     double e = 0.0;
+    bool touched = false;  // read a cell within reach of a w_g != 0 (m1 tile flag)
     // Chunks of EC rows: the track recursion (lane_track, lanes.hpp:83-96)
     // yields EC gather indices, the EC m1 loads are then all in flight
     // together, and the decayed sum consumes them in row order.
@@ -1882,7 +1903,10 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
         }
         double c[EC];
 #pragma unroll
-        for (int k = 0; k < EC; ++k) c[k] = idx[k] >= 0 ? m1[idx[k]] : 0.0;
+        for (int k = 0; k < EC; ++k) {
+            c[k] = idx[k] >= 0 ? m1[idx[k]] : 0.0;
+            touched |= idx[k] >= 0;
+        }
 #pragma unroll
         for (int k = 0; k < EC; ++k)
             if (vc - k >= v_alive) e = c[k] + lg * e;
@@ -1890,6 +1914,7 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
     // rows after the track stops contribute +0.0 (kept: 0 + (-0.0) is +0.0)
     for (int v = v_alive - 1; v >= v_top; --v) e = 0.0 + lg * e;
     d.energy[(size_t)f * d.ext_cols + ci] = e;
+    d.e_touch[(size_t)f * d.ext_cols + ci] = touched;
     // lane_track's finite points (lanes.hpp:83-96), for k_select: NaN is
     // absorbing in track_step (every operation propagates it), so a non-NaN
     // final u means every step was finite; otherwise (rare) recount.
@@ -1903,6 +1928,72 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
         }
     }
     d.track_np[(size_t)f * d.ext_cols + ci] = np;
+}
+
+// =====================================================================
+// Certificate of the lane decisions (lk_frame_report.uncertain). The only
+// arithmetic that differs from the reference's is libdevice's atan2 / exp in
+// theta and w_g (<= 2 ulp; glibc <= 1 ulp); every later sum runs in the
+// reference's order. With the gates certain (k_wg: none within kGateEps of
+// pi/6), |w_g - w_g,ref| <= kWgRel |w_g| (the gate distance moves by < 1e-14,
+// exp's argument by < 1e-14, exp by <= 3 ulp), so over the m0 box and the m1
+// Sobel |m1 - m1,ref| <= 8 (2 nu + 1)(2 varsigma + 1) kWgRel max|w_g| =: e1,
+// an energy (sum of lambda_g^k m1 over the track rows) moves by <= e1 S_lambda
+// when its track reads a cell within reach of a w_g != 0 (the m1 tile flags,
+// e_touch) and not at all otherwise, and the auto threshold (-0.15 rows p99 of
+// |m1|) by <= 0.15 rows e1. A strict comparison is certain when its margin
+// exceeds the two operands' bounds; the count is the minima tests that are not
+// certain, plus order pairs of certain candidates within min_sep whose
+// energies are within their bounds (the greedy suppression could flip).
+// =====================================================================
+constexpr double kWgRel = 1e-12;
+
+__device__ void select_certificate(const Dev& d, int f, const double* h, double tr,
+                                   unsigned int* cbits) {
+    __shared__ unsigned int s_unc;
+    const int n = d.ext_cols, H = d.H, v_top = (int)d.rep[f].horizon;
+    const int rows = H - v_top;
+    const double lg = d.lambda_g;
+    const double wmax = __longlong_as_double((long long)d.aux[f].max_wg);
+    const double e1 = 8.0 * (2 * d.nu + 1) * (2 * d.varsigma + 1) * kWgRel * wmax;
+    const double sl = lg == 1.0 ? (double)rows : (pow(lg, (double)rows) - 1.0) / (lg - 1.0);
+    const double eh = e1 * fabs(sl) * 1.01;
+    const double etr = isnan(d.tr_lpv) ? 0.15 * rows * e1 * 1.01 : 0.0;
+    const uint8_t* touch = d.e_touch + (size_t)f * n;
+    if (threadIdx.x == 0) s_unc = 0;
+    for (int w = threadIdx.x; w < (n + 31) >> 5; w += blockDim.x) cbits[w] = 0;
+    __syncthreads();
+    // 3-valued a < b: 1 certain true, 0 certain false, 2 uncertain
+    auto lt3 = [](double a, double ea, double b, double eb) {
+        const double dd = b - a, m = ea + eb;
+        if (m == 0.0) return dd > 0.0 ? 1 : 0;
+        return dd > m ? 1 : dd <= -m ? 0 : 2;
+    };
+    unsigned unc = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (i < 1 || i + 1 >= n) continue;
+        const double ei = touch[i] ? eh : 0.0;
+        const int a = lt3(h[i], ei, h[i - 1], touch[i - 1] ? eh : 0.0);
+        const int b = lt3(h[i], ei, h[i + 1], touch[i + 1] ? eh : 0.0);
+        const int c = lt3(h[i], ei, tr, etr);
+        const bool fals = a == 0 || b == 0 || c == 0;
+        if (!fals && (a == 2 || b == 2 || c == 2)) ++unc;
+        if (!fals && a == 1 && b == 1 && c == 1) atomicOr(&cbits[i >> 5], 1u << (i & 31));
+    }
+    __syncthreads();
+    const int sep = d.min_lane_sep;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (!((cbits[i >> 5] >> (i & 31)) & 1) || !touch[i]) continue;
+        for (int j = max(0, i - sep + 1); j <= min(n - 1, i + sep - 1); ++j)
+            if (j != i && ((cbits[j >> 5] >> (j & 31)) & 1) &&
+                fabs(h[i] - h[j]) <= eh + (touch[j] ? eh : 0.0))
+                unc += j > i || !touch[j];  // each touched pair once
+    }
+    for (int o = 16; o; o >>= 1) unc += __shfl_xor_sync(0xffffffffu, unc, o);
+    if ((threadIdx.x & 31) == 0 && unc) atomicAdd(&s_unc, unc);
+    __syncthreads();
+    if (threadIdx.x == 0) d.rep[f].uncertain = (int64_t)(s_unc + d.aux[f].uncertain_gates);
+    __syncthreads();
 }
 
 // =====================================================================
@@ -1934,6 +2025,7 @@ __global__ void __launch_bounds__(256) k_select(Dev d, int sort_cap) {
         }
     }
     __syncthreads();
+    select_certificate(d, f, h, tr, (unsigned int*)(cols + sort_cap) + ((n + 31) >> 5));
     const int m = min(s_n, sort_cap);
     int p2 = 1;
     while (p2 < m) p2 <<= 1;

@@ -15,7 +15,7 @@ RECORD_DTYPE = np.dtype([
     ("frame", "<u4"), ("status", "<i4"), ("failed_stage", "<i4"), ("horizon", "<i4"),
     ("beta", "<f8", 3), ("gamma", "<f8", 5), ("lane_count", "<i4"),
     ("lane_bottom_col", "<i4", abi.LK_MAX_INLINE_LANES),
-    ("lane_energy", "<f4", abi.LK_MAX_INLINE_LANES),
+    ("lane_energy", "<f4", abi.LK_MAX_INLINE_LANES), ("uncertain", "<i4"),
 ])
 
 
@@ -31,7 +31,8 @@ def lane_record(rep) -> dict:
     d = rep.as_dict()
     return {"status": d["status"], "failed_stage": d["failed_stage"], "beta": d["beta"],
             "gamma": d["gamma"], "horizon": d["horizon"], "lane_count": d["lane_count"],
-            "lanes": list(zip(d["lane_bottom_col"], d["lane_energy"]))}
+            "lanes": list(zip(d["lane_bottom_col"], d["lane_energy"])),
+            "uncertain": d["uncertain"]}
 
 
 def compact_records(reports, frame0: int, n: int | None = None) -> np.ndarray:
@@ -43,7 +44,7 @@ def compact_records(reports, frame0: int, n: int | None = None) -> np.ndarray:
     out = np.zeros(len(rep), RECORD_DTYPE)
     out["frame"] = frame0 + np.arange(len(rep), dtype=np.uint32)
     for k in ("status", "failed_stage", "horizon", "beta", "gamma", "lane_count",
-              "lane_bottom_col", "lane_energy"):
+              "lane_bottom_col", "lane_energy", "uncertain"):
         out[k] = rep[k]
     return out
 

@@ -19,7 +19,7 @@ INT_REPORT = [
     "vpath_has_evidence", "beta_iterations", "beta_degraded", "beta_inlier_count", "horizon",
     "horizon_in_range", "road_mask_pixels", "edge_pixels", "vpx_votes", "vpx_skipped",
     "upath_has_evidence", "gamma_iterations", "gamma_degraded", "gamma_inlier_count",
-    "lane_count", "lane_bottom_col",
+    "lane_count", "lane_bottom_col", "uncertain",
 ]
 FP_REPORT = [
     "vpath_energy", "beta", "beta_inlier_fraction", "upath_energy", "gamma", "gamma_kappa",

@@ -232,3 +232,25 @@ def test_headline_batch_256_vs_reference(oracle):
             del res
     assert not problems, "\n".join(problems[:20])
     assert all(r.status == 0 for r in reps)
+
+
+def test_certificate_zero_on_batch_and_fires_on_a_tie(oracle):
+    """lk_frame_report.uncertain: 0 on config-2 and stress frames (no lane
+    decision within the libdevice-vs-glibc error bounds), and > 0 when the
+    threshold is set exactly to a touched minimum's energy (a tie the
+    transcendental error bound cannot resolve)."""
+    params = [scenes.batch_scene(i) for i in range(8)] + [scenes.stress_scene(i) for i in range(4)]
+    grey, disp = lanekit.synth_batch(params, threads=8)
+    cfg = abi.default_config()
+    with lanekit.GpuPipeline(1242, 375, cfg, max_batch=len(params)) as pipe:
+        reps = pipe.run(grey, disp)
+        assert [r.uncertain for r in reps] == [0] * len(params)
+        e = pipe.stage(0, "ENERGY")
+    tie = float(e.min())  # the deepest minimum: a touched column with negative energy
+    assert tie < 0
+    cfg2 = abi.default_config(tr_lpv=tie)
+    with lanekit.GpuPipeline(1242, 375, cfg2, max_batch=1) as pipe:
+        r = pipe.run(grey[:1], disp[:1])[0]
+    assert r.uncertain >= 1
+    o = oracle.run(grey[0], disp[0], cfg2)
+    assert o.report.uncertain == 0  # (the CPU checkers never flag)
