@@ -561,7 +561,10 @@ def run_ours(args):
                for b in compare_reports(gpu_reps[i], r)]
         line["parity"] = {"frames": len(ref_reps), "against": cb["kind"],
                           "mismatches": len({i for i, _ in bad}),
-                          "first": bad[0][1] if bad else None}
+                          "first": bad[0][1] if bad else None,
+                          # the GPU's lane-decision certificate over the whole batch
+                          "certified_frames": sum(1 for r in gpu_reps if r.uncertain == 0),
+                          "batch_frames": len(gpu_reps)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     pipe.close()

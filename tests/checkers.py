@@ -38,6 +38,10 @@ class Checker:
         self.lib = C.CDLL(str(path))
         self.p = prefix
         f = self._f
+        f("report_size").restype = C.c_size_t
+        if f("report_size")() != C.sizeof(abi.LkFrameReport):
+            raise RuntimeError(f"{path}: lk_frame_report layout differs from abi.LkFrameReport "
+                               f"(stale build: run `make -C oracle`)")
         f("run").restype = C.c_void_p
         f("run").argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.POINTER(abi.LkConfig)]
         f("free").argtypes = [C.c_void_p]

@@ -19,8 +19,10 @@ INT_REPORT = [
     "vpath_has_evidence", "beta_iterations", "beta_degraded", "beta_inlier_count", "horizon",
     "horizon_in_range", "road_mask_pixels", "edge_pixels", "vpx_votes", "vpx_skipped",
     "upath_has_evidence", "gamma_iterations", "gamma_degraded", "gamma_inlier_count",
-    "lane_count", "lane_bottom_col", "uncertain",
+    "lane_count", "lane_bottom_col",
 ]
+# lk_frame_report.uncertain is the GPU's own certificate (0 from the CPU
+# checkers), not a reference field: tests assert it explicitly
 FP_REPORT = [
     "vpath_energy", "beta", "beta_inlier_fraction", "upath_energy", "gamma", "gamma_kappa",
     "gamma_v_normalizer", "gamma_inlier_fraction", "tr_lpv_used", "lane_energy",

@@ -232,6 +232,7 @@ def test_headline_batch_256_vs_reference(oracle):
             del res
     assert not problems, "\n".join(problems[:20])
     assert all(r.status == 0 for r in reps)
+    assert [r.uncertain for r in reps] == [0] * 256  # every lane decision certified
 
 
 def test_certificate_zero_on_batch_and_fires_on_a_tie(oracle):
