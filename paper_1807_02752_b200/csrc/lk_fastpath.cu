@@ -130,35 +130,64 @@ __global__ void __launch_bounds__(128) k_sobel_screen(Dev d) {
     }
     const float* sf = d.smoothed_f + (size_t)f * d.px;
     // only pre-screen survivors (masked pixels that can still be edges) are
-    // screened, one thread per 32-pixel survivor word: each survivor reads the
-    // s~ of its 3x3 neighbourhood (need pixels of k_bilateral_need, mirrored at
-    // the border, preprocess.hpp:71-72)
+    // screened, one thread per survivor: the tile's 64 survivor words are
+    // prefix-summed, and survivor i (in row-major order) is the n-th set bit
+    // of its word (__fns). Each reads the s~ of its 3x3 neighbourhood (need
+    // pixels of k_bilateral_need, mirrored at the border, preprocess.hpp:71-72).
+    __shared__ unsigned s_pw[SB_TH * TWORD], s_pre[SB_TH * TWORD + 1];
+    static_assert(SB_TH * TWORD == 64, "two warps scan the survivor words");
     const float D = (float)(8.0 * kEpsSmooth + 1e-6);
-    unsigned cw = 0;
     if (tid < SB_TH * TWORD) {
-        const int r = tid / TWORD, wt = tid % TWORD, w = (u0 >> 5) + wt;
-        const int v = v0 + r;
-        unsigned x = v < H && w < d.words_per_row
-                         ? d.pbits[((size_t)f * H + v) * d.words_per_row + w] : 0u;
+        const int r = tid / TWORD, w = (u0 >> 5) + tid % TWORD;
+        const unsigned x = v0 + r < H && w < d.words_per_row
+                               ? d.pbits[((size_t)f * H + v0 + r) * d.words_per_row + w] : 0u;
+        s_pw[tid] = x;
+        s_cw[r][tid % TWORD] = 0;
+        // inclusive prefix of the popcounts over the 64 words (two warps)
+        unsigned c = __popc(x);
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, c, o);
+            if ((tid & 31) >= o) c += y;
+        }
+        s_pre[tid + 1] = c;  // warp-local for now
+    }
+    if (tid == 0) s_pre[0] = 0;
+    __syncthreads();
+    if (tid >= 32 && tid < 64) s_pre[tid + 1] += s_pre[32];  // second warp's offset
+    __syncthreads();
+    const unsigned total = s_pre[SB_TH * TWORD];
+    if (total == 0) {  // no survivor: no edge in this tile
+        if (tid < SB_TH && v0 + tid < H)
+            d.seg_cnt[((size_t)f * H + v0 + tid) * d.n_seg + blockIdx.x] = 0;
+        return;
+    }
+    bool anyc = false;
+    for (unsigned i = tid; i < total; i += blockDim.x) {
+        int lo = 0, hi = SB_TH * TWORD;  // word: s_pre[lo] <= i < s_pre[lo + 1]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_pre[mid] <= i) lo = mid; else hi = mid;
+        }
+        const int bit = (int)__fns(s_pw[lo], 0, (int)(i - s_pre[lo]) + 1);
+        const int r = lo / TWORD, v = v0 + r, u = u0 + 32 * (lo % TWORD) + bit;
         const float* ra = sf + (size_t)mirror(v - 1, H) * W;
         const float* rb = sf + (size_t)v * W;
         const float* rc = sf + (size_t)mirror(v + 1, H) * W;
-        while (x) {
-            const int bit = __ffs(x) - 1;
-            x &= x - 1;
-            const int u = 32 * w + bit, ul = mirror(u - 1, W), ur = mirror(u + 1, W);
-            const float a0 = ra[ul], a1 = ra[u], a2 = ra[ur];
-            const float b0 = rb[ul], b2 = rb[ur];
-            const float c0 = rc[ul], c1 = rc[u], c2 = rc[ur];
-            const float gx = ((a2 - a0) + 2.f * (b2 - b0)) + (c2 - c0);
-            const float gy = ((c0 - a0) + 2.f * (c1 - a1)) + (c2 - a2);
-            const float sg = gx * gx + gy * gy;
-            const float ds = 1.001f * (D * (2.f * fabsf(gx) + D) + D * (2.f * fabsf(gy) + D)) +
-                             4e-7f * sg + 1e-9f;
-            if (sg + ds >= d.sobel_s_star_lo) cw |= 1u << bit;
+        const int ul = mirror(u - 1, W), ur = mirror(u + 1, W);
+        const float a0 = ra[ul], a1 = ra[u], a2 = ra[ur];
+        const float b0 = rb[ul], b2 = rb[ur];
+        const float c0 = rc[ul], c1 = rc[u], c2 = rc[ur];
+        const float gx = ((a2 - a0) + 2.f * (b2 - b0)) + (c2 - c0);
+        const float gy = ((c0 - a0) + 2.f * (c1 - a1)) + (c2 - a2);
+        const float sg = gx * gx + gy * gy;
+        const float ds = 1.001f * (D * (2.f * fabsf(gx) + D) + D * (2.f * fabsf(gy) + D)) +
+                         4e-7f * sg + 1e-9f;
+        if (sg + ds >= d.sobel_s_star_lo) {
+            atomicOr(&s_cw[r][lo % TWORD], 1u << bit);
+            anyc = true;
         }
-        s_cw[r][wt] = cw;
     }
+    const unsigned cw = anyc ? 1u : 0u;
     if (tid == 0) s_nneed = 0;
     if (!__syncthreads_or(cw != 0)) {  // no edge can exist in this tile (most tiles)
         if (tid < SB_TH && v0 + tid < H)
