@@ -432,6 +432,11 @@ def run_ours(args):
     e3.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)
+    # the streamed batches' reports must equal the lk_run_batch ones, byte for byte
+    last = rbufs[(e2_steps - 1) % 2]
+    rsz = C.sizeof(abi.LkFrameReport)
+    e2e_report_mismatch = sum(1 for i in range(B)
+                              if C.string_at(C.addressof(last[i]), rsz) != C.string_at(C.addressof(reps[i]), rsz))
     failed = max([failed] + e2e_failed)
     for rb in rbufs:
         L.lk_host_free(C.cast(rb, C.c_void_p))
@@ -500,6 +505,7 @@ def run_ours(args):
         "failed_frames": failed,
         "stage_ms": {str(k): round(float(stage_ms[k]), 4) for k in range(first, 13)},
         "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": 2 * B * px,
+                "report_mismatches_vs_run_batch": e2e_report_mismatch,
                 "d2h_bytes_per_step": B * C.sizeof(abi.LkFrameReport),
                 "api": ("lk_submit_stereo_batch / lk_wait_batch: pinned host left+right in, "
                         "reports out; step k+1's copy overlaps step k's kernels" if stereo else
