@@ -137,6 +137,23 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
         : "memory");
 }
 
+// Several bulk copies on one barrier: arm it once with their total bytes
+// (mbar_expect), then issue each copy (bulk_copy; 16-byte aligned, size a
+// multiple of 16).
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     asm volatile(
         "{\n .reg .pred p;\n"
@@ -761,13 +778,19 @@ __device__ __forceinline__ void sobel_at(const double* img, int W, int H, int u,
 // =====================================================================
 // K3b  road_mask (preprocess.hpp:14-26) + sobel_gradients (:67-90) +
 // edge_map test (:103-113). Tile SB_TW x SB_TH with the mirrored 1-px halo
-// of the smoothed image staged in shared memory. The magnitude test
-// !(sqrt(s) < t) is evaluated exactly as s >= s* (s* from the host). Writes
-// the edge bitmap and, per (row, SB_TW-column segment), the edge count.
+// of the smoothed image staged in shared memory: the tile's SB_TH + 2 row
+// interiors (SB_TW doubles, 1 KB each) arrive by TMA bulk copies on one
+// mbarrier while the threads load the two mirrored halo columns; tiles at the
+// right border (or an odd width: rows not 16-byte aligned) stage element-wise.
+// The magnitude test !(sqrt(s) < t) is evaluated exactly as s >= s* (s* from
+// the host). Writes the edge bitmap and, per (row, SB_TW-column segment), the
+// edge count.
 // =====================================================================
 __global__ void __launch_bounds__(256) k_sobel_edges(Dev d) {
-    constexpr int SW = SB_TW + 2;
-    __shared__ double s_img[(SB_TH + 2) * SW];
+    constexpr int SW = SB_TW + 2;   // staged columns u0 - 1 .. u0 + SB_TW
+    constexpr int SWP = SB_TW + 4;  // row pitch: column u0 - 1 + c at index 1 + c (interior 16-B aligned)
+    __shared__ __align__(16) double s_img[(SB_TH + 2) * SWP];
+    __shared__ uint64_t s_bar;
     __shared__ int s_seg[SB_TH];
     __shared__ int s_tot[2];
     const int f = blockIdx.z;
@@ -791,7 +814,19 @@ __global__ void __launch_bounds__(256) k_sobel_edges(Dev d) {
     for (int i = threadIdx.x; i < SW; i += blockDim.x) s_col[i] = mirror(u0 - 1 + i, W);
     if (threadIdx.x < SB_TH + 2) s_row[threadIdx.x] = mirror(v0 - 1 + threadIdx.x, H) * W;
     __syncthreads();
-    {  // all loads in flight before the stores
+    const bool tma = u0 + SB_TW <= W && (W & 1) == 0 && (reinterpret_cast<uintptr_t>(img) & 15) == 0;
+    if (tma) {
+        if (threadIdx.x == 0) {
+            mbar_init(&s_bar, 1);
+            mbar_expect(&s_bar, (SB_TH + 2) * SB_TW * 8);
+            for (int r = 0; r < SB_TH + 2; ++r)
+                bulk_copy(s_img + r * SWP + 2, img + (size_t)s_row[r] + u0, SB_TW * 8, &s_bar);
+        }
+        if (threadIdx.x < 2 * (SB_TH + 2)) {  // the mirrored halo columns
+            const int r = threadIdx.x >> 1, c = (threadIdx.x & 1) ? SW - 1 : 0;
+            s_img[r * SWP + 1 + c] = img[(size_t)s_row[r] + s_col[c]];
+        }
+    } else {  // all loads in flight before the stores
         constexpr int NE = ((SB_TH + 2) * SW + 255) / 256;
         double t[NE];
 #pragma unroll
@@ -802,12 +837,13 @@ __global__ void __launch_bounds__(256) k_sobel_edges(Dev d) {
 #pragma unroll
         for (int k = 0; k < NE; ++k) {
             const int i = threadIdx.x + k * 256;
-            if (i < (SB_TH + 2) * SW) s_img[i] = t[k];
+            if (i < (SB_TH + 2) * SW) s_img[(i / SW) * SWP + 1 + i % SW] = t[k];
         }
     }
     if (threadIdx.x < SB_TH) s_seg[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_tot[threadIdx.x] = 0;
     __syncthreads();
+    if (tma) mbar_wait(&s_bar, 0);
     const int lane = threadIdx.x & 31;
     int n_edge = 0, n_mask = 0;
 #pragma unroll
@@ -817,9 +853,9 @@ __global__ void __launch_bounds__(256) k_sobel_edges(Dev d) {
         const int v = v0 + r, u = u0 + c;
         bool edge = false;
         if (v < H && u < W) {
-            const double* a = s_img + r * SW + c;  // row v-1, col u-1
-            const double* b = a + SW;               // row v
-            const double* cc = b + SW;              // row v+1
+            const double* a = s_img + r * SWP + 1 + c;  // row v-1, col u-1
+            const double* b = a + SWP;                   // row v
+            const double* cc = b + SWP;                  // row v+1
             const double gx = (a[2] - a[0]) + 2 * (b[2] - b[0]) + (cc[2] - cc[0]);
             const double gy = (cc[0] - a[0]) + 2 * (cc[1] - a[1]) + (cc[2] - a[2]);
             const double s = gx * gx + gy * gy;
