@@ -386,6 +386,26 @@ constexpr int PQ_RB = 16;  // rows per need block
 constexpr int PQ_RING = 11;  // H ring: the 11 input rows of the current window
 constexpr int PQ_SR = 20;  // survivor bitmap ring rows (>= PQ_RB + 3)
 constexpr uint32_t kOnes = 0x01010101u;
+#ifndef PQ_PFD_N
+#define PQ_PFD_N 2
+#endif
+constexpr int PQ_PFD = PQ_PFD_N;  // rows staged ahead (cp.async): grey row e + 5 and disparity row e - 1
+// bytes of one staged row: the 16-byte chunks covering W bytes at any alignment
+__host__ __device__ __forceinline__ int pq_row_bytes(int W) { return ((W + 30) >> 4 << 4) + 16; }
+
+__device__ __forceinline__ void pq_cp16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void pq_cp8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void pq_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void pq_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ uint32_t pq_byte(uint32_t w, int i) { return (w >> (8 * i)) & 0xffu; }
 
@@ -424,6 +444,11 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
     uint4* ring = reinterpret_cast<uint4*>(pq_sm);                 // [PQ_RING][nt]
     uint32_t* sbits = pq_sm + PQ_RING * 4 * nt;                     // [PQ_SR][wpr + 1]
     const int sbw = wpr + 1;
+    // staged rows (16-byte aligned): grey [PQ_PFD + 1][RB], disparity [PQ_PFD + 1][RB], mask intervals
+    const int RB = pq_row_bytes(W);
+    uint8_t* rowG = reinterpret_cast<uint8_t*>(sbits + ((PQ_SR * sbw + 3) & ~3));
+    uint8_t* rowD = rowG + (PQ_PFD + 1) * RB;
+    int2* rowM = reinterpret_cast<int2*>(rowD + (PQ_PFD + 1) * RB);
     if (tid == 0 && seg == 0) {  // the Sobel screen appends to these
         d.need_cnt[f] = 0;
         d.ctile_cnt[f] = 0;
@@ -457,10 +482,7 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
     int S1[4] = {0, 0, 0, 0}, S2[4] = {0, 0, 0, 0};  // box sums of k, k^2 (exact) per column
     uint32_t cen[6] = {0, 0, 0, 0, 0, 0};  // centre bytes (columns 4q..4q+3) of input rows, newest first
     // H1, H2 of the quad's 4 columns for input row rin (mirrored), packed H1 | H2 << 12
-    auto hrow = [&](int rin, uint4& hp) {
-        const int rr = bigH ? (rin < 0 ? -rin - 1 : rin >= H ? 2 * H - 1 - rin : rin) : mirror(rin, H);
-        uint32_t t0, t1, t2, t3;
-        pq_bytes(g + (size_t)rr * W, q, W, fast, t0, t1, t2, t3);
+    auto hsums = [&](uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, uint4& hp) {
         const uint32_t t2m = t2 & 0x00ffffffu;
         int h1 = (int)__dp4a(t0, kOnes, __dp4a(t1, kOnes, __dp4a(t2m, kOnes, 0u)));
         int h2 = (int)__dp4a(t0, t0, __dp4a(t1, t1, __dp4a(t2m, t2m, 0u)));
@@ -480,6 +502,39 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
         for (int i = 5; i > 0; --i) cen[i] = cen[i - 1];
         cen[0] = __funnelshift_r(t1, t2, 8);  // bytes 5 .. 8 = columns 4q .. 4q + 3
     };
+    auto hrow = [&](int rin, uint4& hp) {
+        const int rr = bigH ? (rin < 0 ? -rin - 1 : rin >= H ? 2 * H - 1 - rin : rin) : mirror(rin, H);
+        uint32_t t0, t1, t2, t3;
+        pq_bytes(g + (size_t)rr * W, q, W, fast, t0, t1, t2, t3);
+        hsums(t0, t1, t2, t3, hp);
+    };
+    // the same from a staged grey row (bytes [0, W) of row rr at offset (src & 15))
+    auto hrow_staged = [&](int rr, int slot, uint4& hp) {
+        const uint8_t* sb = rowG + slot * RB + ((reinterpret_cast<uintptr_t>(g + (size_t)rr * W)) & 15);
+        uint32_t t0, t1, t2, t3;
+        if (fast) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(sb + 4 * q - 5);
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+            const unsigned sh = 8u * (unsigned)(a & 3);
+            const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
+            t0 = __funnelshift_r(w0, w1, sh);
+            t1 = __funnelshift_r(w1, w2, sh);
+            t2 = __funnelshift_r(w2, w3, sh);
+            t3 = __funnelshift_r(w3, w4, sh);
+        } else {
+            uint32_t b[14];
+#pragma unroll
+            for (int i = 0; i < 14; ++i) {  // W >= 160 here: one reflection suffices
+                const int x = 4 * q - 5 + i;
+                b[i] = sb[x < 0 ? -x - 1 : x >= W ? 2 * W - 1 - x : x];
+            }
+            t0 = b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24;
+            t1 = b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24;
+            t2 = b[8] | b[9] << 8 | b[10] << 16 | b[11] << 24;
+            t3 = b[12] | b[13] << 8;
+        }
+        hsums(t0, t1, t2, t3, hp);
+    };
     auto addrow = [&](const uint4& hp, int sg) {
         const uint32_t h[4] = {hp.x, hp.y, hp.z, hp.w};
 #pragma unroll
@@ -493,6 +548,7 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
     //   A2 = m2 / w_min, A1 = m1 + ew sq, sq = 10 m2 + 0.025 >= sqrt(m2) (AM-GM at 0.05),
     // infinite when kappa A2 >= 1/2 (1 / (1 - km) <= 1 + 2 km needs km <= 1/2)
     const int e0 = max(t_lo - 1, 0);  // first E row
+    const int e_last = t_hi + 1;      // == H: the last step mirrors E row H
     for (int i = -5; i <= 5; ++i) {
         uint4 hp;
         hrow(e0 + i, hp);
@@ -536,17 +592,23 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
     // P row r from E rows A = E(r - 1), B = E(r), C = E(r + 1): exact integer
     // Sobel of S1 and |c|-weighted Sobel of E as packed (S1, E) pairs
     const float2 np = make_float2(-1.f, 1.f), two = make_float2(2.f, 2.f);
-    auto test_row = [&](int r, const RowE& A, const RowE& B, const RowE& C) {
+    auto test_row = [&](int r, const RowE& A, const RowE& B, const RowE& C, int slot) {
         // mask inputs of the quad: disparity bytes 4q .. 4q + 3 and the row interval
         uint32_t dw = 0;
         int2 mr = make_int2(256, 0);
         if (outq) {
-            mr = d.mrange[(size_t)f * H + r];
-            const uint8_t* dr = dp + (size_t)r * W + 4 * q;
+            const uint8_t* dr;
+            if (slot >= 0) {  // staged
+                mr = rowM[slot];
+                dr = rowD + slot * RB + ((reinterpret_cast<uintptr_t>(dp + (size_t)r * W)) & 15) + 4 * q;
+            } else {
+                mr = d.mrange[(size_t)f * H + r];
+                dr = dp + (size_t)r * W + 4 * q;
+            }
             if (4 * q + 4 <= W) {
                 const uintptr_t a = reinterpret_cast<uintptr_t>(dr);
                 const uint32_t* wp = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
-                dw = __funnelshift_r(__ldg(wp), __ldg(wp + 1), 8u * (unsigned)(a & 3));
+                dw = __funnelshift_r(wp[0], wp[1], 8u * (unsigned)(a & 3));
             } else {
                 for (int j = 0; j < 4 && 4 * q + j < W; ++j) dw |= (uint32_t)dr[j] << (8 * j);
             }
@@ -631,10 +693,43 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
     int slot = 0;          // ring slot of input row e - 6 (e the next E row); e + 5 reuses it
     // one row step: E row e into N (its storage held E(e - 3)), then P row e - 1
     // with M = E(e - 2) (O = E(e - 1)); at e == H, N = E(H - 1) (the mirror of row H)
+    // staging (bigH): group j = step e0 + 1 + j holds grey row e0 + 6 + j (mirrored), disparity
+    // row e0 + j and its mask interval, in slot j % (PQ_PFD + 1); PQ_PFD groups in flight
+    const bool staged = bigH && W >= 160;
+    auto stage_rows = [&](int j) {
+        const int slot = j % (PQ_PFD + 1);
+        const int rin = e0 + 6 + j, rd = e0 + j;
+        const int rr = rin < 0 ? -rin - 1 : rin >= H ? 2 * H - 1 - rin : rin;
+        const uintptr_t ag = reinterpret_cast<uintptr_t>(g + (size_t)rr * W);
+        const int ng = rin <= min(e_last, H - 1) + 5 ? (int)(((ag & 15) + W + 15) >> 4) : 0;  // consumed by steps e < H
+        const bool dok = rd >= t_lo && rd <= t_hi;
+        const uintptr_t ad = reinterpret_cast<uintptr_t>(dp + (size_t)(dok ? rd : 0) * W);
+        const int nd = dok ? (int)(((ad & 15) + W + 15) >> 4) : 0;
+        for (int i = tid; i < ng + nd; i += nt) {
+            if (i < ng)
+                pq_cp16(rowG + slot * RB + 16 * i, reinterpret_cast<const void*>((ag & ~(uintptr_t)15) + 16 * i));
+            else
+                pq_cp16(rowD + slot * RB + 16 * (i - ng),
+                        reinterpret_cast<const void*>((ad & ~(uintptr_t)15) + 16 * (i - ng)));
+        }
+        if (dok && tid == nt - 1) pq_cp8(rowM + slot, d.mrange + (size_t)f * H + rd);
+        pq_commit();
+    };
     auto step = [&](int e, RowE& M, RowE& O, RowE& N) {
+        const int j = e - e0 - 1, ss = j % (PQ_PFD + 1);  // staging slot of this step
+        if (staged) {
+            pq_wait<PQ_PFD - 1>();  // group j has landed
+            __syncthreads();        // ... for every thread; slot of group j - 1 is free
+            stage_rows(j + PQ_PFD);
+        }
         if (e < H) {
             uint4 hp;
-            hrow(e + 5, hp);
+            if (staged) {
+                const int rin = e + 5;
+                hrow_staged(rin >= H ? 2 * H - 1 - rin : rin, ss, hp);
+            } else {
+                hrow(e + 5, hp);
+            }
             addrow(ring[slot * nt + tid], -1);
             addrow(hp, 1);
             ring[slot * nt + tid] = hp;  // (PQ_RING = 11: row e + 5 takes row e - 6's slot)
@@ -644,7 +739,7 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
             N = O;
         }
         const int r = e - 1;
-        if (r >= t_lo) test_row(r, r == 0 ? O : M, O, N);  // mirror(-1) = 0
+        if (r >= t_lo) test_row(r, r == 0 ? O : M, O, N, staged ? ss : -1);  // mirror(-1) = 0
         // rows up to r are tested: need rows up to r - 1 are final
         if ((r - need_from + 1 >= PQ_RB && r >= t_lo) || r == t_hi) {
             const int re = r == t_hi ? pb : r;
@@ -656,7 +751,8 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
     make_row(Z);  // E row e0
     Y = Z;        // (rolls into the A slot of the first test, which only happens for r >= P0)
     __syncthreads();  // sbits cleared
-    const int e_last = t_hi + 1;  // == H: the last step mirrors E row H
+    if (staged)
+        for (int j = 0; j < PQ_PFD; ++j) stage_rows(j);
     for (int e = e0 + 1; e <= e_last; e += 3) {
         step(e, Y, Z, X);
         if (e + 1 <= e_last) step(e + 1, Z, X, Y);
@@ -667,7 +763,9 @@ __global__ void __launch_bounds__(768) k_prescreen(Dev d, PrescreenParam p) {
 }
 
 size_t prescreen_smem(int W, int nt) {
-    return (size_t)PQ_RING * nt * 16 + (size_t)PQ_SR * ((W + 31) / 32 + 1) * 4;
+    const size_t sb = ((size_t)PQ_SR * ((W + 31) / 32 + 1) + 3) & ~(size_t)3;
+    return (size_t)PQ_RING * nt * 16 + sb * 4 + (size_t)2 * (PQ_PFD + 1) * pq_row_bytes(W) +
+           (size_t)(PQ_PFD + 1) * 8;
 }
 
 int prescreen_segments(int H) { return H >= 128 ? 2 : 1; }
