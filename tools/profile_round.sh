@@ -25,9 +25,12 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -c 200 --csv --log-file "$OUT/launches_hires_single_range.csv" python tools/kernel_times.py hires 3 \
     > "$OUT/ncu_launches_hires.log" 2>&1
-for k in ${KERNELS:-k_prescreen k_bilateral_need k_sobel_screen k_refine_exact k_vdisparity k_vanish k_edge_emit_tiles}; do
+for k in ${KERNELS:-k_prescreen k_bilateral_need k_vanish k_energy k_refine_exact k_m0_m1 k_gamma_fit k_sobel_screen k_sobel_decide k_edge_emit_tiles k_vdisparity}; do
     ncu --set full --clock-control none --import-source on -k "regex:$k" -s 2 -c 1 \
         -o "$OUT/${k}_full" -f python tools/kernel_times.py kitti 2 \
         > "$OUT/ncu_${k}.log" 2>&1
+    python tools/ncu_summary.py "$OUT/${k}_full.ncu-rep" > "$OUT/${k}_ncu.txt" 2>&1
+    python tools/ncu_lines.py "$OUT/${k}_full.ncu-rep" "$k" 25 > "$OUT/${k}_lines.txt" 2>&1
 done
+python tools/fraction_table.py "$OUT"/k_*_ncu.txt > "$OUT/fractions.md" 2>&1
 echo done
