@@ -952,18 +952,26 @@ __global__ void __launch_bounds__(1024) k_edge_scan(Dev d) {
 __device__ __forceinline__ void emit_segment(const Dev& d, int f, int v, int sx, int lane) {
     const int W = d.W, H = d.H;
     const int seg = v * d.n_seg + sx;
-    if (d.seg_cnt[(size_t)f * H * d.n_seg + seg] == 0) return;  // empty segment
+    // every input of the segment requested at once (one memory latency)
+    const int cnt = d.seg_cnt[(size_t)f * H * d.n_seg + seg];
     const int base = d.seg_off[(size_t)f * H * d.n_seg + seg];
-    const double* img = d.smoothed + (size_t)f * d.px;
     const uint32_t* bits = d.ebits + ((size_t)f * H + v) * d.words_per_row;
-    const double vpy = d.vpy[(size_t)f * H + v];
-    const bool sing = d.vsing[(size_t)f * H + v] != 0;
-    const int ext_hi = d.ext_lo + d.ext_cols - 1;
-    int run = 0, n_vote = 0, n_skip = 0;
+    uint32_t bw[SB_TW / 32];
+#pragma unroll
     for (int w = 0; w < SB_TW / 32; ++w) {
         const int word = sx * (SB_TW / 32) + w;
-        if (word >= d.words_per_row) break;
-        const uint32_t b = bits[word];
+        bw[w] = word < d.words_per_row ? bits[word] : 0u;
+    }
+    const double vpy = d.vpy[(size_t)f * H + v];
+    const bool sing = d.vsing[(size_t)f * H + v] != 0;
+    if (cnt == 0) return;  // empty segment
+    const double* img = d.smoothed + (size_t)f * d.px;
+    const int ext_hi = d.ext_lo + d.ext_cols - 1;
+    int run = 0, n_vote = 0, n_skip = 0;
+#pragma unroll
+    for (int w = 0; w < SB_TW / 32; ++w) {
+        const int word = sx * (SB_TW / 32) + w;
+        const uint32_t b = bw[w];
         if ((b >> lane) & 1u) {
             const int u = word * 32 + lane;
             const size_t e = (size_t)f * d.px + base + run + __popc(b & ((1u << lane) - 1u));
