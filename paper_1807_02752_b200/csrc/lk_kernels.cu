@@ -1682,6 +1682,39 @@ __device__ __forceinline__ unsigned long long p99_n(const Dev& d, int f, int* t_
 }
 
 // Picks the bin holding rank `rank` among nb bins (blockDim = 256).
+// One warp: the first index i of a[0..n) (n <= 256) whose running sum
+// exceeds rank (n - 1 if none) and the sum of a[0..i), in every lane: the
+// sequential scan `for (i < n - 1) { if (run + a[i] > rank) break; run += a[i]; }`
+// as 8-entry lane sums, a warp prefix sum and one lane's scan of its 8.
+template <class T>
+__device__ __forceinline__ void warp_find(const T* a, int n, unsigned long long rank, int& idx,
+                                          unsigned long long& before) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (8 * lane + j < n) sum += a[8 * lane + j];
+    unsigned long long inc = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, inc > rank);
+    const int L = hit ? __ffs(hit) - 1 : (n - 1) >> 3;
+    int i = 0;
+    unsigned long long run = 0;
+    if (lane == L) {
+        run = inc - sum;
+        i = 8 * L;
+        for (const int last = min(8 * L + 8, n) - 1; i < last; ++i) {
+            if (run + a[i] > rank) break;
+            run += a[i];
+        }
+    }
+    idx = __shfl_sync(0xffffffffu, i, L);
+    before = __shfl_sync(0xffffffffu, run, L);
+}
+
 __device__ void pick_bin(const unsigned int* h, int nb, unsigned long long rank, int* bin_out,
                          unsigned long long* rank_out) {
     __shared__ unsigned long long s_part[256];
@@ -1690,13 +1723,11 @@ __device__ void pick_bin(const unsigned int* h, int nb, unsigned long long rank,
     for (int b = 0; b < per; ++b) mine += h[threadIdx.x * per + b];
     s_part[threadIdx.x] = mine;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long run = 0;
-        int t = 0;
-        for (; t < 255; ++t) {
-            if (run + s_part[t] > rank) break;
-            run += s_part[t];
-        }
+    if (threadIdx.x < 32) {
+        int t;
+        unsigned long long run;
+        warp_find(s_part, 256, rank, t, run);
+        if (threadIdx.x != 0) return;
         int b = t * per;
         for (; b < (t + 1) * per - 1; ++b) {
             if (run + h[b] > rank) break;
@@ -1841,15 +1872,14 @@ __global__ void __launch_bounds__(256) k_p99_select(Dev d) {
             if ((x & mask) == prefix) atomicAdd(&hist[(x >> sh) & dm], 1u);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long run = 0;
-            unsigned dg = 0;
-            for (; dg < dm; ++dg) {
-                if (run + hist[dg] > rank) break;
-                run += hist[dg];
+        if (threadIdx.x < 32) {
+            int dg;
+            unsigned long long run;
+            warp_find(hist, (int)dm + 1, rank, dg, run);
+            if (threadIdx.x == 0) {
+                s_prefix = prefix | ((unsigned long long)dg << sh);
+                s_rank = rank - run;
             }
-            s_prefix = prefix | ((unsigned long long)dg << sh);
-            s_rank = rank - run;
         }
         __syncthreads();
         prefix = s_prefix;
