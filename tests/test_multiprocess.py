@@ -141,3 +141,25 @@ def test_bench_stream_two_ranks_gather(tmp_path):
                                "bytes_each": line["records"]["bytes_each"]}
     assert line["failed_frames"] == 0 and line["value"] > 0
     assert line["config"]["frames"] == 10 and line["steps"] == 2
+
+
+def test_bench_reference_arm_two_ranks():
+    """bench.py --impl reference launched as the driver launches it for N = 2
+    (torchrun, 127.0.0.1): rank 0 alone times the compiled reference on the host
+    cores and prints one JSON line; rank 1 exits 0 without work."""
+    import json
+    import subprocess
+
+    if not (ROOT / "oracle" / "_ref" / "liblk_ref.so").exists():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    line = lines[0]
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "reference"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
