@@ -423,6 +423,8 @@ def run_ours(args):
             raise RuntimeError(L.lk_last_error().decode())
         e2e_failed.append(sum(1 for i in range(B) if rbufs[k % 2][i].status))
 
+    h2d0, h2d1 = C.c_ulonglong(0), C.c_ulonglong(0)
+    L.lk_h2d_bytes(h, C.byref(h2d0))
     e2.record(stream)
     for k in range(e2_steps):
         submit(h, hg, hd, B, rbufs[k % 2])
@@ -432,6 +434,8 @@ def run_ours(args):
     e3.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)
+    L.lk_h2d_bytes(h, C.byref(h2d1))  # bytes the copies moved (road-row copy: grey rows from the horizon)
+    h2d_per_step = (h2d1.value - h2d0.value) / e2_steps
     # the streamed batches' reports must equal the lk_run_batch ones, byte for byte
     last = rbufs[(e2_steps - 1) % 2]
     rsz = C.sizeof(abi.LkFrameReport)
@@ -504,13 +508,15 @@ def run_ours(args):
         "gpu_launches": launches * args.steps,
         "failed_frames": failed,
         "stage_ms": {str(k): round(float(stage_ms[k]), 4) for k in range(first, 13)},
-        "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": 2 * B * px,
+        "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": round(h2d_per_step),
                 "report_mismatches_vs_run_batch": e2e_report_mismatch,
                 "d2h_bytes_per_step": B * C.sizeof(abi.LkFrameReport),
                 "api": ("lk_submit_stereo_batch / lk_wait_batch: pinned host left+right in, "
                         "reports out; step k+1's copy overlaps step k's kernels" if stereo else
-                        "lk_submit_batch / lk_wait_batch: pinned host grey+disparity in, "
-                        "reports out; step k+1's copy overlaps step k's kernels")},
+                        "lk_submit_batch / lk_wait_batch: pinned host disparity in, then (after "
+                        "stages 5-7 of the step on a side stream) the grey rows from the smallest "
+                        "horizon - 1 - rho down, reports out; step k+1's copies overlap step k's "
+                        "kernels")},
         "roofline": {
             "bound": "hbm", "kernel": f"stage {dom} ({abi.STAGE_NAMES[dom - 1]})",
             "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,

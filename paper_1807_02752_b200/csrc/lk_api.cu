@@ -6,6 +6,7 @@
 // what the reference computes inline (preprocess.hpp:47-50).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -124,6 +125,19 @@ struct lk_ctx {
     int n_pending = 0, next_slot = 0;
     bool last_stereo = false;
     int last_n = 0;
+    // Road-row copy of streamed grey (lk_submit_batch, fast path): a front pass
+    // (stages 5-7 of the batch into scratch buffers, on front_stream) yields
+    // each frame's first grey row read downstream; only rows from the batch's
+    // smallest such row down are copied. h2d_dma counts every H2D byte moved.
+    bool road_copy = true;
+    bool front_ready = false;
+    Dev front{};
+    LaunchPlan front_lp{};
+    cudaStream_t front_stream = nullptr;
+    cudaEvent_t front_done = nullptr;
+    int* d_rows = nullptr;  // [max_batch] first grey row per frame (H: none)
+    int* h_rows = nullptr;  // pinned copy
+    unsigned long long h2d_dma = 0;
 
     template <typename T>
     lk_status alloc(T** p, size_t count) {
@@ -574,6 +588,10 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
     if (e == cudaSuccess && d_nt)
         e = cudaMemcpy(d_nt, need_tab.data(), need_tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
     d.need_tab = d_nt;
+    if (e == cudaSuccess) {
+        const char* r = std::getenv("LK_ROAD_COPY");  // 0: streamed grey is copied whole
+        c->road_copy = !(r && std::atoi(r) == 0);
+    }
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     for (int i = 0; i < 13 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     {
@@ -615,6 +633,12 @@ lk_status lk_destroy(lk_ctx* c) {
     for (int k = 0; k < 2; ++k)
         for (cudaEvent_t e : {c->slot_copied[k], c->slot_free[k], c->slot_done[k]})
             if (e) cudaEventDestroy(e);
+    if (c->front_stream) {
+        cudaStreamSynchronize(c->front_stream);
+        cudaStreamDestroy(c->front_stream);
+    }
+    if (c->front_done) cudaEventDestroy(c->front_done);
+    if (c->h_rows) cudaFreeHost(c->h_rows);
     for (auto& kv : c->range_graphs) cudaGraphExecDestroy(kv.second);
     for (cudaEvent_t e : c->copied)
         if (e) cudaEventDestroy(e);
@@ -830,6 +854,7 @@ static lk_status run_host_pipelined(lk_ctx* c, const uint8_t* grey, const uint8_
                            cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(second + f0 * px, disp + f0 * px, (size_t)nf * px,
                            cudaMemcpyHostToDevice, st));
+        c->h2d_dma += 2 * (unsigned long long)nf * px;
         CU(cudaEventRecord(c->copied[k], st));
         if (k == 0) c->timed_frames = nf;
         if (c->flags & LK_FLAG_NO_GRAPH) {
@@ -918,10 +943,50 @@ static lk_status ensure_streaming(lk_ctx* c) {
     CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
         CU(cudaEventCreateWithFlags(&c->slot_copied[k], cudaEventDisableTiming));
-        CU(cudaEventCreateWithFlags(&c->slot_free[k], cudaEventDisableTiming));
+        // timing-enabled: a copy stream waiting on a DisableTiming event recorded
+        // after a graph launch was measured to serialise with the next batch
+        CU(cudaEventCreate(&c->slot_free[k]));
         CU(cudaEventCreateWithFlags(&c->slot_done[k], cudaEventDisableTiming));
         CU(cudaEventRecord(c->slot_free[k], c->stream));
     }
+    return LK_OK;
+}
+
+// First road-row copy: scratch outputs for the front pass (stages 5-7:
+// reports, v-disparity, v-path, beta inliers, V_py, f(v), mask row ranges;
+// the v-path choices in global memory so its CTAs need 6 KB of shared memory
+// and start beside the running batch), its stream (highest priority) and the
+// per-frame first-row array.
+static lk_status ensure_front(lk_ctx* c) {
+    if (c->front_ready) return LK_OK;
+    const size_t B = c->max_batch, H = c->d.H, D1 = c->d.D1;
+    c->front = c->d;
+    c->front_lp = c->lp;
+    Dev& f = c->front;
+    lk_status s = LK_OK;
+    auto A = [&](auto** p, size_t n) {
+        if (s == LK_OK) s = c->alloc(p, n);
+    };
+    A(&f.rep, B);
+    A(&f.aux, B);
+    A(&c->front_lp.vhistT, B * H * D1);
+    A(&f.vpath, B * D1 * 2);
+    A(&f.beta_inl, B * D1 * 2);
+    A(&f.vpy, B * H);
+    A(&f.vsing, B * H);
+    A(&f.fv, B * H);
+    A(&f.mrange, B * H);
+    A(&f.vchoice, B * D1 * H);
+    A(&c->d_rows, B);
+    if (s != LK_OK) return s;
+    c->front_lp.vpath_choice_smem = 0;
+    c->front_lp.vpath_smem = (size_t)2 * H * 8;
+    CU(cudaMallocHost((void**)&c->h_rows, B * sizeof(int)));
+    int least = 0, greatest = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CU(cudaStreamCreateWithPriority(&c->front_stream, cudaStreamNonBlocking, greatest));
+    CU(cudaEventCreateWithFlags(&c->front_done, cudaEventDisableTiming));
+    c->front_ready = true;
     return LK_OK;
 }
 
@@ -975,10 +1040,44 @@ static lk_status submit(lk_ctx* c, const uint8_t* a, const uint8_t* b, int n,
     c->next_slot ^= 1;
     const size_t bytes = (size_t)n * c->d.px;
     uint8_t* second = stereo ? c->slot_right[sl] : c->slot_disp[sl];
+    const bool road = !stereo && c->road_copy && c->lp.fast_front && !c->d.hooks;
+    if (road)
+        if (lk_status s = ensure_front(c)) return s;
     // inputs into the slot once the batch that last read it has finished
     CU(cudaStreamWaitEvent(c->copy_stream, c->slot_free[sl], 0));
-    CU(cudaMemcpyAsync(c->slot_grey[sl], a, bytes, cudaMemcpyHostToDevice, c->copy_stream));
-    CU(cudaMemcpyAsync(second, b, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+    if (!road) {
+        CU(cudaMemcpyAsync(c->slot_grey[sl], a, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+        CU(cudaMemcpyAsync(second, b, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+        c->h2d_dma += 2 * (unsigned long long)bytes;
+    } else {
+        // Road-row copy: the disparity first; stages 5-7 of this batch on the
+        // front stream give each frame's first grey row read by stages 8-12
+        // (horizon - 1 - rho: the mask is empty above the horizon,
+        // preprocess.hpp:18); the host waits for them (the previous batch keeps
+        // computing) and copies the rows from the batch's smallest one down.
+        // Rows above it stay stale in the slot and are never read.
+        CU(cudaMemcpyAsync(second, b, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+        CU(cudaEventRecord(c->slot_copied[sl], c->copy_stream));
+        cudaStream_t fs = c->front_stream;
+        CU(cudaStreamWaitEvent(fs, c->slot_copied[sl], 0));
+        Dev fd = c->front;
+        fd.disp = second;
+        CU(cudaMemsetAsync(fd.rep, 0, (size_t)n * sizeof(lk_frame_report), fs));
+        CU(cudaMemsetAsync(fd.aux, 0, (size_t)n * sizeof(FrameAux), fs));
+        CU(lkg::launch_road_front(fd, c->front_lp, n, c->d_rows, fs));
+        CU(cudaMemcpyAsync(c->h_rows, c->d_rows, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, fs));
+        CU(cudaEventRecord(c->front_done, fs));
+        CU(cudaEventSynchronize(c->front_done));
+        int r0 = c->d.H;
+        for (int i = 0; i < n; ++i) r0 = std::min(r0, c->h_rows[i]);
+        if (r0 < c->d.H) {
+            const size_t off = (size_t)r0 * c->d.W, w = c->d.px - off;
+            CU(cudaMemcpy2DAsync(c->slot_grey[sl] + off, c->d.px, a + off, c->d.px, w, (size_t)n,
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+            c->h2d_dma += (unsigned long long)w * n;
+        }
+        c->h2d_dma += bytes;
+    }
     CU(cudaEventRecord(c->slot_copied[sl], c->copy_stream));
     // kernels on the slot (graphs are keyed by slot), then the reports. A
     // stereo batch's stage 4 writes the context's disparity buffer as before.
@@ -1246,6 +1345,12 @@ lk_status lk_get_stage(lk_ctx* c, int frame, int stage, void* dst, size_t capaci
 }
 
 // Pinned host memory for end-to-end (host-fed) runs.
+lk_status lk_h2d_bytes(lk_ctx* c, unsigned long long* bytes) {
+    if (!c || !bytes) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
+    *bytes = c->h2d_dma;
+    return LK_OK;
+}
+
 lk_status lk_host_alloc(void** p, size_t bytes) {
     if (!p) return fail(LK_ERR_INVALID_ARGUMENT, "null argument");
     CU(cudaMallocHost(p, bytes));

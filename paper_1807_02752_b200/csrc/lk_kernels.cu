@@ -2307,6 +2307,27 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
     return cudaGetLastError();
 }
 
+// Road-row copy (lk_submit_batch): the first grey row stages 8-12 read per
+// frame, max(0, horizon - 1 - rho) (the Sobel's row above, the filter radius;
+// the mask is empty above the horizon, preprocess.hpp:18), or H for a frame
+// that failed in stages 5-7 (it reads no grey).
+__global__ void k_road_rows(Dev d, int n, int* rows) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= n) return;
+    rows[f] = frame_failed(d, f) ? d.H : min(max((int)d.rep[f].horizon - 1 - d.rho, 0), d.H);
+}
+
+// The front pass of a streamed batch: stages 5-7 into d's (scratch) buffers,
+// then k_road_rows. The batch's own graph recomputes stages 5-7 identically.
+cudaError_t launch_road_front(const Dev& d, const LaunchPlan& lp, int n, int* rows, cudaStream_t s) {
+    const int R = vdisparity_rows(d.W, d.D1);
+    k_vdisparity<<<dim3((d.H + R - 1) / R, n), 256, vdisparity_smem(d.W, d.D1), s>>>(d, lp.vhistT, R);
+    k_vpath<<<n, 512, lp.vpath_smem, s>>>(d, lp.vhistT, lp.vpath_choice_smem);
+    k_road_fit<<<n, 128, lp.road_smem, s>>>(d);
+    k_road_rows<<<(n + 127) / 128, 128, 0, s>>>(d, n, rows);
+    return cudaGetLastError();
+}
+
 void launch_exact_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s) {
     const dim3 g((d.W + BT_W - 1) / BT_W, (d.H + BT_H - 1) / BT_H, n);
     k_bilateral_tile<5, 0><<<g, 256, lp.bt_smem, s>>>(d, lp.ws);

@@ -92,6 +92,8 @@ int need_bilateral_ctas(int sm_count);
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all = 0);
 void launch_sobel_refine(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
 void launch_exact_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s);
+// stages 5-7 into d's (scratch) buffers + each frame's first grey row read downstream
+cudaError_t launch_road_front(const Dev& d, const LaunchPlan& lp, int n, int* rows, cudaStream_t s);
 cudaError_t fast_error(const Dev& d, int n, cudaStream_t s, double* out_dev);
 int launches_per_batch(const Dev& d, const LaunchPlan& lp);
 

@@ -58,6 +58,7 @@ def library() -> C.CDLL:
     L.lk_synchronize.argtypes = [P]
     L.lk_stream.argtypes = [P]
     L.lk_stream.restype = P
+    L.lk_h2d_bytes.argtypes = [P, C.POINTER(C.c_ulonglong)]
     L.lk_host_alloc.argtypes = [C.POINTER(P), SZ]
     L.lk_host_free.argtypes = [P]
     L.lk_abi_sizes.argtypes = [C.POINTER(SZ)]

@@ -205,6 +205,75 @@ def test_streaming_submit_wait_matches_run_batch():
             assert [bytes(r) for r in got[b]] == want[b], b
 
 
+def test_streaming_road_copy_matches_run_batch():
+    """lk_submit_batch from pinned buffers copies the disparity, runs stages 5-7
+    of the batch on a side stream and copies only the grey rows from the
+    batch's smallest horizon - 1 - rho down. The rows above stay stale in the
+    slot (here: noise from an earlier batch), so reports and the throughput-mode
+    hooks must still equal lk_run_batch's, on lane, stress (horizons 81..177),
+    stage-6 and stage-11 failure frames; lk_h2d_bytes counts exactly the
+    disparity plus those rows."""
+    import ctypes as C
+
+    from golden_util import apply_mutation
+
+    cfg = abi.default_config()
+    n, W, H = 8, 1242, 375
+    px = W * H
+    batches = []
+    for b in range(3):
+        params = [scenes.batch_scene(300 + 8 * b + i) for i in range(4)] + \
+                 [scenes.stress_scene(i) for i in range(4)]
+        g, d = lanekit.synth_batch(params, threads=8)
+        g, d = g.copy(), d.copy()
+        if b == 1:
+            apply_mutation("zero_disparity", g[2], d[2])
+            apply_mutation("flat_grey", g[5], d[5])
+        batches.append((g, d))
+    noise = np.random.default_rng(7).integers(0, 256, size=(n, H, W), dtype=np.uint8)
+    L = lanekit.library()
+    with lanekit.GpuPipeline(W, H, cfg, max_batch=n) as pipe:
+        want, want_hooks = [], []
+        for g, d in batches:
+            reps = pipe.run(g, d)
+            want.append([bytes(r) for r in reps])
+            want_hooks.append({(i, k): pipe.stage(i, k).tobytes() for i in range(n)
+                               for k in ("LANES", "ENERGY", "VOTES", "EDGES") if reps[i].status == 0})
+        pipe.run(noise, batches[0][1])  # slot 0's grey: noise above every horizon
+        bufs = []
+        for g, d in batches:
+            pg, pd = C.c_void_p(), C.c_void_p()
+            assert L.lk_host_alloc(C.byref(pg), g.nbytes) == abi.LK_OK
+            assert L.lk_host_alloc(C.byref(pd), d.nbytes) == abi.LK_OK
+            C.memmove(pg, g.ctypes.data, g.nbytes)
+            C.memmove(pd, d.ctypes.data, d.nbytes)
+            bufs.append((pg, pd))
+        got = [(abi.LkFrameReport * n)() for _ in batches]
+        h0, h1 = C.c_ulonglong(0), C.c_ulonglong(0)
+        assert L.lk_h2d_bytes(pipe._h, C.byref(h0)) == abi.LK_OK
+        for b, (pg, pd) in enumerate(bufs):  # the third submit waits for the first
+            assert L.lk_submit_batch(pipe._h, pg, pd, n, got[b]) == abi.LK_OK, L.lk_last_error()
+        for _ in batches[1:]:
+            assert L.lk_wait_batch(pipe._h) in (abi.LK_OK, abi.LK_ERR_FRAME)
+        assert L.lk_h2d_bytes(pipe._h, C.byref(h1)) == abi.LK_OK
+        for b in range(len(batches)):
+            assert [bytes(r) for r in got[b]] == want[b], b
+        last = len(batches) - 1
+        pipe.reports = list(got[last])  # stage() decodes with the last batch's horizons
+        for (i, k), v in want_hooks[last].items():
+            assert pipe.stage(i, k).tobytes() == v, (i, k)
+        expect = 0
+        for b in range(len(batches)):
+            rows = [H if (r.status and r.failed_stage <= 7) else min(max(int(r.horizon) - 6, 0), H)
+                    for r in got[b]]
+            expect += n * px + n * (H - min(rows)) * W
+        assert h1.value - h0.value == expect
+        assert expect < 2 * px * n * len(batches)  # rows above the horizons were not copied
+        for pg, pd in bufs:
+            L.lk_host_free(pg)
+            L.lk_host_free(pd)
+
+
 def test_headline_batch_256_vs_reference(oracle):
     """All 256 frames of the bench's config-2 batch (batch_scene seeds 1..256,
     bench.py make_frames) through the throughput path in one batch, against
