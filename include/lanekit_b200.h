@@ -317,12 +317,13 @@ lk_status lk_fast_path_error(lk_ctx* ctx, double* max_abs_error);
 
 /* Host-to-device bytes the context has copied so far (host-fed inputs). On
  * the streaming fast path (lk_submit_batch, no LK_FLAG_HOOKS) a batch's grey
- * is copied only from row min_f(horizon_f - 1 - rho) down: the disparity is
- * copied first, stages 5-7 of the batch run on a side stream, and the call
- * waits for them (the previous batch keeps computing) before queuing the grey
- * rows stages 8-12 read (the mask is empty above the horizon,
- * preprocess.hpp:18). LK_ROAD_COPY=0 in the environment at lk_create copies
- * whole frames and returns without waiting. */
+ * is copied only from row min_f(horizon_f - 1 - rho) down, per frame chunk
+ * (LK_ROAD_CHUNKS, default 2): the chunk's disparity is copied first, stages
+ * 5-7 of the chunk run on a side stream, and the call waits for them (the
+ * previous batch keeps computing) before queuing the grey rows stages 8-12
+ * read (the mask is empty above the horizon, preprocess.hpp:18).
+ * LK_ROAD_COPY=0 in the environment at lk_create copies whole frames and
+ * returns without waiting. */
 lk_status lk_h2d_bytes(lk_ctx* ctx, unsigned long long* bytes);
 
 /* Page-locked host buffers for host-fed (end-to-end) runs. */

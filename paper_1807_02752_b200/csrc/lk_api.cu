@@ -134,7 +134,9 @@ struct lk_ctx {
     Dev front{};
     LaunchPlan front_lp{};
     cudaStream_t front_stream = nullptr;
-    cudaEvent_t front_done = nullptr;
+    cudaEvent_t front_done[kMaxBranches] = {};
+    cudaEvent_t disp_copied[kMaxBranches] = {};
+    int road_chunks = 2;  // frame chunks of the road-row copy (LK_ROAD_CHUNKS)
     int* d_rows = nullptr;  // [max_batch] first grey row per frame (H: none)
     int* h_rows = nullptr;  // pinned copy
     unsigned long long h2d_dma = 0;
@@ -637,7 +639,10 @@ lk_status lk_destroy(lk_ctx* c) {
         cudaStreamSynchronize(c->front_stream);
         cudaStreamDestroy(c->front_stream);
     }
-    if (c->front_done) cudaEventDestroy(c->front_done);
+    for (int k = 0; k < kMaxBranches; ++k) {
+        if (c->front_done[k]) cudaEventDestroy(c->front_done[k]);
+        if (c->disp_copied[k]) cudaEventDestroy(c->disp_copied[k]);
+    }
     if (c->h_rows) cudaFreeHost(c->h_rows);
     for (auto& kv : c->range_graphs) cudaGraphExecDestroy(kv.second);
     for (cudaEvent_t e : c->copied)
@@ -680,10 +685,9 @@ lk_status lk_device_inputs(lk_ctx* c, uint8_t** grey, uint8_t** disparity) {
 
 // View of frames [f0, f0 + ...) of every frame-major buffer: the same kernels
 // run on a sub-batch without knowing it (layouts are frame-major throughout).
-static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
-    const Dev& d = c->d;
+static void view_of(const Dev& d, const LaunchPlan& dlp, size_t f0, Dev& v, LaunchPlan& lp) {
     v = d;
-    lp = c->lp;
+    lp = dlp;
     const size_t H = d.H, px = d.px, C = d.ext_cols, D1 = d.D1;
     auto sh = [&](auto& p, size_t per) {
         if (p) p += f0 * per;
@@ -749,6 +753,10 @@ static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
     sh(v.theta, px);
     sh(v.acc, H * C);
     sh(v.m0, px);
+}
+
+static void frame_view(const lk_ctx* c, size_t f0, Dev& v, LaunchPlan& lp) {
+    view_of(c->d, c->lp, f0, v, lp);
 }
 
 static lk_status enqueue_range(lk_ctx* c, size_t f0, int n, cudaStream_t st, cudaEvent_t* ev) {
@@ -985,7 +993,12 @@ static lk_status ensure_front(lk_ctx* c) {
     int least = 0, greatest = 0;
     CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     CU(cudaStreamCreateWithPriority(&c->front_stream, cudaStreamNonBlocking, greatest));
-    CU(cudaEventCreateWithFlags(&c->front_done, cudaEventDisableTiming));
+    for (int k = 0; k < kMaxBranches; ++k) {
+        CU(cudaEventCreateWithFlags(&c->front_done[k], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->disp_copied[k], cudaEventDisableTiming));
+    }
+    if (const char* r = std::getenv("LK_ROAD_CHUNKS"))
+        c->road_chunks = std::max(1, std::min(kMaxBranches, std::atoi(r)));
     c->front_ready = true;
     return LK_OK;
 }
@@ -1056,25 +1069,42 @@ static lk_status submit(lk_ctx* c, const uint8_t* a, const uint8_t* b, int n,
         // preprocess.hpp:18); the host waits for them (the previous batch keeps
         // computing) and copies the rows from the batch's smallest one down.
         // Rows above it stay stale in the slot and are never read.
-        CU(cudaMemcpyAsync(second, b, bytes, cudaMemcpyHostToDevice, c->copy_stream));
-        CU(cudaEventRecord(c->slot_copied[sl], c->copy_stream));
+        // In frame chunks, so chunk k's grey copy is queued while chunk k+1's
+        // stages 5-7 run and the link does not wait for them.
+        const size_t px = c->d.px;
+        int nk = c->road_chunks;
+        while (nk > 1 && n / nk < 4) --nk;
         cudaStream_t fs = c->front_stream;
-        CU(cudaStreamWaitEvent(fs, c->slot_copied[sl], 0));
-        Dev fd = c->front;
-        fd.disp = second;
-        CU(cudaMemsetAsync(fd.rep, 0, (size_t)n * sizeof(lk_frame_report), fs));
-        CU(cudaMemsetAsync(fd.aux, 0, (size_t)n * sizeof(FrameAux), fs));
-        CU(lkg::launch_road_front(fd, c->front_lp, n, c->d_rows, fs));
-        CU(cudaMemcpyAsync(c->h_rows, c->d_rows, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, fs));
-        CU(cudaEventRecord(c->front_done, fs));
-        CU(cudaEventSynchronize(c->front_done));
-        int r0 = c->d.H;
-        for (int i = 0; i < n; ++i) r0 = std::min(r0, c->h_rows[i]);
-        if (r0 < c->d.H) {
-            const size_t off = (size_t)r0 * c->d.W, w = c->d.px - off;
-            CU(cudaMemcpy2DAsync(c->slot_grey[sl] + off, c->d.px, a + off, c->d.px, w, (size_t)n,
-                                 cudaMemcpyHostToDevice, c->copy_stream));
-            c->h2d_dma += (unsigned long long)w * n;
+        for (int k = 0, f0 = 0; k < nk; ++k) {
+            const int nf = n / nk + (k < n % nk);
+            CU(cudaMemcpyAsync(second + (size_t)f0 * px, b + (size_t)f0 * px, (size_t)nf * px,
+                               cudaMemcpyHostToDevice, c->copy_stream));
+            CU(cudaEventRecord(c->disp_copied[k], c->copy_stream));
+            CU(cudaStreamWaitEvent(fs, c->disp_copied[k], 0));
+            Dev fd;
+            LaunchPlan flp;
+            view_of(c->front, c->front_lp, (size_t)f0, fd, flp);
+            fd.disp = second + (size_t)f0 * px;
+            CU(cudaMemsetAsync(fd.rep, 0, (size_t)nf * sizeof(lk_frame_report), fs));
+            CU(cudaMemsetAsync(fd.aux, 0, (size_t)nf * sizeof(FrameAux), fs));
+            CU(lkg::launch_road_front(fd, flp, nf, c->d_rows + f0, fs));
+            CU(cudaMemcpyAsync(c->h_rows + f0, c->d_rows + f0, (size_t)nf * sizeof(int),
+                               cudaMemcpyDeviceToHost, fs));
+            CU(cudaEventRecord(c->front_done[k], fs));
+            f0 += nf;
+        }
+        for (int k = 0, f0 = 0; k < nk; ++k) {
+            const int nf = n / nk + (k < n % nk);
+            CU(cudaEventSynchronize(c->front_done[k]));
+            int r0 = c->d.H;
+            for (int i = f0; i < f0 + nf; ++i) r0 = std::min(r0, c->h_rows[i]);
+            if (r0 < c->d.H) {
+                const size_t off = (size_t)f0 * px + (size_t)r0 * c->d.W, w = px - (size_t)r0 * c->d.W;
+                CU(cudaMemcpy2DAsync(c->slot_grey[sl] + off, px, a + off, px, w, (size_t)nf,
+                                     cudaMemcpyHostToDevice, c->copy_stream));
+                c->h2d_dma += (unsigned long long)w * nf;
+            }
+            f0 += nf;
         }
         c->h2d_dma += bytes;
     }

@@ -208,7 +208,7 @@ def test_streaming_submit_wait_matches_run_batch():
 def test_streaming_road_copy_matches_run_batch():
     """lk_submit_batch from pinned buffers copies the disparity, runs stages 5-7
     of the batch on a side stream and copies only the grey rows from the
-    batch's smallest horizon - 1 - rho down. The rows above stay stale in the
+    chunk's smallest horizon - 1 - rho down. The rows above stay stale in the
     slot (here: noise from an earlier batch), so reports and the throughput-mode
     hooks must still equal lk_run_batch's, on lane, stress (horizons 81..177),
     stage-6 and stage-11 failure frames; lk_h2d_bytes counts exactly the
@@ -266,7 +266,9 @@ def test_streaming_road_copy_matches_run_batch():
         for b in range(len(batches)):
             rows = [H if (r.status and r.failed_stage <= 7) else min(max(int(r.horizon) - 6, 0), H)
                     for r in got[b]]
-            expect += n * px + n * (H - min(rows)) * W
+            expect += n * px
+            for c0 in range(0, n, 4):  # two chunks of 4 frames (LK_ROAD_CHUNKS = 2)
+                expect += 4 * (H - min(rows[c0:c0 + 4])) * W
         assert h1.value - h0.value == expect
         assert expect < 2 * px * n * len(batches)  # rows above the horizons were not copied
         for pg, pd in bufs:
