@@ -322,8 +322,10 @@ lk_status lk_fast_path_error(lk_ctx* ctx, double* max_abs_error);
  * 5-7 of the chunk run on a side stream, and the call waits for them (the
  * previous batch keeps computing) before queuing the grey rows stages 8-12
  * read (the mask is empty above the horizon, preprocess.hpp:18).
- * LK_ROAD_COPY=0 in the environment at lk_create copies whole frames and
- * returns without waiting. */
+ * After a batch whose rows above the horizons were < 15 % of its grey (a
+ * high-resolution frame with a high horizon), whole frames are copied without
+ * waiting, re-probing every 16th batch. LK_ROAD_COPY=0 in the environment at
+ * lk_create always copies whole frames. */
 lk_status lk_h2d_bytes(lk_ctx* ctx, unsigned long long* bytes);
 
 /* Page-locked host buffers for host-fed (end-to-end) runs. */

@@ -137,6 +137,8 @@ struct lk_ctx {
     cudaEvent_t front_done[kMaxBranches] = {};
     cudaEvent_t disp_copied[kMaxBranches] = {};
     int road_chunks = 2;  // frame chunks of the road-row copy (LK_ROAD_CHUNKS)
+    double road_saved = 1.0;  // fraction of the grey the last road-row copy skipped
+    unsigned road_probe = 0;
     int* d_rows = nullptr;  // [max_batch] first grey row per frame (H: none)
     int* h_rows = nullptr;  // pinned copy
     unsigned long long h2d_dma = 0;
@@ -1053,7 +1055,11 @@ static lk_status submit(lk_ctx* c, const uint8_t* a, const uint8_t* b, int n,
     c->next_slot ^= 1;
     const size_t bytes = (size_t)n * c->d.px;
     uint8_t* second = stereo ? c->slot_right[sl] : c->slot_disp[sl];
-    const bool road = !stereo && c->road_copy && c->lp.fast_front && !c->d.hooks;
+    // (the front pass and the wait pay off only when the horizon is low enough:
+    // after a batch that skipped < 15 % of its grey rows, whole frames again,
+    // re-probing every 16th batch)
+    const bool road = !stereo && c->road_copy && c->lp.fast_front && !c->d.hooks &&
+                      (c->road_saved >= 0.15 || (++c->road_probe & 15) == 0);
     if (road)
         if (lk_status s = ensure_front(c)) return s;
     // inputs into the slot once the batch that last read it has finished
@@ -1093,6 +1099,7 @@ static lk_status submit(lk_ctx* c, const uint8_t* a, const uint8_t* b, int n,
             CU(cudaEventRecord(c->front_done[k], fs));
             f0 += nf;
         }
+        unsigned long long copied = 0;
         for (int k = 0, f0 = 0; k < nk; ++k) {
             const int nf = n / nk + (k < n % nk);
             CU(cudaEventSynchronize(c->front_done[k]));
@@ -1103,10 +1110,12 @@ static lk_status submit(lk_ctx* c, const uint8_t* a, const uint8_t* b, int n,
                 CU(cudaMemcpy2DAsync(c->slot_grey[sl] + off, px, a + off, px, w, (size_t)nf,
                                      cudaMemcpyHostToDevice, c->copy_stream));
                 c->h2d_dma += (unsigned long long)w * nf;
+                copied += (unsigned long long)w * nf;
             }
             f0 += nf;
         }
         c->h2d_dma += bytes;
+        c->road_saved = 1.0 - (double)copied / (double)bytes;
     }
     CU(cudaEventRecord(c->slot_copied[sl], c->copy_stream));
     // kernels on the slot (graphs are keyed by slot), then the reports. A
