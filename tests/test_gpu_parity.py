@@ -306,6 +306,34 @@ def test_headline_batch_256_vs_reference(oracle):
     assert [r.uncertain for r in reps] == [0] * 256  # every lane decision certified
 
 
+def test_stress_batch_64_vs_reference(oracle):
+    """Config 3 at batch scale: 64 obstacle / pitch-change frames (stress_scene
+    seeds 300..363, all four pitch variants, 1-4 obstacle boxes) through the
+    throughput path in one batch, against the reference's own code: every
+    report field and the throughput-mode hooks, and every lane decision
+    certified."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from checkers import Checker, ref_available
+
+    chk = Checker("ref") if ref_available() else oracle
+    params = [scenes.stress_scene(i) for i in range(64)]
+    grey, disp = lanekit.synth_batch(params, threads=8)
+    cfg = abi.default_config()
+    problems = []
+    with lanekit.GpuPipeline(1242, 375, cfg, max_batch=64) as pipe, ThreadPoolExecutor(8) as pool:
+        reps = pipe.run(grey, disp)
+        for c0 in range(0, 64, 16):
+            res = list(pool.map(lambda i: chk.run(grey[i], disp[i], cfg), range(c0, c0 + 16)))
+            for i, o in zip(range(c0, c0 + 16), res):
+                p = compare_reports(reps[i], o.report)
+                p += compare_frame(lambda name: pipe.stage(i, name), o, hooks=False)
+                problems += [f"frame {i}: {x}" for x in p]
+            del res
+    assert not problems, "\n".join(problems[:20])
+    assert [r.uncertain for r in reps] == [0] * 64
+
+
 def test_certificate_zero_on_batch_and_fires_on_a_tie(oracle):
     """lk_frame_report.uncertain: 0 on config-2 and stress frames (no lane
     decision within the libdevice-vs-glibc error bounds), and > 0 when the
