@@ -334,6 +334,30 @@ def test_stress_batch_64_vs_reference(oracle):
     assert [r.uncertain for r in reps] == [0] * 64
 
 
+def test_hires_batch_8_vs_reference(oracle):
+    """Config 4 (2560x1024, d_max 248, lambda_g 1, lane separation 150): eight
+    frames in one throughput-mode batch against the reference's own code,
+    every report field and the throughput-mode hooks."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from checkers import Checker, ref_available
+
+    chk = Checker("ref") if ref_available() else oracle
+    params = [scenes.hires_scene(i) for i in range(8)]
+    grey, disp = lanekit.synth_batch(params, threads=8)
+    cfg = scenes.hires_config()
+    with lanekit.GpuPipeline(2560, 1024, cfg, max_batch=8) as pipe, ThreadPoolExecutor(8) as pool:
+        reps = pipe.run(grey, disp)
+        res = list(pool.map(lambda i: chk.run(grey[i], disp[i], cfg), range(8)))
+        problems = []
+        for i, o in enumerate(res):
+            p = compare_reports(reps[i], o.report)
+            p += compare_frame(lambda name: pipe.stage(i, name), o, hooks=False)
+            problems += [f"frame {i}: {x}" for x in p]
+    assert not problems, "\n".join(problems[:20])
+    assert all(r.status == 0 and r.lane_count >= 2 for r in reps)
+
+
 def test_certificate_zero_on_batch_and_fires_on_a_tie(oracle):
     """lk_frame_report.uncertain: 0 on config-2 and stress frames (no lane
     decision within the libdevice-vs-glibc error bounds), and > 0 when the
