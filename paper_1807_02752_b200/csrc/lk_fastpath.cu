@@ -768,7 +768,17 @@ size_t prescreen_smem(int W, int nt) {
            (size_t)(PQ_PFD + 1) * 8;
 }
 
-int prescreen_segments(int H) { return H >= 128 ? 2 : 1; }
+// Row segments per frame: 2 for batches that fill the GPU; small batches
+// (the drop-in's one frame at a time) split each frame's walk further, so the
+// latency of a batch is a few short walks instead of one long one (each
+// segment re-reads its 11-row window head, ~12 rows of extra work).
+int prescreen_segments(int H, int n) {
+    if (H < 128) return 1;
+    if (n >= 16) return 2;
+    const int s = 32 / (n < 1 ? 1 : n);
+    const int cap = H / 24;  // segments of at least 24 rows
+    return s < 2 ? 2 : s > cap ? (cap < 2 ? 2 : cap) : s;
+}
 
 int prescreen_threads(int W) {
     const int qlast = (W - 1) >> 2;
@@ -954,7 +964,7 @@ int need_bilateral_ctas(int sm_count) {
 // bilateral of its need pixels (all = 1: every pixel, for lk_fast_path_error).
 void launch_fast_bilateral(const Dev& d, const LaunchPlan& lp, int n, cudaStream_t s, int all) {
     if (!all)
-        k_prescreen<<<dim3(n, prescreen_segments(d.H)), prescreen_threads(d.W),
+        k_prescreen<<<dim3(n, prescreen_segments(d.H, n)), prescreen_threads(d.W),
                       prescreen_smem(d.W, prescreen_threads(d.W)), s>>>(d, lp.ps);
     k_bilateral_need<<<lp.need_ctas, 256, kNeedTabSmem, s>>>(d, lp.nbf, n, all);
 }
