@@ -1599,26 +1599,42 @@ __global__ void __launch_bounds__(256) k_m0_m1(Dev d, int tile_h, int want_hist)
         // columns they span. Consecutive lanes' loads are then contiguous (16 B
         // apart): with 4 outputs per thread they were 32 B apart and every
         // load took twice the shared-memory wavefronts (ncu: 25 M conflicts).
-        constexpr int Q = 2;
+        // A thread also covers R consecutive rows: each staged row it loads
+        // feeds every one of its R x Q outputs whose window holds it (rows
+        // r .. r + 2 vs in increasing order, columns x-minor, as before), so
+        // R outputs share their overlapping rows' loads.
+        constexpr int Q = 2, R = 6;
         const int per_row = (MW + Q - 1) / Q;
-        for (int i = threadIdx.x; i < MH * per_row; i += blockDim.x) {
-            const int r = i / per_row, c = (i - r * per_row) * Q;
-            const double2* g0 = reinterpret_cast<const double2*>(gw + r * GW + c);  // 16-byte aligned
-            double s[Q] = {0.0, 0.0};
-            for (int y = 0; y <= 2 * vs; ++y) {
-                const double2 a = g0[0], b = g0[1];  // columns c .. c+3
+        const int ngrp = (MH + R - 1) / R;
+        for (int i = threadIdx.x; i < ngrp * per_row; i += blockDim.x) {
+            const int rg = i / per_row, c = (i - rg * per_row) * Q;
+            const int r0 = rg * R, rn = min(R, MH - r0);
+            const double2* g0 = reinterpret_cast<const double2*>(gw + r0 * GW + c);  // 16-byte aligned
+            double s[R][Q];
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) s[rr][0] = s[rr][1] = 0.0;
+            for (int y = 0; y < rn + 2 * vs; ++y) {
+                const double2 a = g0[0], b = g0[1];  // columns c .. c+3 of staged row r0 + y
                 const double g[4] = {a.x, a.y, b.x, b.y};
 #pragma unroll
-                for (int k = 0; k < Q; ++k) {
-                    s[k] += g[k];
-                    s[k] += g[k + 1];
-                    s[k] += g[k + 2];
+                for (int rr = 0; rr < R; ++rr) {
+                    const int dy = y - rr;  // the window row of output row r0 + rr
+                    if (dy >= 0 && dy <= 2 * vs) {
+#pragma unroll
+                        for (int k = 0; k < Q; ++k) {
+                            s[rr][k] += g[k];
+                            s[rr][k] += g[k + 1];
+                            s[rr][k] += g[k + 2];
+                        }
+                    }
                 }
                 g0 += GW / 2;
             }
 #pragma unroll
-            for (int k = 0; k < Q; ++k)
-                if (c + k < MW) m0[r * MW + c + k] = s[k];
+            for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+                for (int k = 0; k < Q; ++k)
+                    if (rr < rn && c + k < MW) m0[(r0 + rr) * MW + c + k] = s[rr][k];
         }
     } else {
         for (int i = threadIdx.x; i < MH * MW; i += blockDim.x) {
