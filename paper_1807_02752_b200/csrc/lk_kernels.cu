@@ -1223,6 +1223,70 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
 #ifdef LK_VANISH_PROF
     const long long t1 = clock64();
 #endif
+    if (SP > 0 && use_int && !d.hooks) {
+        // The product loop (int keys, no hooks), with the per-stage work cut
+        // to the DP itself: the offsets' key constants in registers, the
+        // thread's window / counts / choice row as running pointers, stage 0
+        // peeled, no per-state bound test for threads whose states are all
+        // inside [0, C). Same operations per state as upath_stage<SP, true>.
+        constexpr int S = SP > 0 ? SP : 1;
+        int* pv = (int*)prev;
+        int* cu = (int*)cur;
+        const int s0 = threadIdx.x * S;
+        const bool act = s0 < C, full = s0 + S <= C;
+        int uk[11];
+#pragma unroll
+        for (int oi = 0; oi < 11; ++oi) uk[oi] = d.upk[oi];
+        for (int c = threadIdx.x; c < C; c += blockDim.x) pv[c] = nrv_i * cnt0[c];  // stage 0
+        if (nrows > 1) {  // cnt1: band(-1) (empty) -> band(1)
+            int t1b, b1b;
+            band(1, t1b, b1b);
+            slide(cnt1, tm1, bm1, t1b, b1b);
+            tm1 = t0b;
+            bm1 = b0b;
+            t0b = t1b;
+            b0b = b1b;
+        }
+        __syncthreads();
+        int8_t* ch = choice + C + s0;  // stage 1's choice row
+        for (int stg = 1; stg < nrows; ++stg) {
+            const int* cn = ((stg & 1) ? cnt1 : cnt0) + s0;
+            if (act) {
+                int w16[S + 10];
+                const int* pw = pv + s0 - 5;  // 5 sentinels on each side of the rows
+#pragma unroll
+                for (int k = 0; k < S + 10; ++k) w16[k] = pw[k];
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    if (!full && s0 + j >= C) break;
+                    int key[11];
+#pragma unroll
+                    for (int oi = 0; oi < 11; ++oi) key[oi] = w16[j + 5 + upath_off(oi)] + uk[oi];
+                    const int m0 = __vimin3_s32(key[0], key[1], key[2]);
+                    const int m1 = __vimin3_s32(key[3], key[4], key[5]);
+                    const int m2 = __vimin3_s32(key[6], key[7], key[8]);
+                    const int best = __vimin3_s32(__vimin3_s32(m0, m1, m2), key[9], key[10]);
+                    cu[s0 + j] = (best & ~15) + nrv_i * cn[j];
+                    ch[j] = (int8_t)(best & 15);
+                }
+            }
+            if (stg + 1 < nrows) {  // other buffer: band(stg - 1) -> band(stg + 1)
+                int t1b, b1b;
+                band(stg + 1, t1b, b1b);
+                slide((stg & 1) ? cnt0 : cnt1, tm1, bm1, t1b, b1b);
+                tm1 = t0b;
+                bm1 = b0b;
+                t0b = t1b;
+                b0b = b1b;
+            }
+            __syncthreads();
+            int* t = pv;
+            pv = cu;
+            cu = t;
+            ch += C;
+        }
+        prev = (double*)pv;  // the last stage's energies (read below)
+    } else
     for (int stg = 0; stg < nrows; ++stg) {
 #ifdef LK_VANISH_PROF
         const long long tb = clock64();
