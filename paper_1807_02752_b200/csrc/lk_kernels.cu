@@ -1270,10 +1270,22 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
                     ch[j] = (int8_t)(best & 15);
                 }
             }
-            if (stg + 1 < nrows) {  // other buffer: band(stg - 1) -> band(stg + 1)
+            // warp 0 alone slides the other buffer, band(stg - 1) -> band(stg + 1)
+            // (a row holds a few dozen votes: one or two lane strides), so the
+            // other warps issue only their DP
+            if (stg + 1 < nrows && threadIdx.x < 32) {
                 int t1b, b1b;
                 band(stg + 1, t1b, b1b);
-                slide((stg & 1) ? cnt0 : cnt1, tm1, bm1, t1b, b1b);
+                int* cb = (stg & 1) ? cnt0 : cnt1;
+                auto wslide = [&](int e0, int e1, int dlt) {
+                    for (int e = e0 + (int)threadIdx.x; e < e1; e += 32) {
+                        const int c = staged ? (int)s_vcol[e - e_first]
+                                             : (ecol[e] == kSkipCol ? 0xffff : ecol[e] - d.ext_lo);
+                        if (c != 0xffff) atomicAdd(&cb[c], dlt);
+                    }
+                };
+                if (t1b < tm1) wslide(roff[t1b], roff[tm1], 1);             // rows entering
+                if (b1b < bm1) wslide(roff[b1b + 1], roff[bm1 + 1], -1);    // rows leaving
                 tm1 = t0b;
                 bm1 = b0b;
                 t0b = t1b;
