@@ -525,12 +525,26 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
             A(&d.ctile_cnt, (size_t)B);
         }
     }
-    lp.vanish_smem = (size_t)(2 * C + 32) * 8 + (size_t)2 * C * 4 + (size_t)2 * H * 4 +
-                     (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 8 + (size_t)(H + 1) * 4 +
-                     (size_t)lkg::K4_VOTE_CAP * 2 + 16;
     // u-path DP shape: 512 threads (2 CTAs / SM) up to 4096 extended columns,
     // else 1024 threads; SP consecutive states per thread (0 = strided fallback)
     lp.upath_nt = C <= 512 * 8 ? 512 : 1024;
+    {
+        // vote columns staged in shared memory (2 B each): 8 K votes keep two
+        // 512-thread CTAs per SM; a 1024-thread DP runs alone on its SM and
+        // takes as many as fit (a hi-res frame has ~15 K; unstaged, the band
+        // slide waits on a global load every stage)
+        const size_t base = (size_t)(2 * C + 32) * 8 + (size_t)2 * C * 4 + (size_t)2 * H * 4 +
+                            (size_t)lkg::BT_CHUNK * (2 * lkg::BT_SPAN + 1) + 8 +
+                            (size_t)(H + 1) * 4 + 16;
+        size_t cap = lkg::K4_VOTE_CAP;
+        if (lp.upath_nt == 1024) {
+            const size_t room = prop.sharedMemPerBlockOptin > base + 2048
+                                    ? (prop.sharedMemPerBlockOptin - base - 2048) / 2 : 0;
+            cap = std::max(cap, std::min(room, (size_t)32768) & ~(size_t)15);
+        }
+        d.vote_cap = (int)cap;
+        lp.vanish_smem = base + cap * 2;
+    }
     lp.upath_sp = (C + lp.upath_nt - 1) / lp.upath_nt;
     if (lp.upath_sp == 7) lp.upath_sp = 8;
     if (lp.upath_nt == 1024 && lp.upath_sp < 5) lp.upath_sp = 5;

@@ -111,6 +111,7 @@ struct Dev {
     double* m1;             // [B][H][W] (only tiles flagged in m1_nz are written)
     uint8_t* m1_nz;         // [B][m_nty][m_ntx] m0/m1 tile has a non-zero
     int m_tile_shift, m_ntx, m_nty;  // m0/m1 tile: (1 << m_tile_shift) rows x M_TW cols
+    int vote_cap;           // k_vanish: vote columns staged in shared memory
     unsigned int* p99hist;  // [B][2048]
     unsigned int* p99hist2; // [B][4096]
     unsigned long long* p99cand;  // [B][px]

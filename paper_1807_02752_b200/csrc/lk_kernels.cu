@@ -1139,7 +1139,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
     int* pv = px + H;
     int8_t* win = (int8_t*)(pv + H);  // [BT_CHUNK][2*BT_SPAN+1]
     int* s_roff = (int*)(win + BT_CHUNK * (2 * BT_SPAN + 1) + 4 - (BT_CHUNK * (2 * BT_SPAN + 1)) % 4);
-    uint16_t* s_vcol = (uint16_t*)(s_roff + H + 1);  // [K4_VOTE_CAP] vote column - ext_lo
+    uint16_t* s_vcol = (uint16_t*)(s_roff + H + 1);  // [d.vote_cap] vote column - ext_lo
     __shared__ double sv[32];
     __shared__ int si[32];
     __shared__ int s_votes;
@@ -1152,7 +1152,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
     int8_t* choice = d.uchoice + (size_t)f * H * C;
     // per-row vote lists staged once (the band updates of every stage read them)
     const int e_first = groff[v_top], n_edges_in = groff[H] - e_first;
-    const bool staged = n_edges_in <= K4_VOTE_CAP;
+    const bool staged = n_edges_in <= d.vote_cap;
     for (int r = threadIdx.x; r <= H; r += blockDim.x) s_roff[r] = groff[r];
     if (staged)
         for (int e = threadIdx.x; e < n_edges_in; e += blockDim.x) {
