@@ -545,10 +545,22 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         d.vote_cap = (int)cap;
         lp.vanish_smem = base + cap * 2;
     }
-    lp.upath_sp = (C + lp.upath_nt - 1) / lp.upath_nt;
-    if (lp.upath_sp == 7) lp.upath_sp = 8;
-    if (lp.upath_nt == 1024 && lp.upath_sp < 5) lp.upath_sp = 5;
-    if (lp.upath_sp > 8) lp.upath_sp = 0;
+    {
+        // SP consecutive states per thread over NT/32 - 1 warps: the last warp
+        // holds no states and slides the band counts alone (k_vanish's product
+        // loop; measured 419 -> 382 us KITTI, 1348 -> 1093 us hi-res against
+        // warp 0 sliding beside its DP). Without room for it, every warp.
+        const int nt = lp.upath_nt;
+        int sp = (C + nt - 33) / (nt - 32);
+        if (sp == 7) sp = 8;
+        if (sp > 8) {
+            sp = (C + nt - 1) / nt;
+            if (sp == 7) sp = 8;
+        }
+        if (nt == 1024 && sp < 5) sp = 5;
+        lp.upath_sp = sp > 8 ? 0 : sp;
+        if (const char* e = std::getenv("LK_VANISH_SP")) lp.upath_sp = std::atoi(e);  // experiment
+    }
     lp.gamma_smem = (size_t)(GAMMA_NW + 4) * H * 4 + 8 + (size_t)6 * H * 8 + 16;  // px, pv, NW+2 lists, basis rows
     lp.m_tile_h = 16;
     auto m_bytes = [&](int th) {

@@ -1234,6 +1234,9 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
         int* cu = (int*)cur;
         const int s0 = threadIdx.x * S;
         const bool act = s0 < C, full = s0 + S <= C;
+        // the band slide goes to a warp without states when there is one (the
+        // DP warps then issue only their DP), else to warp 0
+        const int slide_warp = ((NT / 32 - 1) * 32) * S >= C ? NT / 32 - 1 : 0;
         int uk[11];
 #pragma unroll
         for (int oi = 0; oi < 11; ++oi) uk[oi] = d.upk[oi];
@@ -1273,12 +1276,12 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_vanish(Dev d) {
             // warp 0 alone slides the other buffer, band(stg - 1) -> band(stg + 1)
             // (a row holds a few dozen votes: one or two lane strides), so the
             // other warps issue only their DP
-            if (stg + 1 < nrows && threadIdx.x < 32) {
+            if (stg + 1 < nrows && (int)(threadIdx.x >> 5) == slide_warp) {
                 int t1b, b1b;
                 band(stg + 1, t1b, b1b);
                 int* cb = (stg & 1) ? cnt0 : cnt1;
                 auto wslide = [&](int e0, int e1, int dlt) {
-                    for (int e = e0 + (int)threadIdx.x; e < e1; e += 32) {
+                    for (int e = e0 + (int)(threadIdx.x & 31); e < e1; e += 32) {
                         const int c = staged ? (int)s_vcol[e - e_first]
                                              : (ecol[e] == kSkipCol ? 0xffff : ecol[e] - d.ext_lo);
                         if (c != 0xffff) atomicAdd(&cb[c], dlt);
