@@ -559,7 +559,6 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         }
         if (nt == 1024 && sp < 5) sp = 5;
         lp.upath_sp = sp > 8 ? 0 : sp;
-        if (const char* e = std::getenv("LK_VANISH_SP")) lp.upath_sp = std::atoi(e);  // experiment
     }
     lp.gamma_smem = (size_t)(GAMMA_NW + 4) * H * 4 + 8 + (size_t)6 * H * 8 + 16;  // px, pv, NW+2 lists, basis rows
     lp.m_tile_h = 16;
