@@ -369,6 +369,70 @@ __global__ void __launch_bounds__(512) k_vpath(Dev d, const int32_t* vhistT, int
         }
     };
     if (regs && D1 > 1) load_col(1);
+    // integral lambda_y (default 30): the energies are integers, exact in
+    // double, so the DP runs on int keys 8 E + o whose minimum is the smallest
+    // energy and, among ties, the first offset in scan order (strict '<',
+    // dp.hpp:43-51); rows past H hold sentinels instead of a bound test
+    const bool use_int = regs && d.lambda_y == floor(d.lambda_y) && d.lambda_y <= 1e4 &&
+                         (double)d.W * (double)D1 + 7e4 * (double)D1 < 1e8;
+    if (use_int) {
+        int* pi = reinterpret_cast<int*>(prev);
+        int* ci = reinterpret_cast<int*>(cur);
+        int ik[7];
+#pragma unroll
+        for (int o = 0; o < 7; ++o) ik[o] = (int)pen[o] * 8 + o;
+        __syncthreads();  // prev's doubles read above
+        for (int s = threadIdx.x; s < H + 7; s += blockDim.x) {
+            pi[s] = s < H ? -hT[(size_t)d.d_max * H + s] * 8 : (1 << 30);
+            if (s >= H) ci[s] = 1 << 30;
+        }
+        __syncthreads();
+        for (int st = 1; st < D1; ++st) {
+            int ccur[VP_MAXS];
+#pragma unroll
+            for (int k = 0; k < VP_MAXS; ++k) ccur[k] = cnext[k];
+            if (st + 1 < D1) load_col(st + 1);
+            int8_t* chr = choice + (size_t)st * H;
+#pragma unroll
+            for (int k = 0; k < VP_MAXS; ++k) {
+                const int s = threadIdx.x + k * blockDim.x;
+                if (s >= H) break;
+                int best = pi[s] + ik[0];
+#pragma unroll
+                for (int o = 1; o < 7; ++o) best = min(best, pi[s + o] + ik[o]);
+                ci[s] = (best & ~7) - ccur[k] * 8;
+                chr[s] = (int8_t)(best & 7);
+            }
+            __syncthreads();
+            int* t = pi;
+            pi = ci;
+            ci = t;
+        }
+        int mvi = 0x7fffffff, mi = 0x7fffffff;
+        for (int s = threadIdx.x; s < H; s += blockDim.x)
+            if (pi[s] < mvi) {  // (pi >> 3 ordered like pi: the low bits hold no offset at the end)
+                mvi = pi[s];
+                mi = s;
+            }
+        const int term = block_argmin((double)(mvi >> 3), mi, sv, si);
+        if (threadIdx.x == 0) {
+            int32_t* pts = d.vpath + (size_t)f * D1 * 2;
+            int p = term;
+            pts[(D1 - 1) * 2] = d.d_max - (D1 - 1);
+            pts[(D1 - 1) * 2 + 1] = p;
+            for (int st = D1 - 1; st > 0; --st) {
+                p += choice[(size_t)st * H + p];
+                pts[(st - 1) * 2] = d.d_max - (st - 1);
+                pts[(st - 1) * 2 + 1] = p;
+            }
+            lk_frame_report& rep = d.rep[f];
+            rep.vpath_energy = (double)(pi[term] >> 3);
+            const bool ev = d.aux[f].hist_total > 0;
+            rep.vpath_has_evidence = ev;
+            if (!ev) fail_frame(d, f, 6, LK_MSG_NO_ROAD_EVIDENCE);  // pipeline.hpp:189-190
+        }
+        return;
+    }
     for (int st = 1; st < D1; ++st) {
         const int32_t* col = hT + (size_t)(d.d_max - st) * H;
         int ccur[VP_MAXS];
