@@ -2230,10 +2230,19 @@ __device__ void select_certificate(const Dev& d, int f, const double* h, double 
     const int sep = d.min_lane_sep;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         if (!((cbits[i >> 5] >> (i & 31)) & 1) || !touch[i]) continue;
-        for (int j = max(0, i - sep + 1); j <= min(n - 1, i + sep - 1); ++j)
-            if (j != i && ((cbits[j >> 5] >> (j & 31)) & 1) &&
-                fabs(h[i] - h[j]) <= eh + (touch[j] ? eh : 0.0))
-                unc += j > i || !touch[j];  // each touched pair once
+        // the certain candidates j within min_sep: set bits of the window's words
+        const int lo = max(0, i - sep + 1), hi = min(n - 1, i + sep - 1);
+        for (int w = lo >> 5; w <= (hi >> 5); ++w) {
+            unsigned int bits = cbits[w];
+            if (w == (lo >> 5)) bits &= ~0u << (lo & 31);
+            if (w == (hi >> 5)) bits &= ~0u >> (31 - (hi & 31));
+            while (bits) {
+                const int j = 32 * w + __ffs(bits) - 1;
+                bits &= bits - 1;
+                if (j != i && fabs(h[i] - h[j]) <= eh + (touch[j] ? eh : 0.0))
+                    unc += j > i || !touch[j];  // each touched pair once
+            }
+        }
     }
     for (int o = 16; o; o >>= 1) unc += __shfl_xor_sync(0xffffffffu, unc, o);
     if ((threadIdx.x & 31) == 0 && unc) atomicAdd(&s_unc, unc);
@@ -2308,36 +2317,59 @@ __global__ void __launch_bounds__(256) k_select(Dev d, int sort_cap) {
     const int nwords = (n + 31) >> 5;
     for (int i = threadIdx.x; i < nwords; i += blockDim.x) kbits[i] = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+        // warp 0 walks the candidates in order; the first 128 kept columns sit
+        // in registers (4 per lane), so "some kept k with |i - k| < min_sep"
+        // is one ballot instead of a scan of the bitmap words (which still
+        // records every kept column and takes over beyond 128)
+        const int lane = threadIdx.x;
+        constexpr int KR = 4;
+        int kc[KR];
+#pragma unroll
+        for (int r = 0; r < KR; ++r) kc[r] = INT_MIN / 2;
         int kept = 0;
         const int sep = d.min_lane_sep;
         for (int q = 0; q < m; ++q) {
             const int i = cols[q];
             bool close = false;
             if (sep > 0) {
-                const int lo = max(0, i - sep + 1), hi = min(n - 1, i + sep - 1);
-                for (int w = lo >> 5; w <= (hi >> 5) && !close; ++w) {
-                    unsigned int bits = kbits[w];
-                    if (w == (lo >> 5)) bits &= ~0u << (lo & 31);
-                    if (w == (hi >> 5)) bits &= ~0u >> (31 - (hi & 31));
-                    close = bits != 0;
+                bool near = false;
+#pragma unroll
+                for (int r = 0; r < KR; ++r) near |= abs(i - kc[r]) < sep;
+                close = __any_sync(0xffffffffu, near);
+                if (!close && kept > 32 * KR) {  // kept columns beyond the registers
+                    const int lo = max(0, i - sep + 1), hi = min(n - 1, i + sep - 1);
+                    for (int w = lo >> 5; w <= (hi >> 5) && !close; ++w) {
+                        unsigned int bits = kbits[w];
+                        if (w == (lo >> 5)) bits &= ~0u << (lo & 31);
+                        if (w == (hi >> 5)) bits &= ~0u >> (31 - (hi & 31));
+                        close = bits != 0;
+                    }
                 }
             }
             if (close) continue;
-            kbits[i >> 5] |= 1u << (i & 31);
-            if (kept < d.lane_cap) {
+            if (lane == 0) kbits[i >> 5] |= 1u << (i & 31);
+            if (kept < 32 * KR && lane == (kept & 31)) {
+#pragma unroll
+                for (int r = 0; r < KR; ++r)
+                    if (r == (kept >> 5)) kc[r] = i;
+            }
+            if (lane == 0 && kept < d.lane_cap) {
                 lanes[kept].bottom_col = d.ext_lo + i;
                 lanes[kept].energy = h[i];
                 lanes[kept].n_points = 0;
             }
             ++kept;
+            __syncwarp();  // lane 0's bitmap word before the next candidate's scan
         }
+        if (lane == 0) {
         s_kept = kept;
         lk_frame_report& rep = d.rep[f];
         rep.lane_count = kept;
         for (int k = 0; k < kept && k < LK_MAX_INLINE_LANES; ++k) {
             rep.lane_bottom_col[k] = lanes[k].bottom_col;
             rep.lane_energy[k] = lanes[k].energy;
+        }
         }
     }
     __syncthreads();
