@@ -189,7 +189,7 @@ __device__ __forceinline__ void ldlt_solve(const double (&A)[N][N], const int (&
 // Normal equations (A, b) -> model, exactly as fit_parabola_lsq / fit_quartic
 // finish: solve, one refinement pass for the quartic, rescale by s^k.
 template <int K>
-__device__ __noinline__ void solve_model(const double (&A)[K][K], const double (&b)[K], double s,
+__device__ __forceinline__ void solve_model(const double (&A)[K][K], const double (&b)[K], double s,
                                             double* model) {
     double L[K][K], x[K];
     int t[K];
