@@ -91,6 +91,16 @@ __device__ __forceinline__ void xchg(T& a, T& b) {
     b = t;
 }
 
+// x mod d for a 64-bit x and 0 < d < 2^16 (a RANSAC index range) exactly, in
+// three 32-bit steps (16 bits of x at a time) instead of the 64-bit division
+// routine: ((x_hi mod d) 2^16 + x[31:16]) mod d, then the same with x[15:0].
+__device__ __forceinline__ unsigned mod64_small(unsigned long long x, unsigned d) {
+    const unsigned hi = (unsigned)(x >> 32), lo = (unsigned)x;
+    unsigned r = hi % d;
+    r = ((r << 16) | (lo >> 16)) % d;
+    return ((r << 16) | (lo & 0xffffu)) % d;
+}
+
 // ---- LDLT (Appendix B) in registers, row-major N x N, lower triangle used.
 template <int N>
 __device__ __forceinline__ void ldlt_factor(double (&A)[N][N], int (&t)[N]) {
@@ -405,7 +415,7 @@ __device__ void block_ransac(const int* px, const int* pv, int n, double tol, do
                 const uint64_t* r = rng + (size_t)it * K;
 #pragma unroll
                 for (int i = 0; i < K; ++i) {
-                    const int j = i + (int)(r[i] % (uint64_t)(msz - i));
+                    const int j = i + (int)mod64_small(r[i], (unsigned)(msz - i));
                     int vi = i, vj = j;
                     for (int q = 0; q < no; ++q) {
                         if (opos[q] == i) vi = oval[q];
