@@ -58,3 +58,22 @@ def test_energy_track_llround_via_half_add():
         # C llround (half away from zero) on -0.5 < u: 0 for negatives, else floor + (frac >= 0.5)
         exact = 0 if u < 0 else math.floor(u) + (1 if u - math.floor(u) >= 0.5 else 0)
         assert fast(u) == exact, u
+
+
+def test_mod64_small_identity():
+    """lk_fit.cuh mod64_small: x mod d (x 64-bit, 0 < d < 2^16, the RANSAC draw
+    rng() % (m.size() - i), ransac.hpp:58-64) as three 32-bit modulos over 16-bit
+    slices of x. Exhaustive over the edge cases, random elsewhere."""
+    import random
+
+    def mod64_small(x, d):
+        hi, lo = x >> 32, x & 0xFFFFFFFF
+        r = hi % d
+        r = ((r << 16) | (lo >> 16)) % d
+        return ((r << 16) | (lo & 0xFFFF)) % d
+
+    rng = random.Random(3)
+    edges = [0, 1, 2**16 - 1, 2**32 - 1, 2**32, 2**48 - 1, 2**63, 2**64 - 1]
+    for d in list(range(1, 300)) + [2**15, 2**16 - 1, 40000]:
+        for x in edges + [rng.getrandbits(64) for _ in range(50)]:
+            assert mod64_small(x, d) == x % d
