@@ -560,7 +560,8 @@ lk_status lk_create(lk_ctx** out, int device, const lk_config* cfg, int width, i
         if (nt == 1024 && sp < 5) sp = 5;
         lp.upath_sp = sp > 8 ? 0 : sp;
     }
-    lp.gamma_smem = (size_t)(GAMMA_NW + 4) * H * 4 + 8 + (size_t)6 * H * 8 + 16;  // px, pv, NW+2 lists, basis rows
+    lp.gamma_smem = (size_t)(GAMMA_NW + 4) * H * 4 + 8 + (size_t)6 * H * 8 + 16 +  // px, pv, NW+2 lists, basis rows
+                    (size_t)kMaxIter * 5 * 8;                                     // + the staged draws
     lp.m_tile_h = 16;
     auto m_bytes = [&](int th) {
         const size_t GH = th + 2 + 2 * cfg->varsigma, GW = lkg::M_TW + 2 + 2 * cfg->nu;

@@ -1520,6 +1520,10 @@ __global__ void __launch_bounds__(32 * GAMMA_NW, 2) k_gamma_fit(Dev d) {
     int* bufs[NW + 2];
     for (int b = 0; b < NW + 2; ++b) bufs[b] = pv + H + b * H;
     double* tbuf = align8(pv + H + (NW + 2) * H);
+    // the draws of every iteration staged on chip (a round's first load is
+    // then a shared-memory read, not an L2 round trip)
+    uint64_t* s_rng = reinterpret_cast<uint64_t*>(tbuf + 6 * H);
+    for (int i = threadIdx.x; i < d.max_iter * 5; i += blockDim.x) s_rng[i] = d.rng[i];
     __shared__ RansacState st;
     const int32_t* up = d.upath + (size_t)f * H * 2;
     for (int i = threadIdx.x; i < nrows; i += blockDim.x) {
@@ -1532,7 +1536,7 @@ __global__ void __launch_bounds__(32 * GAMMA_NW, 2) k_gamma_fit(Dev d) {
 #ifdef LK_GAMMA_PROF
     const long long t0 = clock64();
 #endif
-    block_ransac<5, NW>(px, pv, nrows, d.tr_x, d.eps_x, d.max_iter, d.rng, bufs, tbuf, st);
+    block_ransac<5, NW>(px, pv, nrows, d.tr_x, d.eps_x, d.max_iter, s_rng, bufs, tbuf, st);
 #ifdef LK_GAMMA_PROF
     const long long t1 = clock64();
 #endif
