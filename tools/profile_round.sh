@@ -31,6 +31,8 @@ for k in ${KERNELS:-k_prescreen k_bilateral_need k_vanish k_energy k_refine_exac
         > "$OUT/ncu_${k}.log" 2>&1
     python tools/ncu_summary.py "$OUT/${k}_full.ncu-rep" > "$OUT/${k}_ncu.txt" 2>&1
     python tools/ncu_lines.py "$OUT/${k}_full.ncu-rep" "$k" 25 > "$OUT/${k}_lines.txt" 2>&1
+    # the summaries are what is kept; the reports would exceed gpurun's 64 MiB copy-back
+    [ -n "${KEEP_REPS:-}" ] || rm -f "$OUT/${k}_full.ncu-rep"
 done
 python tools/fraction_table.py "$OUT"/k_*_ncu.txt > "$OUT/fractions.md" 2>&1
 echo done
