@@ -21,8 +21,9 @@ namespace lkg {
 // results of steps t-1 and t-2, fetched by shuffle. Lane 0 reads them from
 // the previous group's last row. The recurrence and its rounding are the
 // reference's, element for element.
+constexpr int IR = 64;  // k_integral output ring: columns per row kept on chip
 __global__ void __launch_bounds__(128) k_integral(Dev d) {
-    extern __shared__ double sh_int[];  // [4 warps][W] last row of the previous group
+    extern __shared__ double sh_int[];  // [4 warps][W] last row of the previous group, then rings
     __shared__ double s_val[256];
     const int f = blockIdx.x;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) s_val[i] = d.val[i];
@@ -33,6 +34,20 @@ __global__ void __launch_bounds__(128) k_integral(Dev d) {
     const uint8_t* img = (warp >= 2 ? d.right : d.grey) + (size_t)f * d.px;
     double* out = d.sat + ((size_t)f * 4 + warp) * d.px;
     double* last = sh_int + (size_t)warp * W;  // row 32g - 1, kept on chip for lane 0
+    // the group's results go through a [32 rows][IR columns] ring and leave in
+    // row segments of 32 columns (one coalesced 256-byte store per row)
+    // instead of 32 one-lane-per-row stores per step
+    double* ring = sh_int + (size_t)4 * W + (size_t)warp * 32 * IR;
+    auto flush = [&](int g, int c0) {  // columns c0 .. c0 + 31 (complete) of rows 32g ..
+        __syncwarp();
+        const int u = c0 + lane;
+        if (u < W)
+            for (int r = 0; r < 32; ++r) {
+                const int vr = g * 32 + r;
+                if (vr < H) out[(size_t)vr * W + u] = ring[r * IR + (u & (IR - 1))];
+            }
+        __syncwarp();
+    };
     for (int g = 0; g * 32 < H; ++g) {
         __syncwarp();  // lane 31's writes of the previous group are visible to lane 0
         const int v = g * 32 + lane;
@@ -72,16 +87,22 @@ __global__ void __launch_bounds__(128) k_integral(Dev d) {
                     double x = s_val[kb_cur[j]];
                     if (sq) x = x * x;
                     val = ((up + mine1) - diag) + x;  // mine1 = in(u-1, v)
-                    out[(size_t)v * W + u] = val;
+                    ring[lane * IR + (u & (IR - 1))] = val;
                 }
                 mine2 = mine1;
                 mine1 = val;
                 // lane 31 hands its row to the next group's lane 0 (read after __syncwarp)
                 if (lane == 31 && act) last[u] = val;
+                // column c is complete at step c + 31: columns [t - 62, t - 30) leave
+                // before lane 0 reuses their slots (step t - 62 + IR)
+                if (t >= 62 && ((t - 62) & 31) == 0) flush(g, t - 62);
             }
 #pragma unroll
             for (int j = 0; j < PB; ++j) kb_cur[j] = kb_nxt[j];
         }
+        // the blocks the steps did not reach (every column is complete now)
+        const int tl = ((W + 31 + PB - 1) / PB) * PB - 1;  // the last step run
+        for (int c0 = tl >= 62 ? ((tl - 62) / 32 + 1) * 32 : 0; c0 < W; c0 += 32) flush(g, c0);
     }
 }
 
@@ -407,7 +428,7 @@ __global__ void __launch_bounds__(256) k_lrc(Dev d) {
     }
 }
 
-size_t integral_smem(const Dev& d) { return (size_t)4 * d.W * 8; }
+size_t integral_smem(const Dev& d) { return (size_t)4 * d.W * 8 + (size_t)4 * 32 * IR * 8; }
 
 size_t stereo_smem(const Dev& d) {
     const size_t wp = (size_t)((d.W + 16 + 3) & ~3);
