@@ -2091,6 +2091,8 @@ __device__ __forceinline__ double track_step(const double4 rw, int v, double u) 
     return a / rw.z;
 }
 
+// LG1: lambda_g == 1 (the default, config.hpp:38): c + 1.0 * e is c + e exactly
+template <bool LG1>
 __global__ void __launch_bounds__(128) k_energy(Dev d) {
     extern __shared__ double4 sh_e4[];  // per row v: (vpx[v+1], vpy[v+1], denom, 1/denom)
     __shared__ int s_dead;
@@ -2159,7 +2161,7 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
         }
 #pragma unroll
         for (int k = 0; k < EC; ++k)
-            if (vc - k >= v_alive) e = c[k] + lg * e;
+            if (vc - k >= v_alive) e = LG1 ? c[k] + e : c[k] + lg * e;
     }
     // rows after the track stops contribute +0.0 (kept: 0 + (-0.0) is +0.0)
     for (int v = v_alive - 1; v >= v_top; --v) e = 0.0 + lg * e;
@@ -2508,7 +2510,11 @@ cudaError_t launch_pipeline(const Dev& d, const LaunchPlan& lp, int n, cudaStrea
         k_p99_collect<<<dim3(lp.collect_blocks, n), 256, 0, s>>>(d);
         k_p99_select<<<n, 256, 0, s>>>(d);
     }
-    k_energy<<<dim3((d.ext_cols + 127) / 128, n), 128,
+    if (d.lambda_g == 1.0)
+    k_energy<true><<<dim3((d.ext_cols + 127) / 128, n), 128,
+               (size_t)d.H * sizeof(double4) + (size_t)d.m_nty * d.m_ntx, s>>>(d);
+    else
+    k_energy<false><<<dim3((d.ext_cols + 127) / 128, n), 128,
                (size_t)d.H * sizeof(double4) + (size_t)d.m_nty * d.m_ntx, s>>>(d);
     k_select<<<n, 256, lp.select_smem, s>>>(d, lp.sort_cap);
     k_finish<<<(n + 127) / 128, 128, 0, s>>>(d, n);
